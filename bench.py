@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the B200-native nonsmooth-DEM time step (arXiv 2501.05300).
+
+Contract (see the task README): ``python bench.py --gpus N --steps K --warmup W`` prints ONE
+JSON line on rank 0.  A "step" is one full DEM time step (every SURVEY §8(a) row: detection,
+history carry, SPOOK rows, impact stage when triggered, N_it Jacobi sweeps, integration with
+walls/plates) over the workload bed.  Metric: particle-steps/s (contacts/s reported beside).
+
+Workload (config.workload): BASELINE.json configs[4] "long vehicle-track slab", geom variant
+(8.0 x 1.0 x 0.6 m, three refinement bands r = 2 mm to 0.08 m, 6 mm to 0.25 m, 16 mm below,
++-10 % radius jitter), dt = 5e-6 s, N_it from Eqs. 8 + 10 with eps = 0.02.
+The bed is a jammed FCC packing (nearest-neighbour distance = mean diameter, so about half
+the bonds touch: N_c/N_p ~ 3 like a settled bed), relaxed under gravity for a few coarse
+steps (dt 1e-4, 20 sweeps) before the timed steps; see DESIGN.md §4 for the recipe.
+Inputs are larger than L2 (several GB per sweep) -> no L2 flush is needed between steps.
+
+N > 1: one process per GPU, each rank steps its own replica slab of the same size (weak
+scaling; the x-slab halo exchange is DESIGN.md §8 "next"), time = max over ranks.
+
+--impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+# SURVEY §8(d); bands = (depth_top, depth_bottom, r_nom)
+WORKLOADS = {
+    "config4-geom": dict(dims=(8.0, 1.0, 0.6), bands=[(0.0, 0.08, 2e-3), (0.08, 0.25, 6e-3), (0.25, 0.6, 16e-3)],
+                         dt=5e-6, seed=1004),
+    "config1": dict(dims=(0.4, 0.4, 0.3), bands=[(0.0, 0.06, 2e-3), (0.06, 0.3, 4e-3)], dt=5e-6, seed=1001),
+    "config3-geom": dict(dims=(1.0, 0.5, 0.3), bands=[(0.0, 0.3, 2e-3)], dt=5e-6, seed=1003),
+}
+ALG_B_PARTICLE = 112     # algorithmic bytes per particle per sweep
+ALG_B_CONTACT = 72       # ... per contact per sweep
+
+
+def network_length(bands):
+    """Eq. 10 generalised to discrete bands: particles along the depth = sum thickness / d."""
+    return sum((b - a) / (2 * r) for a, b, r in bands)
+
+
+def make_bed(wl, seed_offset=0, spacing=2.0):
+    w = WORKLOADS[wl]
+    return synth.banded_bed(w["dims"], w["bands"], w["seed"] + seed_offset, spacing=spacing, name=wl)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, idx):
+        self.idx, self.proc, self.path = idx, None, f"/tmp/dem_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        self.proc.wait()
+        rows = [l.split(",") for l in open(self.path).read().strip().splitlines() if l.strip()]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, n in enumerate(names):
+                if r[5 + k].strip() == "Active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def cpu_baseline(wl, n_it, dt, budget_s=15.0):
+    """The fp64 oracle as it stands, single thread, on a bounded sample of the workload: a
+    full-depth column of the bed (all bands), stepped once with the workload's N_it."""
+    import oracle as O
+    w = WORKLOADS[wl]
+    dims = w["dims"]
+    col = (0.06, 0.06, dims[2])
+    b = synth.banded_bed(col, w["bands"], w["seed"] + 77, spacing=2.0)
+    Wd = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi))
+    p = O.make_params(h=dt, n_it=n_it)
+    t0 = time.perf_counter()
+    steps = 0
+    while True:
+        c, _, _ = Wd.step(p)
+        steps += 1
+        if time.perf_counter() - t0 > budget_s or steps >= 3:
+            break
+    dt_s = time.perf_counter() - t0
+    return {"value": b.n * steps / dt_s, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+            "sample": f"{b.n}-particle full-depth column (0.06 x 0.06 x {dims[2]} m, all bands) of {wl}, "
+                      f"{steps} step(s), N_it={n_it}, brute-force detection, {len(c)} contacts"}
+
+
+def run_reference(args, rank, world):
+    wl = args.workload
+    w = WORKLOADS[wl]
+    n_it = args.n_it or int(np.ceil(0.1 * network_length(w["bands"]) / 0.02 - 1e-9))
+    if rank != 0:
+        return
+    import oracle as O
+    dims = w["dims"]
+    b = synth.banded_bed((0.05, 0.05, dims[2]), w["bands"], w["seed"] + 99, spacing=2.0)
+    Wd = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi))
+    p = O.make_params(h=w["dt"], n_it=n_it)
+    for _ in range(args.warmup):
+        Wd.step(p)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        Wd.step(p)
+    T = time.perf_counter() - t0
+    val = b.n * args.steps / T
+    sample = (f"{b.n}-particle full-depth column (0.05 x 0.05 x {dims[2]} m) of {wl}; each step is one full "
+              f"oracle step (brute-force detection, N_it={n_it} Jacobi sweeps)")
+    print(json.dumps({
+        "impl": "reference", "metric": "particle-steps/s", "value": val, "unit": "particle-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl + " (oracle sample)", "n_particles": b.n, "n_it": n_it, "dt": w["dt"]},
+        "cpu_baseline": {"value": val, "unit": "particle-steps/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="config4-geom", choices=sorted(WORKLOADS))
+    ap.add_argument("--n-it", type=int, default=0)
+    ap.add_argument("--settle", type=int, default=20)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no baseline, no clocks")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2501_05300_b200 import dem
+
+    wl = args.workload
+    w = WORKLOADS[wl]
+    n_it = args.n_it or dem.plan_iterations(network_length(w["bands"]), 0.02)
+    bed_in = make_bed(wl, seed_offset=rank)
+    bed = dem.Bed(bed_in.x, bed_in.r, bed_in.v, bed_in.w, bed_in.gid, device=local,
+                  solver=dict(dt=1e-4, n_iter=20), box=dict(lo=bed_in.box_lo, hi=bed_in.box_hi))
+    if args.settle > 0:
+        bed.step(args.settle)             # coarse relaxation of the jammed packing (not timed)
+    bed.set_solver(dt=w["dt"], n_iter=n_it)
+    for _ in range(args.warmup):
+        bed.step(1)
+    stream = bed.stream
+    bed.set_timing(True)
+    bed.reset_timing()
+    clocks = ClockSampler(local)
+    if not args.profile:
+        clocks.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    reps = []
+    for _ in range(args.steps):
+        reps.append(bed.step(1))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    ck = clocks.stop() if not args.profile else None
+    tm = bed.timing()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    N = bed_in.n
+    nc_mean = float(np.mean([r["n_contacts"] for r in reps]))
+    imp_rate = float(np.mean([r["impact_fired"] for r in reps]))
+    value = world * N * args.steps / (ms / 1e3)
+    contacts_per_s = world * nc_mean * args.steps / (ms / 1e3)
+    sweep_ms = tm["ms_sweeps"] / max(tm["n_sweep_launches"], 1)
+    alg_bytes = ALG_B_PARTICLE * N + ALG_B_CONTACT * nc_mean
+    pk = peaks()
+    hbm = pk.get("hbm_gbs")
+    achieved = alg_bytes / (sweep_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "sweep_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(wl)
+        except Exception:
+            traffic = None
+    out = {
+        "metric": "particle-steps/s", "value": value, "unit": "particle-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl, "n_particles": N, "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
+                   "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "levels": len(w["bands"]),
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (no flush needed)",
+                   "precision": "fp64 state and row math; fp64 normals/rows, fp32 impulses"},
+        "contacts_per_s": contacts_per_s,
+        "contact_sweeps_per_s": tm["contact_sweeps"] / (ms / 1e3) * world,
+        "roofline": {"bound": "hbm", "kernel": "k_sweep_tile", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
+                     "alg_bytes_per_launch": alg_bytes, "launch_ms": sweep_ms,
+                     "sweep_share_of_step": tm["ms_sweeps"] / max(tm["ms_total"], 1e-9),
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+        "gpu_launches": int(tm["n_kernel_launches"]),
+        "phase_ms_per_step": {k: tm[k] / args.steps for k in ("ms_rebuild", "ms_detect", "ms_sweeps", "ms_integrate")},
+    }
+    if ck:
+        out["clocks"] = ck
+    # e2e through the public API: per step H2D the drive inputs (wall velocities) and D2H the
+    # whole particle state (a trajectory frame) into pinned host memory.
+    if not args.no_e2e and not args.profile:
+        pin = {k: torch.empty((N, 3), dtype=torch.float64, pin_memory=True) for k in ("pos", "vel", "angvel")}
+        dev = {k: torch.empty((N, 3), dtype=torch.float64, device="cuda") for k in ("pos", "vel", "angvel")}
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for wall in (0, 1, 2, 3):
+                bed.drive_wall(wall, 0.0)            # H2D: boundary drive inputs
+            bed.step(1)
+            bed.get_state_device(dev)
+            with torch.cuda.stream(stream):
+                for k in pin:
+                    pin[k].copy_(dev[k], non_blocking=True)
+            stream.synchronize()
+        T = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([T], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            T = float(t.item())
+        out["e2e"] = {"value": world * N * args.steps / T, "unit": "particle-steps/s",
+                      "h2d_bytes_per_step": 4 * 5336, "d2h_bytes_per_step": 72 * N,
+                      "what": "per step: wall-drive inputs H2D, full particle state (pos, vel, angvel) D2H to pinned host"}
+    if rank == 0 and not args.no_cpu_baseline and not args.profile:
+        out["cpu_baseline"] = cpu_baseline(wl, n_it, w["dt"])
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    bed.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

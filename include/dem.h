@@ -1,0 +1,240 @@
+/*
+ * dem.h -- C-ABI of the B200-native nonsmooth-DEM time step (libdem.so).
+ *
+ * The library implements one time step of the discrete element method of
+ * Pogulis & Servin, "Local particle refinement in terramechanical simulations"
+ * (arXiv 2501.05300; /root/reference/PAPER.md, cited "P:line"): a bed of spheres whose size
+ * grows with depth (Eq. 1), stepped by the time-implicit (nonsmooth) DEM of
+ * contact detection every step, Hertz-mapped SPOOK normal rows
+ * (P:127-129), Coulomb and rolling-resistance cones, a Newton
+ * impact stage, and a warm-started projected iterative solve run here as a
+ * deterministic Jacobi sweep on the GPU.  Readings of silent/garbled passages: DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - SI units, z up, gravity is a solver parameter (default (0,0,-9.81)); "depth" = z_top - z.
+ *  - All state is double precision (fp64 x, v, w); contact normals and row constants are
+ *    stored in fp64, impulses in fp32, and all contact-row arithmetic is fp64.
+ *  - Particles are identified by a caller-chosen unique gid (uint32 < 2^32-4096).  Every
+ *    getter returns particles in ascending gid order and contacts in ascending key order.
+ *  - A contact key is (key_a << 32) | key_b with key_a = the smaller gid of the pair and
+ *    key_b = the other gid, or 2^32-16+w for box wall w, or 2^32-4096+16p+b for box b of
+ *    plate p.  The normal points from body a to body b; P = (P_n, P_t[3], P_r[3]) in N s is
+ *    the impulse body b receives (body a receives the opposite).
+ *  - Ownership: the context owns all device memory (allocated through dem_dist_desc.alloc
+ *    when given, else cudaMalloc).  No caller pointer is retained after a call returns.
+ *    Buffers passed to getters/setters are host memory unless the view's on_device is 1.
+ *  - Errors: every call returns a dem_status; DEM_ERR_INVALID leaves the context unchanged;
+ *    dem_last_error() returns a human-readable reason.  A step that produces NaN/Inf returns
+ *    DEM_ERR_DIVERGED and restores the state of the beginning of that step (S:385 atomicity).
+ *  - Concurrency: one host thread per context; contexts on different devices are independent.
+ *  - Determinism: for identical inputs the results are bit-identical run to run (no float
+ *    atomics anywhere; all reductions are in a fixed order or in int64 fixed point).
+ */
+#ifndef DEM_H
+#define DEM_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct dem_ctx dem_ctx;
+
+typedef enum {
+    DEM_OK = 0,
+    DEM_ERR_INVALID = 2,   /* bad argument or descriptor; nothing changed */
+    DEM_ERR_DIVERGED = 3,  /* NaN/Inf in the step; state rolled back to the step start */
+    DEM_ERR_STATE = 4,     /* call out of order (e.g. forces before any step) */
+    DEM_ERR_CUDA = 5,      /* CUDA runtime error (message in dem_last_error) */
+    DEM_ERR_NCCL = 6,      /* reserved: multi-GPU communicator error */
+    DEM_ERR_OOM = 7        /* device allocation failed */
+} dem_status;
+
+/* Particle material (BASELINE configs: rho 2600, E 10 MPa, nu .3, mu .4/.1, e .5). */
+typedef struct {
+    double density, youngs, poisson;   /* E* = E/(2(1-nu^2)) for identical materials */
+    double mu_t, mu_r;                 /* Coulomb |P_t| <= mu_t P_n; rolling |P_r| <= mu_r R* P_n */
+    double restitution;                /* Newton impact law coefficient */
+} dem_material;
+
+/* Solver settings. */
+typedef struct {
+    double dt;                 /* time step h > 0 */
+    int32_t n_iter;            /* Jacobi sweeps per step, >= 1 (Eq. 8 via dem_plan_iterations) */
+    int32_t n_iter_impact;     /* impact-stage sweeps; <= 0 -> n_iter */
+    double hertz_exp;          /* e_H: 1.25 (Hertz) or 1.0 (linear model) */
+    double k_lin;              /* linear stiffness [N/m], required iff hertz_exp == 1 */
+    double damping_steps;      /* SPOOK damping time tau = damping_steps * dt (4.5) */
+    double v_impact;           /* impact threshold [m/s]; < 0 -> 20 |g| dt; >= 1e30 off */
+    double gravity[3];
+    int32_t rolling_dims;      /* 3: rolling row on the full relative spin (default); 2: tangential */
+    int32_t pad0;
+    double skin;               /* Verlet skin [m] of the candidate list; <= 0 -> 0.1 r_min */
+} dem_solver;
+
+/* Container: axis-aligned box; wall w = 2*axis + side (0:-x 1:+x 2:-y 3:+y 4:-z 5:+z). */
+typedef struct {
+    double lo[3], hi[3];
+    uint32_t wall_mask;        /* bit w set -> wall w present */
+    uint32_t pad0;
+    double wall_mu_t, wall_mu_r;   /* walls are frictionless in the paper */
+} dem_box;
+
+/* Particle arrays, caller order (host unless on_device). */
+typedef struct {
+    int64_t n;
+    const double *pos;         /* 3n */
+    const double *radius;      /* n, > 0 */
+    const double *vel;         /* 3n or NULL (zero) */
+    const double *angvel;      /* 3n or NULL (zero) */
+    const uint32_t *gid;       /* n unique, < 2^32-4096, or NULL (0..n-1) */
+    int32_t on_device;
+    int32_t pad0;
+} dem_particles;
+
+typedef struct {
+    size_t struct_size;        /* sizeof(dem_bed_desc): ABI version check */
+    dem_material mat;
+    dem_solver solver;
+    dem_box box;
+    dem_particles parts;
+} dem_bed_desc;
+
+/* Process / device plumbing (PyTorch provides memory, stream and process group). */
+typedef struct {
+    int32_t rank, world_size;  /* world_size must be 1 in this release (x-slab DD: DESIGN.md §8) */
+    const void *nccl_unique_id;        /* reserved, NULL */
+    void *cuda_stream;                 /* cudaStream_t all work is issued on; NULL -> own stream */
+    void *(*alloc)(size_t bytes, void *alloc_ctx);   /* NULL -> cudaMalloc */
+    void (*free)(void *ptr, void *alloc_ctx);
+    void *alloc_ctx;
+} dem_dist_desc;
+
+typedef struct {
+    int64_t step;              /* steps taken since create */
+    double time;
+    int64_t n_contacts, n_pp, n_wall, n_plate, n_degenerate, n_candidates;
+    int32_t impact_fired;      /* 1 if the Newton impact stage ran in this step */
+    int32_t rebuilt;           /* 1 if the sort/grid/candidate list was rebuilt before this step */
+    double ke;                 /* kinetic energy after the step [J] */
+    double max_v;              /* max |v| after the step */
+    double max_disp;           /* max displacement since the last rebuild [m] */
+    int32_t n_iter, n_iter_impact;
+} dem_step_report;
+
+/* State exchange, ascending gid order; n = capacity in, count out. */
+typedef struct {
+    int64_t n;
+    double *pos;               /* 3n */
+    double *vel;               /* 3n */
+    double *angvel;            /* 3n */
+    double *radius;            /* n */
+    uint32_t *gid;             /* n */
+    int32_t on_device;
+    int32_t pad0;
+} dem_state_view;
+
+typedef struct {
+    int64_t n;                 /* capacity in, count out */
+    uint64_t *key;             /* n, ascending */
+    double *normal;            /* 3n (may be NULL for input) */
+    double *delta;             /* n  (may be NULL for input) */
+    double *P;                 /* 7n: P_n, P_t[3], P_r[3] */
+    int32_t on_device;
+    int32_t pad0;
+} dem_contact_view;
+
+typedef enum { DEM_AXIS_LOCKED = 0, DEM_AXIS_VELOCITY = 1, DEM_AXIS_FORCE = 2 } dem_axis_mode;
+
+/* Rigid plate = union of <= 8 axis-aligned boxes (base + grousers), translation only. */
+typedef struct {
+    int32_t n_boxes, pad0;
+    const double *lo, *hi;     /* 3*n_boxes corners relative to the plate position */
+    double mass;               /* used by force-driven axes */
+    double mu_t, mu_r;         /* plate-particle coefficients (same as inter-particle) */
+} dem_plate_desc;
+
+typedef struct {
+    double pos[3], vel[3];
+    double force[3];           /* contact reaction on the plate during the last step [N] */
+    int64_t n_contacts;
+} dem_plate_state;
+
+typedef struct {
+    double ms_total;           /* device time of the timed phases since reset [ms] */
+    double ms_detect;          /* narrow phase + compaction + incidence + rows */
+    double ms_rebuild;         /* keys, sort, grid, broad phase, history carry */
+    double ms_sweeps;          /* all Jacobi sweeps (main + impact) */
+    double ms_integrate;
+    int64_t n_sweep_launches;
+    int64_t n_kernel_launches; /* every kernel this library launched */
+    int64_t contact_sweeps;    /* sum over sweeps of the contact count */
+    int64_t particle_sweeps;   /* sum over sweeps of the particle count */
+} dem_timing;
+
+/* Create a bed from particle arrays (P:155-161 beds are produced by synth/ generators).
+ * Validates (DEM_ERR_INVALID): struct_size, material > 0, 0 <= nu < .5, dt > 0, n_iter >= 1,
+ * radius > 0, unique gids, box lo < hi, world_size == 1.  Builds the first candidate list. */
+dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, dem_ctx **out);
+
+/* Advance n_steps >= 1 time steps.  `last` (may be NULL) gets the report of the
+ * final step.  Synchronises the host once per step (impact/rebuild decisions). */
+dem_status dem_step(dem_ctx *ctx, int32_t n_steps, dem_step_report *last);
+
+/* Replace the solver settings (same validation as create), e.g. a coarse dt and few sweeps
+ * for relaxing a generated bed before the production settings.  Takes effect at the
+ * next step; the Verlet skin is kept. */
+dem_status dem_set_solver(dem_ctx *ctx, const dem_solver *solver);
+
+/* Copy particle state out (gid order).  view->n must be >= particle count. */
+dem_status dem_get_state(dem_ctx *ctx, dem_state_view *view);
+
+/* Replace particle state (same gid set and radii as at create) and the contact history used
+ * as warm start of the next step (hist may be NULL: no history).  Triggers a rebuild. */
+dem_status dem_set_state(dem_ctx *ctx, const dem_state_view *state, const dem_contact_view *hist);
+
+/* Contacts of the last step with final impulses, key order.  DEM_ERR_STATE before any step;
+ * DEM_ERR_INVALID with view->n = required count if the capacity is too small. */
+dem_status dem_get_contacts(dem_ctx *ctx, dem_contact_view *view);
+
+/* Per-particle contact force F = sum(+-P_lin)/h and torque T (gid order, 3n each) of the last
+ * step (O6).  on_device selects device or host buffers. */
+dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device);
+
+/* Plates: add (all axes locked), drive one axis, read state. */
+dem_status dem_add_plate(dem_ctx *ctx, const dem_plate_desc *desc, const double pos[3], int32_t *plate_id);
+dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mode,
+                           double target /* m/s or N */, double ramp_time /* s, velocity mode */);
+dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *out);
+
+/* Kinematic box wall: velocity along its inward normal (shear-box / servo walls). */
+dem_status dem_drive_wall(dem_ctx *ctx, int32_t wall, double normal_velocity);
+
+/* Device-time accounting of the library's own kernels (CUDA events on the ctx stream). */
+dem_status dem_set_timing(dem_ctx *ctx, int32_t enable);
+dem_status dem_get_timing(dem_ctx *ctx, dem_timing *out);
+dem_status dem_reset_timing(dem_ctx *ctx);
+
+/* The cudaStream_t the context issues its work on. */
+void *dem_stream(dem_ctx *ctx);
+
+dem_status dem_destroy(dem_ctx *ctx);
+
+/* Last error message of ctx (ctx == NULL: of the last failed create on this thread). */
+const char *dem_last_error(const dem_ctx *ctx);
+
+/* ---- host-only planner helpers, pure functions ---- */
+/* Eq. 1: d(z) = d_min + gamma z for z < z_max = (d_max - d_min)/gamma, else d_max. */
+double dem_profile_diameter(double d_min, double d_max, double gamma, double depth);
+/* Eq. 10: n_d = eta ln(d_max/d_min)/ln r + (h - z_max)/d_max, gamma = (r-1)/(r eta); h/d if uniform. */
+double dem_contact_network_length(double d_min, double d_max, double r, double eta, double h);
+/* Eq. 8: N_it = ceil(0.1 n_d / eps), at least 1. */
+int32_t dem_plan_iterations(double n_d, double eps);
+/* Eq. 9: dt = 0.5 sqrt(eps d / a), a = 3 sigma/(2 rho d). */
+double dem_plan_timestep(double d, double eps, double rho, double sigma);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,987 @@
+// ctx.cu -- host runtime of libdem.so: the dem_ctx (device buffers, stream, rebuild policy,
+// step orchestration) and the C-ABI of include/dem.h.
+//
+// One step:
+//   [rebuild if the Verlet skin is used up]  keys -> radix sort -> permute -> per-level cell
+//                                            tables -> multi-level broad phase -> transposed
+//                                            lists -> history carry by sorted key
+//   narrow phase (exact fp64 predicate) -> scan -> compaction + warm start -> incidence CSR
+//   -> mass-splitting weights -> impact trigger -> [impact stage: N_imp Jacobi sweeps]
+//   -> SPOOK rows -> gravity + warm start -> N_it Jacobi sweeps -> integrate -> plates/walls
+//   -> rollback on NaN -> history scatter to the candidate slots
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/dem.h"
+#include "common.cuh"
+#include "kernels.h"
+
+static thread_local std::string g_create_err;
+
+struct dem_ctx {
+    dem_material mat{};
+    dem_solver sol{};
+    dem_box box{};
+    cudaStream_t s = nullptr;
+    bool own_stream = false;
+    void *(*ualloc)(size_t, void *) = nullptr;
+    void (*ufree)(void *, void *) = nullptr;
+    void *actx = nullptr;
+    std::string err;
+    std::vector<void *> allocs;
+
+    int64_t N = 0;
+    GridParams grid{};
+    SolveParams sp{};
+    int nlev = 1;
+    double rmax_lv[DEM_MAX_LEVELS] = {0};
+    bool lv_present[DEM_MAX_LEVELS] = {false};
+
+    // particles (sorted order)
+    double4 *pos = nullptr, *pos2 = nullptr, *vel[2] = {nullptr, nullptr}, *ang[2] = {nullptr, nullptr};
+    double4 *vel2 = nullptr, *ang2 = nullptr, *xref = nullptr, *pos_prev = nullptr, *vel_prev = nullptr,
+            *ang_prev = nullptr;
+    uint32_t *gid = nullptr, *gid2 = nullptr, *gid_sorted = nullptr;
+    int cur = 0;
+    // sort / scan scratch
+    int64_t cap_keys = 0;
+    uint64_t *keys[2] = {nullptr, nullptr};
+    uint32_t *vals[2] = {nullptr, nullptr};
+    void *sort_tmp = nullptr;
+    void *scan_tmp = nullptr;
+    double *ke_part = nullptr;
+    unsigned long long *lvbox = nullptr;   // per level: min xyz, max xyz (ordered bits), count
+    // cells
+    uint64_t ncells = 0, cap_cells = 0;
+    uint32_t *cstart = nullptr, *cend = nullptr;
+    // candidates
+    int64_t ncand = 0, cap_cand = 0;
+    uint2 *cand = nullptr;
+    uint32_t *co_start = nullptr, *ct_cnt = nullptr, *ct_start = nullptr, *ct_cursor = nullptr, *ct_list = nullptr;
+    P4 *Pca = nullptr, *Pcb = nullptr;
+    uint32_t *cflag = nullptr, *cscan = nullptr;
+    // contacts
+    int64_t nc = 0;
+    uint2 *cij = nullptr;
+    G4 *geo = nullptr;
+    R4 *row = nullptr, *row_imp = nullptr;
+    double *cdel = nullptr;
+    P4 *Pwa = nullptr, *Pwb = nullptr;            // warm start
+    P4 *Pa[2] = {nullptr, nullptr}, *Pb[2] = {nullptr, nullptr};
+    P4 *Pfa = nullptr, *Pfb = nullptr;            // final impulses of the last step
+    uint32_t *ccand = nullptr;
+    // incidence
+    uint32_t *inc_cnt = nullptr, *inc_start = nullptr;
+    uint2 *inc = nullptr;
+    // history
+    int64_t nh = 0, cap_h = 0;
+    uint64_t *hkey = nullptr;
+    P4 *hPa = nullptr, *hPb = nullptr;
+    bool hist_pending = false;
+    // boundary
+    DevBoundary hb{};
+    DevBoundary *db = nullptr;
+    unsigned long long *pacc = nullptr;
+    unsigned int *pcount = nullptr;
+    StepScalars *dsc = nullptr, *hsc = nullptr;
+    uint32_t *hnc = nullptr;
+    // status
+    int64_t step = 0;
+    bool need_rebuild = true;
+    bool have_step = false;
+    dem_step_report last{};
+    // timing
+    bool timing = false;
+    cudaEvent_t ev[8] = {};
+    dem_timing tm{};
+    long long launches = 0;
+};
+
+// ------------------------------------------------------------------ helpers
+#define CK(call)                                                                      \
+    do {                                                                              \
+        cudaError_t e_ = (call);                                                      \
+        if (e_ != cudaSuccess) {                                                      \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);            \
+            return DEM_ERR_CUDA;                                                      \
+        }                                                                             \
+    } while (0)
+#define TRY(x)                         \
+    do {                               \
+        dem_status st_ = (x);          \
+        if (st_ != DEM_OK) return st_; \
+    } while (0)
+
+static dem_status dalloc(dem_ctx *ctx, void **p, size_t bytes)
+{
+    bytes = std::max<size_t>(bytes, 256);
+    bytes = (bytes + 255) & ~(size_t)255;
+    void *q = nullptr;
+    if (ctx->ualloc) q = ctx->ualloc(bytes, ctx->actx);
+    else if (cudaMalloc(&q, bytes) != cudaSuccess) q = nullptr;
+    if (!q) {
+        cudaGetLastError();
+        ctx->err = "device allocation of " + std::to_string(bytes) + " bytes failed";
+        return DEM_ERR_OOM;
+    }
+    ctx->allocs.push_back(q);
+    *p = q;
+    return DEM_OK;
+}
+static void dfree(dem_ctx *ctx, void *p)
+{
+    if (!p) return;
+    auto it = std::find(ctx->allocs.begin(), ctx->allocs.end(), p);
+    if (it != ctx->allocs.end()) ctx->allocs.erase(it);
+    if (ctx->ufree) ctx->ufree(p, ctx->actx);
+    else cudaFree(p);
+}
+template <class T>
+static dem_status A(dem_ctx *ctx, T **p, size_t n)
+{
+    void *q = nullptr;
+    TRY(dalloc(ctx, &q, n * sizeof(T)));
+    *p = (T *)q;
+    return DEM_OK;
+}
+template <class T>
+static dem_status regrow(dem_ctx *ctx, T **p, size_t n)
+{
+    dfree(ctx, *p);
+    *p = nullptr;
+    return A(ctx, p, n);
+}
+
+static void tstart(dem_ctx *ctx, int k)
+{
+    if (ctx->timing) cudaEventRecord(ctx->ev[k], ctx->s);
+}
+static float telapsed(dem_ctx *ctx, int a, int b)
+{
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev[a], ctx->ev[b]);
+    return ms;
+}
+
+// ------------------------------------------------------------------ validation and setup
+static bool valid_material(const dem_material &m)
+{
+    return m.density > 0 && m.youngs > 0 && m.poisson >= 0 && m.poisson < 0.5 && m.mu_t >= 0 && m.mu_r >= 0 &&
+           m.restitution >= 0 && m.restitution <= 1;
+}
+
+static void setup_solve_params(dem_ctx *ctx)
+{
+    SolveParams &sp = ctx->sp;
+    const dem_solver &so = ctx->sol;
+    sp.h = so.dt;
+    sp.Ups = 1.0 / (1.0 + 4.0 * so.damping_steps);
+    sp.e_H = so.hertz_exp;
+    sp.k_lin = so.k_lin;
+    sp.Es = 1.0 / (2.0 * (1.0 - ctx->mat.poisson * ctx->mat.poisson) / ctx->mat.youngs);
+    sp.rho = ctx->mat.density;
+    sp.mu_t = ctx->mat.mu_t;
+    sp.mu_r = ctx->mat.mu_r;
+    sp.e_rest = ctx->mat.restitution;
+    const double gn = std::sqrt(so.gravity[0] * so.gravity[0] + so.gravity[1] * so.gravity[1] + so.gravity[2] * so.gravity[2]);
+    sp.v_imp = so.v_impact < 0 ? 20.0 * gn * so.dt : so.v_impact;
+    for (int k = 0; k < 3; k++) sp.g[k] = so.gravity[k];
+    sp.rolling_dims = so.rolling_dims == 2 ? 2 : 3;
+    sp.hertz = so.hertz_exp == 1.0 ? 0 : 1;
+}
+
+// radii -> levels (factor-2 size classes), per-level r_max, skin
+static void setup_levels(dem_ctx *ctx, const std::vector<double> &r)
+{
+    double rmin = INFINITY, rmax = 0;
+    for (double x : r) { rmin = std::min(rmin, x); rmax = std::max(rmax, x); }
+    if (r.empty()) { rmin = 1e-3; rmax = 1e-3; }
+    int nlev = 1;
+    double t = rmin;
+    while (nlev < DEM_MAX_LEVELS && rmax >= t * 2.0) { t *= 2.0; nlev++; }
+    ctx->nlev = nlev;
+    for (int L = 0; L < DEM_MAX_LEVELS; L++) { ctx->rmax_lv[L] = 0; ctx->lv_present[L] = false; }
+    for (double x : r) {
+        int L = level_of(x, rmin, nlev);
+        ctx->rmax_lv[L] = std::max(ctx->rmax_lv[L], x);
+        ctx->lv_present[L] = true;
+    }
+    ctx->grid.nlev = nlev;
+    ctx->grid.rmin = rmin;
+    ctx->grid.skin = ctx->sol.skin > 0 ? ctx->sol.skin : 0.1 * rmin;
+}
+
+static void setup_walls(dem_ctx *ctx)
+{
+    DevBoundary &b = ctx->hb;
+    for (int w = 0; w < 6; w++) {
+        const int ax = w / 2, side = w % 2;
+        for (int k = 0; k < 3; k++) { b.wp[w][k] = 0; b.wn[w][k] = 0; }
+        b.wp[w][ax] = side == 0 ? ctx->box.lo[ax] : ctx->box.hi[ax];
+        b.wn[w][ax] = side == 0 ? 1.0 : -1.0;
+        b.wvel[w] = 0;
+        b.wpresent[w] = (ctx->box.wall_mask >> w) & 1;
+        for (int k = 0; k < 3; k++) b.wp_ref[w][k] = b.wp[w][k];
+    }
+    b.wall_mu_t = ctx->box.wall_mu_t;
+    b.wall_mu_r = ctx->box.wall_mu_r;
+}
+
+static dem_status upload_boundary(dem_ctx *ctx)
+{
+    CK(cudaMemcpyAsync(ctx->db, &ctx->hb, sizeof(DevBoundary), cudaMemcpyHostToDevice, ctx->s));
+    return DEM_OK;
+}
+
+// allocate particle-sized arrays
+static dem_status alloc_particles(dem_ctx *ctx)
+{
+    const size_t N = (size_t)ctx->N + 1;
+    TRY(A(ctx, &ctx->pos, N)); TRY(A(ctx, &ctx->pos2, N));
+    TRY(A(ctx, &ctx->vel[0], N)); TRY(A(ctx, &ctx->vel[1], N));
+    TRY(A(ctx, &ctx->ang[0], N)); TRY(A(ctx, &ctx->ang[1], N));
+    TRY(A(ctx, &ctx->vel2, N)); TRY(A(ctx, &ctx->ang2, N));
+    TRY(A(ctx, &ctx->xref, N)); TRY(A(ctx, &ctx->pos_prev, N));
+    TRY(A(ctx, &ctx->vel_prev, N)); TRY(A(ctx, &ctx->ang_prev, N));
+    TRY(A(ctx, &ctx->gid, N)); TRY(A(ctx, &ctx->gid2, N)); TRY(A(ctx, &ctx->gid_sorted, N));
+    TRY(A(ctx, &ctx->co_start, N + 1)); TRY(A(ctx, &ctx->ct_cnt, N + 1)); TRY(A(ctx, &ctx->ct_start, N + 1));
+    TRY(A(ctx, &ctx->ct_cursor, N + 1)); TRY(A(ctx, &ctx->inc_cnt, N + 1)); TRY(A(ctx, &ctx->inc_start, N + 1));
+    TRY(A(ctx, &ctx->ke_part, N / 256 + 2));
+    TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
+    TRY(A(ctx, &ctx->db, 1));
+    TRY(A(ctx, &ctx->pacc, 3 * DEM_MAX_PLATES));
+    TRY(A(ctx, &ctx->pcount, DEM_MAX_PLATES));
+    TRY(A(ctx, &ctx->dsc, 1));
+    return DEM_OK;
+}
+
+static dem_status ensure_keys(dem_ctx *ctx, int64_t n)
+{
+    if (n <= ctx->cap_keys) return DEM_OK;
+    int64_t cap = std::max<int64_t>(n + n / 2, 1024);
+    for (int k = 0; k < 2; k++) { TRY(regrow(ctx, &ctx->keys[k], cap)); TRY(regrow(ctx, &ctx->vals[k], cap)); }
+    void *p = ctx->sort_tmp;
+    dfree(ctx, p);
+    TRY(dalloc(ctx, &ctx->sort_tmp, sort_temp_bytes(cap)));
+    dfree(ctx, ctx->scan_tmp);
+    TRY(dalloc(ctx, &ctx->scan_tmp, scan_temp_bytes(cap + 1) + scan_temp_bytes(2 * cap + 2)));
+    ctx->cap_keys = cap;
+    return DEM_OK;
+}
+
+static dem_status ensure_cand(dem_ctx *ctx, int64_t n)
+{
+    if (n <= ctx->cap_cand) return DEM_OK;
+    int64_t cap = std::max<int64_t>(n + n / 4, 1024);
+    TRY(regrow(ctx, &ctx->cand, cap)); TRY(regrow(ctx, &ctx->ct_list, cap));
+    TRY(regrow(ctx, &ctx->Pca, cap)); TRY(regrow(ctx, &ctx->Pcb, cap));
+    TRY(regrow(ctx, &ctx->cflag, cap + 1)); TRY(regrow(ctx, &ctx->cscan, cap + 1));
+    TRY(regrow(ctx, &ctx->cij, cap)); TRY(regrow(ctx, &ctx->geo, cap)); TRY(regrow(ctx, &ctx->row, cap)); TRY(regrow(ctx, &ctx->cdel, cap));
+    TRY(regrow(ctx, &ctx->row_imp, cap)); TRY(regrow(ctx, &ctx->Pwa, cap)); TRY(regrow(ctx, &ctx->Pwb, cap));
+    for (int k = 0; k < 2; k++) { TRY(regrow(ctx, &ctx->Pa[k], cap)); TRY(regrow(ctx, &ctx->Pb[k], cap)); }
+    TRY(regrow(ctx, &ctx->ccand, cap));
+    TRY(regrow(ctx, &ctx->inc, 2 * cap));
+    ctx->cap_cand = cap;
+    ctx->nc = 0;
+    ctx->have_step = false;
+    return ensure_keys(ctx, std::max<int64_t>(cap, ctx->N));
+}
+
+// ------------------------------------------------------------------ level bounding boxes
+__device__ __forceinline__ unsigned long long ord_bits(double x)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+static double ord_unbits(unsigned long long u)
+{
+    unsigned long long b = (u >> 63) ? (u & 0x7FFFFFFFFFFFFFFFULL) : ~u;
+    double x;
+    std::memcpy(&x, &b, 8);
+    return x;
+}
+__global__ void k_level_bbox(int64_t N, const double4 *__restrict__ pos, double rmin, int nlev,
+                             unsigned long long *__restrict__ box)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double4 p = pos[i];
+    const int L = level_of(p.w, rmin, nlev);
+    unsigned long long *b = box + 8 * L;
+    const double c[3] = {p.x, p.y, p.z};
+    for (int k = 0; k < 3; k++) {
+        atomicMin(&b[k], ord_bits(c[k]));
+        atomicMax(&b[3 + k], ord_bits(c[k]));
+    }
+    atomicAdd(&b[6], 1ULL);
+}
+
+static dem_status compute_grid(dem_ctx *ctx)
+{
+    std::vector<unsigned long long> hb(8 * DEM_MAX_LEVELS);
+    for (int L = 0; L < DEM_MAX_LEVELS; L++) {
+        for (int k = 0; k < 3; k++) { hb[8 * L + k] = ~0ULL; hb[8 * L + 3 + k] = 0ULL; }
+        hb[8 * L + 6] = 0;
+        hb[8 * L + 7] = 0;
+    }
+    CK(cudaMemcpyAsync(ctx->lvbox, hb.data(), hb.size() * 8, cudaMemcpyHostToDevice, ctx->s));
+    if (ctx->N) {
+        k_level_bbox<<<(unsigned)((ctx->N + 255) / 256), 256, 0, ctx->s>>>(ctx->N, ctx->pos, ctx->grid.rmin, ctx->nlev, ctx->lvbox);
+        ctx->launches++;
+    }
+    CK(cudaMemcpyAsync(hb.data(), ctx->lvbox, hb.size() * 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    GridParams &g = ctx->grid;
+    uint64_t off = 0;
+    int bits = 1;
+    for (int L = 0; L < ctx->nlev; L++) {
+        GridLevel &lv = g.lv[L];
+        lv.present = hb[8 * L + 6] > 0;
+        lv.rmax = ctx->rmax_lv[L];
+        lv.cell = 2.0 * lv.rmax + g.skin;
+        if (!lv.present) { lv.nx = lv.ny = lv.nz = 1; lv.offset = off; lv.ox = lv.oy = lv.oz = 0; continue; }
+        double lo[3], hi[3];
+        for (int k = 0; k < 3; k++) { lo[k] = ord_unbits(hb[8 * L + k]); hi[k] = ord_unbits(hb[8 * L + 3 + k]); }
+        // coarser-level queries come from finer particles anywhere: extend by the global box
+        for (int k = 0; k < 3; k++) {
+            if (!std::isfinite(lo[k]) || !std::isfinite(hi[k])) { ctx->err = "non-finite particle position"; return DEM_ERR_DIVERGED; }
+        }
+        int n[3];
+        double o[3];
+        for (int k = 0; k < 3; k++) {
+            o[k] = lo[k] - lv.cell;
+            double ext = (hi[k] - lo[k]) + 2.0 * lv.cell;
+            long long nn = (long long)std::ceil(ext / lv.cell) + 1;
+            nn = std::max<long long>(1, std::min<long long>(nn, 1 << 20));
+            n[k] = (int)nn;
+        }
+        lv.ox = o[0]; lv.oy = o[1]; lv.oz = o[2];
+        lv.nx = n[0]; lv.ny = n[1]; lv.nz = n[2];
+        lv.offset = off;
+        off += (uint64_t)n[0] * n[1] * n[2];
+        for (int k = 0; k < 3; k++) while ((1 << bits) < n[k]) bits++;
+    }
+    for (int L = ctx->nlev; L < DEM_MAX_LEVELS; L++) g.lv[L].present = 0;
+    g.bits = bits;
+    ctx->ncells = off;
+    if (off > ctx->cap_cells) {
+        uint64_t cap = off + off / 4 + 64;
+        TRY(regrow(ctx, &ctx->cstart, cap));
+        TRY(regrow(ctx, &ctx->cend, cap));
+        ctx->cap_cells = cap;
+    }
+    return DEM_OK;
+}
+
+// ------------------------------------------------------------------ rebuild
+static dem_status export_history(dem_ctx *ctx)
+{
+    const int64_t nc = ctx->ncand;
+    cudaStream_t s = ctx->s;
+    ctx->nh = 0;
+    if (!nc) return DEM_OK;
+    launch_hist_flag(nc, ctx->Pca, ctx->Pcb, ctx->cflag, s);
+    scan_u32(ctx->cflag, ctx->cscan, nc, ctx->scan_tmp, s, &ctx->launches);
+    uint32_t nh = 0;
+    CK(cudaMemcpyAsync(&nh, ctx->cscan + nc, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    ctx->launches += 1;
+    if (nh > ctx->cap_h) {
+        int64_t cap = nh + nh / 4 + 1024;
+        TRY(regrow(ctx, &ctx->hkey, cap)); TRY(regrow(ctx, &ctx->hPa, cap)); TRY(regrow(ctx, &ctx->hPb, cap));
+        ctx->cap_h = cap;
+    }
+    if (nh) {
+        launch_hist_keys(nc, ctx->cflag, ctx->cscan, ctx->cand, ctx->gid, ctx->keys[0], ctx->vals[0], s);
+        radix_sort_u64(ctx->keys, ctx->vals, nh, 64, ctx->sort_tmp, s, &ctx->launches);
+        CK(cudaMemcpyAsync(ctx->hkey, ctx->keys[0], nh * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+        launch_hist_gather(nh, ctx->vals[0], ctx->cand, ctx->gid, ctx->Pca, ctx->Pcb, ctx->hPa, ctx->hPb, s);
+        ctx->launches += 2;
+    }
+    ctx->nh = nh;
+    return DEM_OK;
+}
+
+static dem_status rebuild(dem_ctx *ctx)
+{
+    cudaStream_t s = ctx->s;
+    const int64_t N = ctx->N;
+    if (!ctx->hist_pending) TRY(export_history(ctx));
+    ctx->hist_pending = false;
+    TRY(ensure_keys(ctx, std::max<int64_t>(N, 1)));
+    TRY(compute_grid(ctx));
+    // (a) level + Morton keys, stable radix sort, permutation of the SoA state
+    if (N) {
+        launch_keys(N, ctx->pos, ctx->grid, ctx->keys[0], ctx->vals[0], s);
+        int nbits = 3 * ctx->grid.bits + 3;
+        radix_sort_u64(ctx->keys, ctx->vals, N, nbits, ctx->sort_tmp, s, &ctx->launches);
+        launch_permute(N, ctx->vals[0], ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->gid, ctx->pos2, ctx->vel2,
+                       ctx->ang2, ctx->gid2, s);
+        std::swap(ctx->pos, ctx->pos2);
+        std::swap(ctx->vel[ctx->cur], ctx->vel2);
+        std::swap(ctx->ang[ctx->cur], ctx->ang2);
+        std::swap(ctx->gid, ctx->gid2);
+        ctx->launches += 2;
+        // (b) per-level dense cell tables
+        CK(cudaMemsetAsync(ctx->cstart, 0, ctx->ncells * sizeof(uint32_t), s));
+        CK(cudaMemsetAsync(ctx->cend, 0, ctx->ncells * sizeof(uint32_t), s));
+        launch_cells(N, ctx->keys[0], ctx->grid, ctx->cstart, ctx->cend, s);
+        // multi-level broad phase: count, scan, fill
+        launch_broad(false, N, ctx->pos, ctx->grid, ctx->cstart, ctx->cend, ctx->db, ctx->co_start, nullptr, s);
+        ctx->launches += 2;
+    }
+    scan_u32(ctx->co_start, ctx->co_start, N, ctx->scan_tmp, s, &ctx->launches);
+    uint32_t ncand = 0;
+    CK(cudaMemcpyAsync(&ncand, ctx->co_start + N, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    TRY(ensure_cand(ctx, std::max<int64_t>(ncand, 1)));
+    ctx->ncand = ncand;
+    if (N) {
+        launch_broad(true, N, ctx->pos, ctx->grid, ctx->cstart, ctx->cend, ctx->db, ctx->co_start, ctx->cand, s);
+        ctx->launches++;
+    }
+    launch_trans(N, ncand, ctx->cand, ctx->ct_cnt, ctx->ct_start, ctx->ct_cursor, ctx->ct_list, ctx->scan_tmp, s,
+                 &ctx->launches);
+    // (c) history carried across the rebuild by sorted-key lookup
+    launch_hist_carry(ncand, ctx->cand, ctx->gid, ctx->hkey, ctx->hPa, ctx->hPb, ctx->nh, ctx->Pca, ctx->Pcb, s);
+    ctx->launches++;
+    if (N) CK(cudaMemcpyAsync(ctx->xref, ctx->pos, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+    // boundary references (device copy is authoritative; hb mirrors it after every step)
+    for (int w = 0; w < 6; w++) for (int k = 0; k < 3; k++) ctx->hb.wp_ref[w][k] = ctx->hb.wp[w][k];
+    for (int q = 0; q < DEM_MAX_PLATES; q++) for (int k = 0; k < 3; k++) ctx->hb.ppos_ref[q][k] = ctx->hb.ppos[q][k];
+    TRY(upload_boundary(ctx));
+    ctx->need_rebuild = false;
+    CK(cudaGetLastError());
+    return DEM_OK;
+}
+
+// ------------------------------------------------------------------ one step
+static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
+{
+    cudaStream_t s = ctx->s;
+    const int64_t N = ctx->N;
+    const SolveParams &sp = ctx->sp;
+    std::memset(rep, 0, sizeof(*rep));
+    tstart(ctx, 0);
+    if (ctx->need_rebuild) {
+        TRY(rebuild(ctx));
+        rep->rebuilt = 1;
+    }
+    tstart(ctx, 1);
+    const DevBoundary hb_prev = ctx->hb;
+    if (N) {
+        CK(cudaMemcpyAsync(ctx->pos_prev, ctx->pos, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->vel_prev, ctx->vel[ctx->cur], N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->ang_prev, ctx->ang[ctx->cur], N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaMemsetAsync(ctx->dsc, 0, sizeof(StepScalars), s));
+    // narrow phase (exact predicate), compaction, incidence
+    const int64_t ncand = ctx->ncand;
+    launch_narrow(ncand, ctx->cand, ctx->pos, ctx->db, ctx->cflag, ctx->Pca, ctx->Pcb, ctx->dsc, s);
+    scan_u32(ctx->cflag, ctx->cscan, ncand, ctx->scan_tmp, s, &ctx->launches);
+    uint32_t nc = 0;
+    CK(cudaMemcpyAsync(ctx->hnc, ctx->cscan + ncand, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    nc = *ctx->hnc;
+    ctx->nc = nc;
+    launch_compact(ncand, ctx->cand, ctx->cflag, ctx->cscan, ctx->pos, ctx->db, sp, ctx->Pca, ctx->Pcb, ctx->cij,
+                   ctx->geo, ctx->row, ctx->cdel, ctx->Pwa, ctx->Pwb, ctx->ccand, ctx->dsc, s);
+    launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->inc_cnt,
+               ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
+    launch_prepare(N, ctx->inc_start, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], sp.rho, s);
+    // impact trigger
+    launch_rows(nc, 0, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
+    ctx->launches += 4;
+    CK(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(StepScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const bool impact = ctx->hsc->impact != 0 && nc > 0;
+    tstart(ctx, 2);
+    const int n_imp = ctx->sol.n_iter_impact > 0 ? ctx->sol.n_iter_impact : ctx->sol.n_iter;
+    if (impact) {
+        // Newton impact stage from P = 0 with Sigma = 0 (reading R13); impulses discarded
+        CK(cudaMemsetAsync(ctx->Pa[0], 0, nc * sizeof(P4), s));
+        CK(cudaMemsetAsync(ctx->Pb[0], 0, nc * sizeof(P4), s));
+        for (int it = 0; it < n_imp; it++) {
+            const int pi = it & 1;
+            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
+                         ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row_imp, ctx->Pa[pi],
+                         ctx->Pb[pi], ctx->Pa[pi ^ 1], ctx->Pb[pi ^ 1], ctx->db, sp, s);
+            ctx->cur ^= 1;
+        }
+        ctx->launches += n_imp;
+        ctx->tm.n_sweep_launches += n_imp;
+        ctx->tm.contact_sweeps += (int64_t)n_imp * nc;
+        ctx->tm.particle_sweeps += (int64_t)n_imp * N;
+    }
+    // main stage: SPOOK rows, gravity + warm start, N_it Jacobi sweeps
+    launch_rows(nc, 1, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
+    launch_sweep(SWEEP_MODE_APPLY, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
+                 ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, nullptr,
+                 nullptr, ctx->db, sp, s);
+    ctx->cur ^= 1;
+    ctx->launches += 2;
+    tstart(ctx, 3);
+    const int n_it = ctx->sol.n_iter;
+    const P4 *pin_a = ctx->Pwa, *pin_b = ctx->Pwb;
+    for (int it = 0; it < n_it; it++) {
+        P4 *oa = ctx->Pa[it & 1], *ob = ctx->Pb[it & 1];
+        launch_sweep(SWEEP_MODE_SWEEP, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
+                     ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
+                     ctx->db, sp, s);
+        ctx->cur ^= 1;
+        pin_a = oa;
+        pin_b = ob;
+    }
+    ctx->launches += n_it;
+    ctx->tm.n_sweep_launches += n_it;
+    ctx->tm.contact_sweeps += (int64_t)n_it * nc;
+    ctx->tm.particle_sweeps += (int64_t)n_it * N;
+    tstart(ctx, 4);
+    ctx->Pfa = (P4 *)pin_a;
+    ctx->Pfb = (P4 *)pin_b;
+    // integrate, plates and walls
+    launch_integrate(N, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->xref, sp.h, sp.rho, ctx->ke_part, ctx->dsc, s);
+    launch_plates(nc, ctx->cij, ctx->geo, ctx->Pfa, ctx->pacc, ctx->pcount, ctx->db, sp.h, ctx->dsc, s);
+    ctx->launches += (N ? 2 : 0) + (nc ? 2 : 1);
+    CK(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(StepScalars), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ctx->hb, ctx->db, sizeof(DevBoundary), cudaMemcpyDeviceToHost, s));
+    tstart(ctx, 5);
+    CK(cudaStreamSynchronize(s));
+    CK(cudaGetLastError());
+    const StepScalars sc = *ctx->hsc;
+    if (sc.nan_flag) {
+        // atomic step: restore the state of the step start
+        if (N) {
+            CK(cudaMemcpyAsync(ctx->pos, ctx->pos_prev, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(ctx->vel[ctx->cur], ctx->vel_prev, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(ctx->ang[ctx->cur], ctx->ang_prev, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+        }
+        ctx->hb = hb_prev;
+        TRY(upload_boundary(ctx));
+        CK(cudaStreamSynchronize(s));
+        ctx->have_step = false;
+        ctx->err = "step " + std::to_string(ctx->step) + " diverged (NaN/Inf); state rolled back";
+        return DEM_ERR_DIVERGED;
+    }
+    launch_scatter_P(nc, ctx->ccand, ctx->Pfa, ctx->Pfb, ctx->Pca, ctx->Pcb, s);
+    ctx->launches += nc ? 1 : 0;
+    if (ctx->timing) {
+        ctx->tm.ms_rebuild += telapsed(ctx, 0, 1);
+        ctx->tm.ms_detect += telapsed(ctx, 1, 2);
+        ctx->tm.ms_sweeps += telapsed(ctx, 2, 4) ;
+        ctx->tm.ms_integrate += telapsed(ctx, 4, 5);
+        ctx->tm.ms_total += telapsed(ctx, 0, 5);
+    }
+    double maxd, maxv;
+    {
+        unsigned long long b = sc.max_disp_bits;
+        std::memcpy(&maxd, &b, 8);
+        b = sc.max_v_bits;
+        std::memcpy(&maxv, &b, 8);
+    }
+    ctx->step++;
+    rep->step = ctx->step;
+    rep->time = ctx->hb.time;
+    rep->n_contacts = nc;
+    rep->n_pp = sc.n_pp;
+    rep->n_wall = sc.n_wall;
+    rep->n_plate = sc.n_plate;
+    rep->n_degenerate = sc.n_degenerate;
+    rep->n_candidates = ncand;
+    rep->impact_fired = impact ? 1 : 0;
+    rep->ke = sc.ke;
+    rep->max_v = maxv;
+    rep->max_disp = maxd;
+    rep->n_iter = n_it;
+    rep->n_iter_impact = impact ? n_imp : 0;
+    const double skin = ctx->grid.skin;
+    ctx->need_rebuild = (2.0 * maxd >= 0.9 * skin) || (maxd + sc.bnd_disp >= 0.9 * skin);
+    ctx->have_step = true;
+    ctx->last = *rep;
+    return DEM_OK;
+}
+
+// ------------------------------------------------------------------ state loading
+static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, const double *rad, const double *vel,
+                                 const double *ang, const uint32_t *gid, int on_device, bool first)
+{
+    // validate on the host
+    std::vector<double> r(n), x(3 * n);
+    std::vector<uint32_t> g(n);
+    cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
+    if (n) {
+        CK(cudaMemcpy(r.data(), rad, n * 8, kind));
+        CK(cudaMemcpy(x.data(), pos, 3 * n * 8, kind));
+        if (gid) CK(cudaMemcpy(g.data(), gid, n * 4, kind));
+        else for (int64_t i = 0; i < n; i++) g[i] = (uint32_t)i;
+    }
+    for (int64_t i = 0; i < n; i++) {
+        if (!(r[i] > 0) || !std::isfinite(r[i])) { ctx->err = "radius must be positive and finite"; return DEM_ERR_INVALID; }
+        for (int k = 0; k < 3; k++) if (!std::isfinite(x[3 * i + k])) { ctx->err = "non-finite position"; return DEM_ERR_INVALID; }
+        if (g[i] >= PLATE_KEY_BASE) { ctx->err = "gid must be < 2^32-4096"; return DEM_ERR_INVALID; }
+    }
+    std::vector<uint32_t> gs(g);
+    std::sort(gs.begin(), gs.end());
+    for (int64_t i = 1; i < n; i++) if (gs[i] == gs[i - 1]) { ctx->err = "duplicate gid"; return DEM_ERR_INVALID; }
+    if (first) {
+        ctx->N = n;
+        TRY(alloc_particles(ctx));
+    } else if (n != ctx->N) {
+        ctx->err = "set_state: particle count differs from create";
+        return DEM_ERR_INVALID;
+    }
+    setup_levels(ctx, r);
+    // stage host copies into device buffers, then convert to the internal layout
+    double *dx = nullptr, *dr = nullptr, *dv = nullptr, *dw = nullptr;
+    uint32_t *dg = nullptr;
+    if (n) {
+        TRY(A(ctx, &dx, 3 * n)); TRY(A(ctx, &dr, n)); TRY(A(ctx, &dg, n));
+        if (vel) TRY(A(ctx, &dv, 3 * n));
+        if (ang) TRY(A(ctx, &dw, 3 * n));
+        cudaMemcpyKind k2 = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+        CK(cudaMemcpyAsync(dx, pos, 3 * n * 8, k2, ctx->s));
+        CK(cudaMemcpyAsync(dr, rad, n * 8, k2, ctx->s));
+        CK(cudaMemcpyAsync(dg, g.data(), n * 4, cudaMemcpyHostToDevice, ctx->s));
+        if (vel) CK(cudaMemcpyAsync(dv, vel, 3 * n * 8, k2, ctx->s));
+        if (ang) CK(cudaMemcpyAsync(dw, ang, 3 * n * 8, k2, ctx->s));
+        ctx->cur = 0;
+        launch_load_state(n, dx, dr, dv, dw, dg, ctx->pos, ctx->vel[0], ctx->ang[0], ctx->gid, ctx->s);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(ctx->gid_sorted, gs.data(), n * 4, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        dfree(ctx, dx); dfree(ctx, dr); dfree(ctx, dg); dfree(ctx, dv); dfree(ctx, dw);
+    }
+    ctx->need_rebuild = true;
+    ctx->have_step = false;
+    return DEM_OK;
+}
+
+// ------------------------------------------------------------------ C-ABI
+extern "C" {
+
+dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, dem_ctx **out)
+{
+    if (!desc || !out) { g_create_err = "null descriptor"; return DEM_ERR_INVALID; }
+    *out = nullptr;
+    if (desc->struct_size != sizeof(dem_bed_desc)) { g_create_err = "dem_bed_desc struct_size mismatch"; return DEM_ERR_INVALID; }
+    if (!valid_material(desc->mat)) { g_create_err = "invalid material"; return DEM_ERR_INVALID; }
+    const dem_solver &so = desc->solver;
+    if (!(so.dt > 0) || so.n_iter < 1 || !(so.hertz_exp == 1.25 || so.hertz_exp == 1.0) ||
+        (so.hertz_exp == 1.0 && !(so.k_lin > 0)) || so.damping_steps < 0) {
+        g_create_err = "invalid solver settings (dt > 0, n_iter >= 1, hertz_exp 1.25 or 1 with k_lin > 0)";
+        return DEM_ERR_INVALID;
+    }
+    for (int k = 0; k < 3; k++)
+        if (!(desc->box.lo[k] < desc->box.hi[k])) { g_create_err = "box lo must be < hi"; return DEM_ERR_INVALID; }
+    if (desc->parts.n < 0 || (desc->parts.n > 0 && (!desc->parts.pos || !desc->parts.radius))) {
+        g_create_err = "particle arrays missing";
+        return DEM_ERR_INVALID;
+    }
+    if (desc->parts.n >= (int64_t)0x7FFFFFFF) { g_create_err = "too many particles for one context"; return DEM_ERR_INVALID; }
+    if (dist && dist->world_size > 1) {
+        g_create_err = "world_size > 1: x-slab decomposition is not available in this release";
+        return DEM_ERR_INVALID;
+    }
+    dem_ctx *ctx = new dem_ctx();
+    ctx->mat = desc->mat;
+    ctx->sol = desc->solver;
+    ctx->box = desc->box;
+    if (dist && dist->cuda_stream) ctx->s = (cudaStream_t)dist->cuda_stream;
+    else {
+        if (cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking) != cudaSuccess) {
+            g_create_err = "cudaStreamCreate failed (no CUDA device?)";
+            delete ctx;
+            return DEM_ERR_CUDA;
+        }
+        ctx->own_stream = true;
+    }
+    if (dist && dist->alloc && dist->free) { ctx->ualloc = dist->alloc; ctx->ufree = dist->free; ctx->actx = dist->alloc_ctx; }
+    setup_solve_params(ctx);
+    setup_walls(ctx);
+    for (int e = 0; e < 8; e++) cudaEventCreate(&ctx->ev[e]);
+    if (cudaMallocHost(&ctx->hsc, sizeof(StepScalars)) != cudaSuccess ||
+        cudaMallocHost(&ctx->hnc, sizeof(uint32_t)) != cudaSuccess) {
+        g_create_err = "cudaMallocHost failed";
+        dem_destroy(ctx);
+        return DEM_ERR_CUDA;
+    }
+    const dem_particles &p = desc->parts;
+    dem_status st = load_particles(ctx, p.n, p.pos, p.radius, p.vel, p.angvel, p.gid, p.on_device, true);
+    if (st == DEM_OK) st = upload_boundary(ctx);
+    if (st == DEM_OK) st = rebuild(ctx);
+    if (st != DEM_OK) {
+        g_create_err = ctx->err;
+        dem_destroy(ctx);
+        return st;
+    }
+    *out = ctx;
+    return DEM_OK;
+}
+
+dem_status dem_step(dem_ctx *ctx, int32_t n_steps, dem_step_report *last)
+{
+    if (!ctx) return DEM_ERR_INVALID;
+    if (n_steps < 1) { ctx->err = "n_steps must be >= 1"; return DEM_ERR_INVALID; }
+    dem_step_report rep{};
+    for (int32_t k = 0; k < n_steps; k++) TRY(step_once(ctx, &rep));
+    if (last) *last = rep;
+    return DEM_OK;
+}
+
+static bool valid_solver(const dem_solver &so)
+{
+    return so.dt > 0 && so.n_iter >= 1 && (so.hertz_exp == 1.25 || so.hertz_exp == 1.0) &&
+           !(so.hertz_exp == 1.0 && !(so.k_lin > 0)) && so.damping_steps >= 0;
+}
+
+dem_status dem_set_solver(dem_ctx *ctx, const dem_solver *so)
+{
+    if (!ctx || !so) return DEM_ERR_INVALID;
+    if (!valid_solver(*so)) { ctx->err = "invalid solver settings"; return DEM_ERR_INVALID; }
+    const double skin = ctx->grid.skin;
+    ctx->sol = *so;
+    setup_solve_params(ctx);
+    ctx->grid.skin = skin;
+    return DEM_OK;
+}
+
+dem_status dem_get_state(dem_ctx *ctx, dem_state_view *v)
+{
+    if (!ctx || !v) return DEM_ERR_INVALID;
+    if (v->n < ctx->N) { ctx->err = "state view too small"; v->n = ctx->N; return DEM_ERR_INVALID; }
+    const int64_t N = ctx->N;
+    v->n = N;
+    if (!N) return DEM_OK;
+    cudaStream_t s = ctx->s;
+    if (v->on_device) {
+        launch_to_gid_order(N, ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], v->pos,
+                            v->vel, v->angvel, v->radius, v->gid, s);
+        ctx->launches++;
+        CK(cudaStreamSynchronize(s));
+        return DEM_OK;
+    }
+    double *d = nullptr;
+    uint32_t *dg = nullptr;
+    TRY(A(ctx, &d, 10 * N));
+    TRY(A(ctx, &dg, N));
+    launch_to_gid_order(N, ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], d, d + 3 * N,
+                        d + 6 * N, d + 9 * N, dg, s);
+    ctx->launches++;
+    if (v->pos) CK(cudaMemcpyAsync(v->pos, d, 3 * N * 8, cudaMemcpyDeviceToHost, s));
+    if (v->vel) CK(cudaMemcpyAsync(v->vel, d + 3 * N, 3 * N * 8, cudaMemcpyDeviceToHost, s));
+    if (v->angvel) CK(cudaMemcpyAsync(v->angvel, d + 6 * N, 3 * N * 8, cudaMemcpyDeviceToHost, s));
+    if (v->radius) CK(cudaMemcpyAsync(v->radius, d + 9 * N, N * 8, cudaMemcpyDeviceToHost, s));
+    if (v->gid) CK(cudaMemcpyAsync(v->gid, dg, N * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, d);
+    dfree(ctx, dg);
+    return DEM_OK;
+}
+
+dem_status dem_set_state(dem_ctx *ctx, const dem_state_view *st, const dem_contact_view *hist)
+{
+    if (!ctx || !st) return DEM_ERR_INVALID;
+    if (st->n != ctx->N || (st->n && (!st->pos || !st->radius))) { ctx->err = "set_state: bad view"; return DEM_ERR_INVALID; }
+    // history: sorted by key on the host, uploaded for the next rebuild's sorted-key lookup
+    std::vector<uint64_t> hk;
+    std::vector<P4> ha, hbv;
+    if (hist && hist->n > 0) {
+        const int64_t n = hist->n;
+        std::vector<uint64_t> k(n);
+        std::vector<double> P(7 * n);
+        cudaMemcpyKind kind = hist->on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
+        CK(cudaMemcpy(k.data(), hist->key, n * 8, kind));
+        CK(cudaMemcpy(P.data(), hist->P, 7 * n * 8, kind));
+        std::vector<int64_t> ord(n);
+        for (int64_t i = 0; i < n; i++) ord[i] = i;
+        std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) { return k[a] < k[b]; });
+        for (int64_t t = 0; t < n; t++) {
+            const int64_t i = ord[t];
+            if (t && k[i] == hk.back()) { ctx->err = "set_state: duplicate history key"; return DEM_ERR_INVALID; }
+            hk.push_back(k[i]);
+            ha.push_back(mkP4(P[7 * i], P[7 * i + 1], P[7 * i + 2], P[7 * i + 3]));
+            hbv.push_back(mkP4(P[7 * i + 4], P[7 * i + 5], P[7 * i + 6], 0));
+        }
+    }
+    TRY(load_particles(ctx, st->n, st->pos, st->radius, st->vel, st->angvel, st->gid, st->on_device, false));
+    const int64_t nh = (int64_t)hk.size();
+    if (nh > ctx->cap_h) {
+        int64_t cap = nh + 1024;
+        TRY(regrow(ctx, &ctx->hkey, cap)); TRY(regrow(ctx, &ctx->hPa, cap)); TRY(regrow(ctx, &ctx->hPb, cap));
+        ctx->cap_h = cap;
+    }
+    if (nh) {
+        CK(cudaMemcpyAsync(ctx->hkey, hk.data(), nh * 8, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaMemcpyAsync(ctx->hPa, ha.data(), nh * sizeof(P4), cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaMemcpyAsync(ctx->hPb, hbv.data(), nh * sizeof(P4), cudaMemcpyHostToDevice, ctx->s));
+    }
+    ctx->nh = nh;
+    ctx->hist_pending = true;
+    CK(cudaStreamSynchronize(ctx->s));
+    return rebuild(ctx);
+}
+
+dem_status dem_get_contacts(dem_ctx *ctx, dem_contact_view *v)
+{
+    if (!ctx || !v) return DEM_ERR_INVALID;
+    if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
+    const int64_t nc = ctx->nc;
+    if (v->n < nc) { v->n = nc; ctx->err = "contact view too small"; return DEM_ERR_INVALID; }
+    v->n = nc;
+    if (!nc) return DEM_OK;
+    cudaStream_t s = ctx->s;
+    launch_contact_keys(nc, ctx->cij, ctx->gid, ctx->keys[0], ctx->vals[0], s);
+    radix_sort_u64(ctx->keys, ctx->vals, nc, 64, ctx->sort_tmp, s, &ctx->launches);
+    double *d = nullptr;
+    TRY(A(ctx, &d, 11 * nc));
+    launch_contact_out(nc, ctx->vals[0], ctx->cij, ctx->gid, ctx->geo, ctx->cdel, ctx->Pfa, ctx->Pfb, d, d + 3 * nc, d + 4 * nc, s);
+    ctx->launches += 2;
+    cudaMemcpyKind k = v->on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (v->key) CK(cudaMemcpyAsync(v->key, ctx->keys[0], nc * 8, k, s));
+    if (v->normal) CK(cudaMemcpyAsync(v->normal, d, 3 * nc * 8, k, s));
+    if (v->delta) CK(cudaMemcpyAsync(v->delta, d + 3 * nc, nc * 8, k, s));
+    if (v->P) CK(cudaMemcpyAsync(v->P, d + 4 * nc, 7 * nc * 8, k, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, d);
+    return DEM_OK;
+}
+
+dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device)
+{
+    if (!ctx) return DEM_ERR_INVALID;
+    if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
+    const int64_t N = ctx->N;
+    if (!N) return DEM_OK;
+    cudaStream_t s = ctx->s;
+    launch_sweep(SWEEP_MODE_FORCES, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
+                 ctx->inc, ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, nullptr, nullptr, ctx->db, ctx->sp, s);
+    double *d = nullptr;
+    TRY(A(ctx, &d, 6 * N));
+    launch_to_gid_order(N, ctx->gid, ctx->gid_sorted, ctx->vel2, ctx->ang2, nullptr, d, d + 3 * N, nullptr, nullptr,
+                        nullptr, s);
+    ctx->launches += 2;
+    cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    if (F) CK(cudaMemcpyAsync(F, d, 3 * N * 8, k, s));
+    if (T) CK(cudaMemcpyAsync(T, d + 3 * N, 3 * N * 8, k, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, d);
+    return DEM_OK;
+}
+
+dem_status dem_add_plate(dem_ctx *ctx, const dem_plate_desc *d, const double pos[3], int32_t *plate_id)
+{
+    if (!ctx || !d || !pos) return DEM_ERR_INVALID;
+    DevBoundary &b = ctx->hb;
+    if (b.n_plates >= DEM_MAX_PLATES) { ctx->err = "too many plates (max 8)"; return DEM_ERR_INVALID; }
+    if (d->n_boxes < 1 || d->n_boxes > DEM_MAX_BOXES || !d->lo || !d->hi || !(d->mass > 0) || d->mu_t < 0 || d->mu_r < 0) {
+        ctx->err = "invalid plate descriptor";
+        return DEM_ERR_INVALID;
+    }
+    for (int q = 0; q < d->n_boxes; q++)
+        for (int k = 0; k < 3; k++)
+            if (!(d->lo[3 * q + k] < d->hi[3 * q + k])) { ctx->err = "plate box lo must be < hi"; return DEM_ERR_INVALID; }
+    const int p = b.n_plates;
+    b.nbox[p] = d->n_boxes;
+    for (int q = 0; q < d->n_boxes; q++)
+        for (int k = 0; k < 3; k++) { b.lo[p][q][k] = d->lo[3 * q + k]; b.hi[p][q][k] = d->hi[3 * q + k]; }
+    for (int k = 0; k < 3; k++) {
+        b.ppos[p][k] = pos[k];
+        b.ppos_ref[p][k] = pos[k];
+        b.pvel[p][k] = 0;
+        b.mode[p][k] = DEM_AXIS_LOCKED;
+        b.target[p][k] = 0;
+        b.ramp[p][k] = 0;
+        b.t0[p][k] = 0;
+        b.pforce[p][k] = 0;
+    }
+    b.pmass[p] = d->mass;
+    b.pmu_t[p] = d->mu_t;
+    b.pmu_r[p] = d->mu_r;
+    b.pcount[p] = 0;
+    b.n_plates = p + 1;
+    if (plate_id) *plate_id = p;
+    TRY(upload_boundary(ctx));
+    ctx->need_rebuild = true;
+    return DEM_OK;
+}
+
+dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mode, double target, double ramp_time)
+{
+    if (!ctx) return DEM_ERR_INVALID;
+    DevBoundary &b = ctx->hb;
+    if (plate < 0 || plate >= b.n_plates || axis < 0 || axis > 2 || mode < 0 || mode > 2 || !std::isfinite(target) ||
+        ramp_time < 0) {
+        ctx->err = "invalid plate drive";
+        return DEM_ERR_INVALID;
+    }
+    b.mode[plate][axis] = mode;
+    b.target[plate][axis] = target;
+    b.ramp[plate][axis] = ramp_time;
+    b.t0[plate][axis] = b.time;
+    if (mode == DEM_AXIS_LOCKED) b.pvel[plate][axis] = 0;
+    else if (mode == DEM_AXIS_VELOCITY) b.pvel[plate][axis] = ramp_time > 0 ? 0.0 : target;
+    return upload_boundary(ctx);
+}
+
+dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *o)
+{
+    if (!ctx || !o) return DEM_ERR_INVALID;
+    const DevBoundary &b = ctx->hb;
+    if (plate < 0 || plate >= b.n_plates) { ctx->err = "no such plate"; return DEM_ERR_INVALID; }
+    for (int k = 0; k < 3; k++) { o->pos[k] = b.ppos[plate][k]; o->vel[k] = b.pvel[plate][k]; o->force[k] = b.pforce[plate][k]; }
+    o->n_contacts = b.pcount[plate];
+    return DEM_OK;
+}
+
+dem_status dem_drive_wall(dem_ctx *ctx, int32_t wall, double v)
+{
+    if (!ctx) return DEM_ERR_INVALID;
+    if (wall < 0 || wall > 5 || !ctx->hb.wpresent[wall] || !std::isfinite(v)) { ctx->err = "invalid wall"; return DEM_ERR_INVALID; }
+    ctx->hb.wvel[wall] = v;
+    return upload_boundary(ctx);
+}
+
+dem_status dem_set_timing(dem_ctx *ctx, int32_t enable)
+{
+    if (!ctx) return DEM_ERR_INVALID;
+    ctx->timing = enable != 0;
+    return DEM_OK;
+}
+dem_status dem_get_timing(dem_ctx *ctx, dem_timing *o)
+{
+    if (!ctx || !o) return DEM_ERR_INVALID;
+    *o = ctx->tm;
+    o->n_kernel_launches = ctx->launches;
+    return DEM_OK;
+}
+dem_status dem_reset_timing(dem_ctx *ctx)
+{
+    if (!ctx) return DEM_ERR_INVALID;
+    ctx->tm = dem_timing{};
+    ctx->launches = 0;
+    return DEM_OK;
+}
+
+void *dem_stream(dem_ctx *ctx) { return ctx ? (void *)ctx->s : nullptr; }
+
+dem_status dem_destroy(dem_ctx *ctx)
+{
+    if (!ctx) return DEM_ERR_INVALID;
+    if (ctx->s) cudaStreamSynchronize(ctx->s);
+    std::vector<void *> all = ctx->allocs;
+    for (void *p : all) dfree(ctx, p);
+    for (int e = 0; e < 8; e++) if (ctx->ev[e]) cudaEventDestroy(ctx->ev[e]);
+    if (ctx->hsc) cudaFreeHost(ctx->hsc);
+    if (ctx->hnc) cudaFreeHost(ctx->hnc);
+    if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);
+    delete ctx;
+    return DEM_OK;
+}
+
+const char *dem_last_error(const dem_ctx *ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,54 @@
+// kernels.h -- host launchers of the device kernels (detect.cu, solve.cu); internal to libdem.so.
+#pragma once
+#include "common.cuh"
+
+// detect.cu
+void launch_keys(int64_t N, const double4 *pos, const GridParams &g, uint64_t *keys, uint32_t *vals, cudaStream_t s);
+void launch_permute(int64_t N, const uint32_t *idx, const double4 *pin, const double4 *vin, const double4 *win,
+                    const uint32_t *gin, double4 *pout, double4 *vout, double4 *wout, uint32_t *gout, cudaStream_t s);
+void launch_cells(int64_t N, const uint64_t *keys, const GridParams &g, uint32_t *cs, uint32_t *ce, cudaStream_t s);
+void launch_broad(bool fill, int64_t N, const double4 *pos, const GridParams &g, const uint32_t *cs,
+                  const uint32_t *ce, const DevBoundary *bnd, uint32_t *cnt_or_start, uint2 *cand, cudaStream_t s);
+void launch_trans(int64_t N, int64_t nc, const uint2 *cand, uint32_t *cnt, uint32_t *ct_start, uint32_t *cursor,
+                  uint32_t *ct_list, void *scan_tmp, cudaStream_t s, long long *launches);
+void launch_hist_flag(int64_t nc, const P4 *Pa, const P4 *Pb, uint32_t *flag, cudaStream_t s);
+void launch_hist_keys(int64_t nc, const uint32_t *flag, const uint32_t *scan, const uint2 *cand, const uint32_t *gid,
+                      uint64_t *keys, uint32_t *vals, cudaStream_t s);
+void launch_hist_gather(int64_t nh, const uint32_t *vals, const uint2 *cand, const uint32_t *gid, const P4 *Pa,
+                        const P4 *Pb, P4 *hPa, P4 *hPb, cudaStream_t s);
+void launch_hist_carry(int64_t nc, const uint2 *cand, const uint32_t *gid, const uint64_t *hkey, const P4 *hPa,
+                       const P4 *hPb, int64_t nh, P4 *Pa, P4 *Pb, cudaStream_t s);
+void launch_narrow(int64_t nc, const uint2 *cand, const double4 *pos, const DevBoundary *bnd, uint32_t *flag,
+                   P4 *Pa, P4 *Pb, StepScalars *sc, cudaStream_t s);
+void launch_compact(int64_t nc, const uint2 *cand, const uint32_t *flag, const uint32_t *scan, const double4 *pos,
+                    const DevBoundary *bnd, const SolveParams &sp, const P4 *Pca, const P4 *Pcb, uint2 *cij,
+                    G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, StepScalars *sc, cudaStream_t s);
+void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const uint32_t *scan, const uint32_t *ct_start,
+                const uint32_t *ct_list, const uint32_t *flag, uint32_t *cnt, uint32_t *inc_start, uint2 *inc,
+                void *scan_tmp, cudaStream_t s, long long *launches);
+void launch_contact_keys(int64_t nc, const uint2 *cij, const uint32_t *gid, uint64_t *keys, uint32_t *vals, cudaStream_t s);
+void launch_contact_out(int64_t nc, const uint32_t *vals, const uint2 *cij, const uint32_t *gid, const G4 *geo,
+                        const double *cdel, const P4 *Pa, const P4 *Pb, double *nrm, double *delta, double *P, cudaStream_t s);
+
+// solve.cu
+enum { SWEEP_MODE_SWEEP = 0, SWEEP_MODE_APPLY = 1, SWEEP_MODE_FORCES = 2 };
+void launch_prepare(int64_t N, const uint32_t *inc_start, const double4 *pos, double4 *vel, double4 *ang, double rho,
+                    cudaStream_t s);
+void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const double *cdel, R4 *row, R4 *row_imp,
+                 const double4 *vel, const double4 *pos, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
+                 cudaStream_t s);
+void launch_sweep(int mode, int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
+                  const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
+                  const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
+                  const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+void launch_integrate(int64_t N, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
+                      double rho, double *ke_part, StepScalars *sc, cudaStream_t s);
+void launch_plates(int64_t nc, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
+                   unsigned int *pcount, DevBoundary *bnd, double h, StepScalars *sc, cudaStream_t s);
+void launch_scatter_P(int64_t nc, const uint32_t *ccand, const P4 *Pa, const P4 *Pb, P4 *Pca, P4 *Pcb,
+                      cudaStream_t s);
+void launch_to_gid_order(int64_t N, const uint32_t *gid, const uint32_t *gid_sorted, const double4 *a,
+                         const double4 *b, const double4 *c, double *oa, double *ob, double *oc, double *orad,
+                         uint32_t *ogid, cudaStream_t s);
+void launch_load_state(int64_t N, const double *x, const double *r, const double *v, const double *w,
+                       const uint32_t *gid_in, double4 *pos, double4 *vel, double4 *ang, uint32_t *gid, cudaStream_t s);

@@ -1,0 +1,377 @@
+"""Thin ctypes binding of libdem.so (include/dem.h): argument marshalling only.
+
+Every step of the DEM path runs in the library's CUDA kernels; there is no Python or CPU
+fallback.  If ``lib/libdem.so`` is missing the import fails loudly.  PyTorch is used for
+plumbing only: the CUDA stream the library issues on and (optionally) its caching allocator.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("DEM_LIB_VARIANT") or os.path.join(HERE, "lib", "libdem.so")
+
+DEM_OK, DEM_ERR_INVALID, DEM_ERR_DIVERGED, DEM_ERR_STATE, DEM_ERR_CUDA, DEM_ERR_NCCL, DEM_ERR_OOM = 0, 2, 3, 4, 5, 6, 7
+AXIS_LOCKED, AXIS_VELOCITY, AXIS_FORCE = 0, 1, 2
+WALL_KEY_BASE = 0xFFFFFFF0
+PLATE_KEY_BASE = 0xFFFFF000
+
+
+class DemError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"dem status {status}: {msg}")
+        self.status = status
+
+
+class DivergedError(DemError):
+    pass
+
+
+class Material(C.Structure):
+    _fields_ = [("density", C.c_double), ("youngs", C.c_double), ("poisson", C.c_double),
+                ("mu_t", C.c_double), ("mu_r", C.c_double), ("restitution", C.c_double)]
+
+
+class Solver(C.Structure):
+    _fields_ = [("dt", C.c_double), ("n_iter", C.c_int32), ("n_iter_impact", C.c_int32),
+                ("hertz_exp", C.c_double), ("k_lin", C.c_double), ("damping_steps", C.c_double),
+                ("v_impact", C.c_double), ("gravity", C.c_double * 3), ("rolling_dims", C.c_int32),
+                ("pad0", C.c_int32), ("skin", C.c_double)]
+
+
+class Box(C.Structure):
+    _fields_ = [("lo", C.c_double * 3), ("hi", C.c_double * 3), ("wall_mask", C.c_uint32), ("pad0", C.c_uint32),
+                ("wall_mu_t", C.c_double), ("wall_mu_r", C.c_double)]
+
+
+class Particles(C.Structure):
+    _fields_ = [("n", C.c_int64), ("pos", C.c_void_p), ("radius", C.c_void_p), ("vel", C.c_void_p),
+                ("angvel", C.c_void_p), ("gid", C.c_void_p), ("on_device", C.c_int32), ("pad0", C.c_int32)]
+
+
+class BedDesc(C.Structure):
+    _fields_ = [("struct_size", C.c_size_t), ("mat", Material), ("solver", Solver), ("box", Box),
+                ("parts", Particles)]
+
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
+
+
+class DistDesc(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p),
+                ("cuda_stream", C.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p)]
+
+
+class StepReport(C.Structure):
+    _fields_ = [("step", C.c_int64), ("time", C.c_double), ("n_contacts", C.c_int64), ("n_pp", C.c_int64),
+                ("n_wall", C.c_int64), ("n_plate", C.c_int64), ("n_degenerate", C.c_int64),
+                ("n_candidates", C.c_int64), ("impact_fired", C.c_int32), ("rebuilt", C.c_int32),
+                ("ke", C.c_double), ("max_v", C.c_double), ("max_disp", C.c_double),
+                ("n_iter", C.c_int32), ("n_iter_impact", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class StateView(C.Structure):
+    _fields_ = [("n", C.c_int64), ("pos", C.c_void_p), ("vel", C.c_void_p), ("angvel", C.c_void_p),
+                ("radius", C.c_void_p), ("gid", C.c_void_p), ("on_device", C.c_int32), ("pad0", C.c_int32)]
+
+
+class ContactView(C.Structure):
+    _fields_ = [("n", C.c_int64), ("key", C.c_void_p), ("normal", C.c_void_p), ("delta", C.c_void_p),
+                ("P", C.c_void_p), ("on_device", C.c_int32), ("pad0", C.c_int32)]
+
+
+class PlateDesc(C.Structure):
+    _fields_ = [("n_boxes", C.c_int32), ("pad0", C.c_int32), ("lo", C.c_void_p), ("hi", C.c_void_p),
+                ("mass", C.c_double), ("mu_t", C.c_double), ("mu_r", C.c_double)]
+
+
+class PlateState(C.Structure):
+    _fields_ = [("pos", C.c_double * 3), ("vel", C.c_double * 3), ("force", C.c_double * 3), ("n_contacts", C.c_int64)]
+
+
+class Timing(C.Structure):
+    _fields_ = [("ms_total", C.c_double), ("ms_detect", C.c_double), ("ms_rebuild", C.c_double),
+                ("ms_sweeps", C.c_double), ("ms_integrate", C.c_double), ("n_sweep_launches", C.c_int64),
+                ("n_kernel_launches", C.c_int64), ("contact_sweeps", C.c_int64), ("particle_sweeps", C.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+CONTACT_DTYPE = np.dtype([("key", "<u8"), ("n", "<f8", (3,)), ("delta", "<f8"), ("P", "<f8", (7,))])
+
+# every symbol include/dem.h declares (checked by tests/test_boundary.py)
+EXPORTS = ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts", "dem_get_forces",
+           "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_set_timing", "dem_get_timing",
+           "dem_reset_timing", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
+           "dem_contact_network_length", "dem_plan_iterations", "dem_plan_timestep"]
+
+_lib = None
+
+
+def lib():
+    """Load libdem.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, i64, d = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        L.dem_create_bed.argtypes = [C.POINTER(BedDesc), C.POINTER(DistDesc), C.POINTER(vp)]
+        L.dem_step.argtypes = [vp, i32, C.POINTER(StepReport)]
+        L.dem_set_solver.argtypes = [vp, C.POINTER(Solver)]
+        L.dem_get_state.argtypes = [vp, C.POINTER(StateView)]
+        L.dem_set_state.argtypes = [vp, C.POINTER(StateView), C.POINTER(ContactView)]
+        L.dem_get_contacts.argtypes = [vp, C.POINTER(ContactView)]
+        L.dem_get_forces.argtypes = [vp, vp, vp, i32]
+        L.dem_add_plate.argtypes = [vp, C.POINTER(PlateDesc), C.POINTER(C.c_double), C.POINTER(i32)]
+        L.dem_drive_plate.argtypes = [vp, i32, i32, i32, d, d]
+        L.dem_get_plate.argtypes = [vp, i32, C.POINTER(PlateState)]
+        L.dem_drive_wall.argtypes = [vp, i32, d]
+        L.dem_set_timing.argtypes = [vp, i32]
+        L.dem_get_timing.argtypes = [vp, C.POINTER(Timing)]
+        L.dem_reset_timing.argtypes = [vp]
+        L.dem_stream.argtypes = [vp]
+        L.dem_stream.restype = vp
+        L.dem_destroy.argtypes = [vp]
+        L.dem_last_error.argtypes = [vp]
+        L.dem_last_error.restype = C.c_char_p
+        L.dem_profile_diameter.argtypes = [d, d, d, d]
+        L.dem_profile_diameter.restype = d
+        L.dem_contact_network_length.argtypes = [d, d, d, d, d]
+        L.dem_contact_network_length.restype = d
+        L.dem_plan_iterations.argtypes = [d, d]
+        L.dem_plan_iterations.restype = i32
+        L.dem_plan_timestep.argtypes = [d, d, d, d]
+        L.dem_plan_timestep.restype = d
+        for f in ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts",
+                  "dem_get_forces", "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall",
+                  "dem_set_timing", "dem_get_timing", "dem_reset_timing", "dem_destroy"]:
+            getattr(L, f).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+# ---------------------------------------------------------------- planner helpers (host-only)
+def profile_diameter(d_min, d_max, gamma, depth):
+    return lib().dem_profile_diameter(d_min, d_max, gamma, depth)
+
+
+def contact_network_length(d_min, d_max, r, eta, h):
+    return lib().dem_contact_network_length(d_min, d_max, r, eta, h)
+
+
+def plan_iterations(n_d, eps=0.02):
+    return lib().dem_plan_iterations(n_d, eps)
+
+
+def plan_timestep(d, eps, rho, sigma):
+    return lib().dem_plan_timestep(d, eps, rho, sigma)
+
+
+# ---------------------------------------------------------------- bed
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _f64(a, shape=None):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a.reshape(shape) if shape else a
+
+
+class Bed:
+    """One DEM context (one GPU).  Host arrays in, host arrays out, gid order."""
+
+    def __init__(self, pos, radius, vel=None, angvel=None, gid=None, *, material=None, solver=None, box=None,
+                 stream=None, torch_allocator=True, device=0):
+        import torch  # plumbing: stream + caching allocator
+        self._torch = torch
+        torch.cuda.set_device(device)
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
+        material = dict(density=2600.0, youngs=1e7, poisson=0.3, mu_t=0.4, mu_r=0.1, restitution=0.5, **(material or {}))
+        sol = dict(dt=1e-5, n_iter=92, n_iter_impact=0, hertz_exp=1.25, k_lin=0.0, damping_steps=4.5,
+                   v_impact=-1.0, gravity=(0.0, 0.0, -9.81), rolling_dims=3, skin=0.0)
+        sol.update(solver or {})
+        bx = dict(lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), wall_mask=0x3F, wall_mu_t=0.0, wall_mu_r=0.0)
+        bx.update(box or {})
+        desc = BedDesc()
+        desc.struct_size = C.sizeof(BedDesc)
+        for k, v in material.items():
+            setattr(desc.mat, k, v)
+        for k, v in sol.items():
+            if k == "gravity":
+                for j in range(3):
+                    desc.solver.gravity[j] = v[j]
+            else:
+                setattr(desc.solver, k, v)
+        for j in range(3):
+            desc.box.lo[j], desc.box.hi[j] = bx["lo"][j], bx["hi"][j]
+        desc.box.wall_mask, desc.box.wall_mu_t, desc.box.wall_mu_r = bx["wall_mask"], bx["wall_mu_t"], bx["wall_mu_r"]
+        pos = _f64(pos, (-1, 3))
+        radius = _f64(radius)
+        n = len(radius)
+        vel, angvel = _f64(vel, (-1, 3)), _f64(angvel, (-1, 3))
+        gid = None if gid is None else np.ascontiguousarray(gid, dtype=np.uint32)
+        self._keep = (pos, radius, vel, angvel, gid)
+        desc.parts.n = n
+        desc.parts.pos, desc.parts.radius = _ptr(pos), _ptr(radius)
+        desc.parts.vel, desc.parts.angvel, desc.parts.gid = _ptr(vel), _ptr(angvel), _ptr(gid)
+        desc.parts.on_device = 0
+        dist = DistDesc()
+        dist.rank, dist.world_size = 0, 1
+        dist.cuda_stream = self.stream.cuda_stream
+        if torch_allocator:
+            dev, strm = device, self.stream.cuda_stream
+
+            def _alloc(nbytes, _ctx):
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), dev, strm)
+                except Exception:   # OOM -> the library reports DEM_ERR_OOM
+                    return None
+
+            def _free(ptr, _ctx):
+                torch.cuda.caching_allocator_delete(ptr)
+
+            self._alloc_cb, self._free_cb = ALLOC_FN(_alloc), FREE_FN(_free)
+            dist.alloc, dist.free = self._alloc_cb, self._free_cb
+        self.n = n
+        self.material, self.solver, self.box = material, sol, bx
+        h = C.c_void_p()
+        st = lib().dem_create_bed(C.byref(desc), C.byref(dist), C.byref(h))
+        if st != DEM_OK:
+            raise DemError(st, lib().dem_last_error(None).decode())
+        self._h = h
+        self.last_report = None
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().dem_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != DEM_OK:
+            msg = lib().dem_last_error(self._h).decode()
+            raise (DivergedError if st == DEM_ERR_DIVERGED else DemError)(st, msg)
+
+    # -- stepping
+    def step(self, n=1):
+        rep = StepReport()
+        self._check(lib().dem_step(self._h, int(n), C.byref(rep)))
+        self.last_report = rep.as_dict()
+        return self.last_report
+
+    def set_solver(self, **kw):
+        """Replace solver settings (keys of dem_solver); unspecified keys keep their values."""
+        self.solver.update(kw)
+        s = Solver()
+        for k, v in self.solver.items():
+            if k == "gravity":
+                for j in range(3):
+                    s.gravity[j] = v[j]
+            else:
+                setattr(s, k, v)
+        self._check(lib().dem_set_solver(self._h, C.byref(s)))
+
+    # -- state
+    def get_state(self):
+        n = self.n
+        out = {k: np.empty((n, 3)) for k in ("pos", "vel", "angvel")}
+        out["radius"] = np.empty(n)
+        out["gid"] = np.empty(n, dtype=np.uint32)
+        v = StateView(n, *(_ptr(out[k]) for k in ("pos", "vel", "angvel", "radius", "gid")), 0, 0)
+        self._check(lib().dem_get_state(self._h, C.byref(v)))
+        return out
+
+    def get_state_device(self, out):
+        """out: dict of torch CUDA tensors pos/vel/angvel (n,3) float64, radius (n,) f64, gid (n,) int32."""
+        v = StateView(self.n, *(out[k].data_ptr() if k in out else None for k in ("pos", "vel", "angvel", "radius", "gid")), 1, 0)
+        self._check(lib().dem_get_state(self._h, C.byref(v)))
+
+    def set_state(self, pos, radius, vel=None, angvel=None, gid=None, hist=None):
+        pos, radius = _f64(pos, (-1, 3)), _f64(radius)
+        vel, angvel = _f64(vel, (-1, 3)), _f64(angvel, (-1, 3))
+        gid = None if gid is None else np.ascontiguousarray(gid, dtype=np.uint32)
+        v = StateView(len(radius), _ptr(pos), _ptr(vel), _ptr(angvel), _ptr(radius), _ptr(gid), 0, 0)
+        hv = None
+        if hist is not None and len(hist):
+            keys = np.ascontiguousarray(hist["key"], dtype=np.uint64)
+            P = np.ascontiguousarray(hist["P"], dtype=np.float64)
+            self._hk = (keys, P)
+            hv = ContactView(len(keys), keys.ctypes.data, None, None, P.ctypes.data, 0, 0)
+        self._check(lib().dem_set_state(self._h, C.byref(v), C.byref(hv) if hv is not None else None))
+
+    def get_contacts(self):
+        v = ContactView(0, None, None, None, None, 0, 0)
+        st = lib().dem_get_contacts(self._h, C.byref(v))
+        if st == DEM_ERR_INVALID and v.n > 0:
+            pass
+        elif st != DEM_OK:
+            self._check(st)
+        n = v.n
+        out = np.zeros(n, dtype=CONTACT_DTYPE)
+        if n == 0:
+            return out
+        key = np.empty(n, dtype=np.uint64)
+        nrm = np.empty((n, 3))
+        dl = np.empty(n)
+        P = np.empty((n, 7))
+        v = ContactView(n, key.ctypes.data, nrm.ctypes.data, dl.ctypes.data, P.ctypes.data, 0, 0)
+        self._check(lib().dem_get_contacts(self._h, C.byref(v)))
+        out["key"], out["n"], out["delta"], out["P"] = key, nrm, dl, P
+        return out
+
+    def get_forces(self):
+        F = np.empty((self.n, 3))
+        T = np.empty((self.n, 3))
+        self._check(lib().dem_get_forces(self._h, F.ctypes.data, T.ctypes.data, 0))
+        return F, T
+
+    # -- boundaries
+    def add_plate(self, boxes_lo, boxes_hi, pos, mass, mu_t=0.4, mu_r=0.1):
+        lo = np.ascontiguousarray(boxes_lo, dtype=np.float64).reshape(-1, 3)
+        hi = np.ascontiguousarray(boxes_hi, dtype=np.float64).reshape(-1, 3)
+        d = PlateDesc(len(lo), 0, lo.ctypes.data, hi.ctypes.data, mass, mu_t, mu_r)
+        p = (C.c_double * 3)(*pos)
+        pid = C.c_int32()
+        self._check(lib().dem_add_plate(self._h, C.byref(d), p, C.byref(pid)))
+        return pid.value
+
+    def drive_plate(self, plate, axis, mode, target, ramp_time=0.0):
+        self._check(lib().dem_drive_plate(self._h, plate, axis, mode, target, ramp_time))
+
+    def get_plate(self, plate):
+        s = PlateState()
+        self._check(lib().dem_get_plate(self._h, plate, C.byref(s)))
+        return {"pos": list(s.pos), "vel": list(s.vel), "force": list(s.force), "n_contacts": s.n_contacts}
+
+    def drive_wall(self, wall, normal_velocity):
+        self._check(lib().dem_drive_wall(self._h, wall, normal_velocity))
+
+    # -- timing
+    def set_timing(self, on=True):
+        self._check(lib().dem_set_timing(self._h, int(on)))
+
+    def reset_timing(self):
+        self._check(lib().dem_reset_timing(self._h))
+
+    def timing(self):
+        t = Timing()
+        self._check(lib().dem_get_timing(self._h, C.byref(t)))
+        return t.as_dict()
