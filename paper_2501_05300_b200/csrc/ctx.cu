@@ -75,7 +75,7 @@ struct dem_ctx {
     P4 *Pfa = nullptr, *Pfb = nullptr;            // final impulses of the last step
     uint32_t *ccand = nullptr;
     // incidence
-    uint32_t *inc_cnt = nullptr, *inc_start = nullptr;
+    uint32_t *inc_cnt = nullptr, *inc_start = nullptr, *order = nullptr;
     uint2 *inc = nullptr;
     // history
     int64_t nh = 0, cap_h = 0;
@@ -249,7 +249,7 @@ static dem_status alloc_particles(dem_ctx *ctx)
     TRY(A(ctx, &ctx->vel_prev, N)); TRY(A(ctx, &ctx->ang_prev, N));
     TRY(A(ctx, &ctx->gid, N)); TRY(A(ctx, &ctx->gid2, N)); TRY(A(ctx, &ctx->gid_sorted, N));
     TRY(A(ctx, &ctx->co_start, N + 1)); TRY(A(ctx, &ctx->ct_cnt, N + 1)); TRY(A(ctx, &ctx->ct_start, N + 1));
-    TRY(A(ctx, &ctx->ct_cursor, N + 1)); TRY(A(ctx, &ctx->inc_cnt, N + 1)); TRY(A(ctx, &ctx->inc_start, N + 1));
+    TRY(A(ctx, &ctx->ct_cursor, N + 1)); TRY(A(ctx, &ctx->inc_cnt, N + 1)); TRY(A(ctx, &ctx->inc_start, N + 1)); TRY(A(ctx, &ctx->order, N + 1));
     TRY(A(ctx, &ctx->ke_part, N / 256 + 2));
     TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
     TRY(A(ctx, &ctx->db, 1));
@@ -493,9 +493,10 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->inc_cnt,
                ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
     launch_prepare(N, ctx->inc_start, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], sp.rho, s);
+    launch_tile_order(N, ctx->inc_start, ctx->order, s);
     // impact trigger
     launch_rows(nc, 0, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
-    ctx->launches += 4;
+    ctx->launches += 5;
     CK(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(StepScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const bool impact = ctx->hsc->impact != 0 && nc > 0;
@@ -507,7 +508,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         CK(cudaMemsetAsync(ctx->Pb[0], 0, nc * sizeof(P4), s));
         for (int it = 0; it < n_imp; it++) {
             const int pi = it & 1;
-            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
+            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                          ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row_imp, ctx->Pa[pi],
                          ctx->Pb[pi], ctx->Pa[pi ^ 1], ctx->Pb[pi ^ 1], ctx->db, sp, s);
             ctx->cur ^= 1;
@@ -519,7 +520,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     }
     // main stage: SPOOK rows, gravity + warm start, N_it Jacobi sweeps
     launch_rows(nc, 1, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
-    launch_sweep(SWEEP_MODE_APPLY, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
+    launch_sweep(SWEEP_MODE_APPLY, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                  ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, nullptr,
                  nullptr, ctx->db, sp, s);
     ctx->cur ^= 1;
@@ -529,7 +530,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     const P4 *pin_a = ctx->Pwa, *pin_b = ctx->Pwb;
     for (int it = 0; it < n_it; it++) {
         P4 *oa = ctx->Pa[it & 1], *ob = ctx->Pb[it & 1];
-        launch_sweep(SWEEP_MODE_SWEEP, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
+        launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                      ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
                      ctx->db, sp, s);
         ctx->cur ^= 1;
@@ -857,7 +858,7 @@ dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device)
     const int64_t N = ctx->N;
     if (!N) return DEM_OK;
     cudaStream_t s = ctx->s;
-    launch_sweep(SWEEP_MODE_FORCES, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
+    launch_sweep(SWEEP_MODE_FORCES, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
                  ctx->inc, ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, nullptr, nullptr, ctx->db, ctx->sp, s);
     double *d = nullptr;
     TRY(A(ctx, &d, 6 * N));

@@ -37,10 +37,11 @@ void launch_prepare(int64_t N, const uint32_t *inc_start, const double4 *pos, do
 void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const double *cdel, R4 *row, R4 *row_imp,
                  const double4 *vel, const double4 *pos, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
                  cudaStream_t s);
-void launch_sweep(int mode, int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
-                  const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
+void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin, const double4 *win, double4 *vout,
+                  double4 *wout, const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
                   const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s);
 void launch_integrate(int64_t N, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
                       double rho, double *ke_part, StepScalars *sc, cudaStream_t s);
 void launch_plates(int64_t nc, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
