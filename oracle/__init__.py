@@ -50,7 +50,7 @@ class Params(C.Structure):
 
 class Wall(C.Structure):
     _fields_ = [("p", C.c_double * 3), ("n", C.c_double * 3), ("vel", C.c_double),
-                ("mu_t", C.c_double), ("mu_r", C.c_double)]
+                ("mu_t", C.c_double), ("mu_r", C.c_double), ("id", C.c_int32), ("pad", C.c_int32)]
 
 
 class Plate(C.Structure):
@@ -119,6 +119,8 @@ def lib():
         L.or_detect.argtypes = [C.POINTER(World), C.POINTER(Params), C.c_void_p, i64,
                                 C.POINTER(i64), C.POINTER(i64)]
         L.or_detect.restype = i32
+        L.or_contacts_of.argtypes = [C.POINTER(World), C.c_void_p, i64, C.c_void_p, i64, C.POINTER(i64)]
+        L.or_contacts_of.restype = i32
         L.or_step.argtypes = [C.POINTER(World), C.POINTER(Params), C.c_void_p, i64, C.c_void_p, i64,
                               C.POINTER(i64), pd, pd, C.POINTER(Report)]
         L.or_step.restype = i32
@@ -197,6 +199,7 @@ def box_walls(lo, hi, mask=0x3F, mu_t=0.0, mu_r=0.0):
             for k in range(3):
                 w.p[k], w.n[k] = p[k], n[k]
             w.vel, w.mu_t, w.mu_r = 0.0, mu_t, mu_r
+            w.id = 2 * ax + side
             walls.append(w)
     return walls
 
@@ -257,6 +260,18 @@ class OracleWorld:
         if rc:
             raise RuntimeError(f"or_detect failed rc={rc}")
         return out[: n.value].copy(), nd.value
+
+    def contacts_of(self, idx):
+        """Brute-force contacts of the given particle indices (caller order), sorted by key."""
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        W = self._world()
+        cap = 64 * len(idx) + 64
+        out = np.zeros(cap, dtype=CONTACT_DTYPE)
+        n = C.c_int64()
+        rc = lib().or_contacts_of(C.byref(W), idx.ctypes.data, len(idx), out.ctypes.data, cap, C.byref(n))
+        if rc:
+            raise RuntimeError("or_contacts_of failed")
+        return out[: n.value].copy()
 
     def step(self, params: Params, n_steps: int = 1, want_forces: bool = False):
         """Advance n_steps; returns (contacts of the last step, F, T)."""

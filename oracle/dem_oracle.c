@@ -176,7 +176,7 @@ static int detect_all(const or_world *w, raw_list *L, int64_t *n_degen)
                        + (w->x[3 * i + 2] - W->p[2]) * W->n[2];
             if (!(s < w->r[i])) continue;
             raw_contact c;
-            c.key = ((uint64_t)w->gid[i] << 32) | (uint64_t)WALL_KEY(k);
+            c.key = ((uint64_t)w->gid[i] << 32) | (uint64_t)WALL_KEY(W->id);
             c.a = i; c.b = -1; c.kind = 1; c.idx = k;
             c.n[0] = -W->n[0]; c.n[1] = -W->n[1]; c.n[2] = -W->n[2];
             c.delta = w->r[i] - s;
@@ -241,6 +241,62 @@ int32_t or_detect(const or_world *w, const or_params *p, or_contact *out, int64_
         out[c].delta = L.v[c].delta;
         memset(out[c].P, 0, sizeof(out[c].P));
     }
+    free(L.v);
+    return 0;
+}
+
+/* Contacts of selected particles only (brute force against all N, walls and plates): the
+ * full-size sampled check of the pair set.  Same predicate and orientation as detect_all. */
+int32_t or_contacts_of(const or_world *w, const int64_t *idx, int64_t nidx, or_contact *out, int64_t cap,
+                       int64_t *n_out)
+{
+    raw_list L = {0, 0, 0};
+    const int64_t N = w->n;
+    for (int64_t q = 0; q < nidx; q++) {
+        const int64_t i = idx[q];
+        for (int64_t j = 0; j < N; j++) {
+            if (j == i) continue;
+            int64_t a = i, b = j;
+            if (w->gid[j] < w->gid[i]) { a = j; b = i; }
+            double dx = w->x[3 * b + 0] - w->x[3 * a + 0];
+            double dy = w->x[3 * b + 1] - w->x[3 * a + 1];
+            double dz = w->x[3 * b + 2] - w->x[3 * a + 2];
+            double d2 = (dx * dx + dy * dy) + dz * dz;
+            double R = w->r[a] + w->r[b];
+            if (!(d2 < R * R) || d2 == 0.0) continue;
+            double d = sqrt(d2);
+            raw_contact c;
+            c.key = ((uint64_t)w->gid[a] << 32) | (uint64_t)w->gid[b];
+            c.a = a; c.b = b; c.kind = 0; c.idx = -1;
+            c.n[0] = dx / d; c.n[1] = dy / d; c.n[2] = dz / d;
+            c.delta = R - d;
+            if (push(&L, &c)) { free(L.v); return -1; }
+        }
+        for (int32_t k = 0; k < w->n_walls; k++) {
+            const or_wall *W = &w->walls[k];
+            double s = ((w->x[3 * i] - W->p[0]) * W->n[0] + (w->x[3 * i + 1] - W->p[1]) * W->n[1])
+                       + (w->x[3 * i + 2] - W->p[2]) * W->n[2];
+            if (!(s < w->r[i])) continue;
+            raw_contact c;
+            c.key = ((uint64_t)w->gid[i] << 32) | (uint64_t)WALL_KEY(W->id);
+            c.a = i; c.b = -1; c.kind = 1; c.idx = k;
+            c.n[0] = -W->n[0]; c.n[1] = -W->n[1]; c.n[2] = -W->n[2];
+            c.delta = w->r[i] - s;
+            if (push(&L, &c)) { free(L.v); return -1; }
+        }
+    }
+    qsort(L.v, (size_t)L.n, sizeof(raw_contact), cmp_raw);
+    int64_t m = 0;
+    for (int64_t c = 0; c < L.n; c++) {
+        if (m && L.v[c].key == out[m - 1].key) continue;       /* pair found from both ends */
+        if (m >= cap) { free(L.v); return -1; }
+        out[m].key = L.v[c].key;
+        memcpy(out[m].n, L.v[c].n, sizeof(out[m].n));
+        out[m].delta = L.v[c].delta;
+        memset(out[m].P, 0, sizeof(out[m].P));
+        m++;
+    }
+    *n_out = m;
     free(L.v);
     return 0;
 }

@@ -43,6 +43,7 @@ typedef struct {
     double n[3];              /* unit normal pointing INTO the domain */
     double vel;               /* kinematic velocity along n (drive_wall) */
     double mu_t, mu_r;        /* frictionless by default */
+    int32_t id, pad;          /* wall id in contact keys: 2*axis + side (0:-x 1:+x ... 5:+z) */
 } or_wall;
 
 #define OR_MAX_BOX 8
@@ -107,6 +108,11 @@ double or_planned_timestep(double d, double eps, double rho, double sigma);
 /* brute-force O(N^2) detection: contacts sorted by key; returns 0 or -1 (cap) */
 int32_t or_detect(const or_world *w, const or_params *p, or_contact *out, int64_t cap,
                   int64_t *n_out, int64_t *n_degenerate);
+
+/* brute-force contacts of the particles idx[0..nidx) only (walls too; plates not included),
+ * deduplicated and sorted by key: sampled pair-set checks on full-size beds */
+int32_t or_contacts_of(const or_world *w, const int64_t *idx, int64_t nidx, or_contact *out, int64_t cap,
+                       int64_t *n_out);
 
 /* one full time step: detection, impact stage, SPOOK rows, warm start,
  * n_it Jacobi sweeps, integration, plates/walls.  hist (any order) supplies the warm start.

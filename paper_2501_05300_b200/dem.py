@@ -198,7 +198,9 @@ class Bed:
         torch.cuda.set_device(device)
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.Stream(device=device)
-        material = dict(density=2600.0, youngs=1e7, poisson=0.3, mu_t=0.4, mu_r=0.1, restitution=0.5, **(material or {}))
+        mat = dict(density=2600.0, youngs=1e7, poisson=0.3, mu_t=0.4, mu_r=0.1, restitution=0.5)
+        mat.update(material or {})
+        material = mat
         sol = dict(dt=1e-5, n_iter=92, n_iter_impact=0, hertz_exp=1.25, k_lin=0.0, damping_steps=4.5,
                    v_impact=-1.0, gravity=(0.0, 0.0, -9.81), rolling_dims=3, skin=0.0)
         sol.update(solver or {})

@@ -1,18 +1,39 @@
 """GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on identical inputs.
 
 Bars (BASELINE.json acceptance): contact pair set bit-exact; per-particle force and torque
-relative error <= 1e-5 under the physical floors of tests/parity.py (reading R34)."""
+relative error <= 1e-5 under the physical floors of tests/parity.py (reading R34);
+1,000-step trajectories on config 0 (and the settled config 0s) within 1e-4 of the mean radius.
+"""
+import os
+
 import numpy as np
 import pytest
 
+import oracle as O
 import synth
-from tests.parity import compare_step
+from tests.parity import compare_step, gpu_bed, oracle_params, oracle_world
 
 pytestmark = pytest.mark.gpu
 
 TOL_F = 1e-5
+HERE = os.path.dirname(os.path.abspath(__file__))
 
 
+def dem():
+    from paper_2501_05300_b200 import dem as D
+    return D
+
+
+def config0s():
+    f = np.load(os.path.join(HERE, "golden", "config0s_state.npz"))
+    bed = synth.Bed(x=f["x"], r=f["r"], v=f["v"], w=f["w"], gid=f["gid"], box_lo=tuple(f["box_lo"]),
+                    box_hi=tuple(f["box_hi"]), name="config0s")
+    hist = np.zeros(len(f["hist_key"]), dtype=O.CONTACT_DTYPE)
+    hist["key"], hist["P"] = f["hist_key"], f["hist_P"]
+    return bed, hist
+
+
+# ------------------------------------------------------------------ one-step parity
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_one_step_random_cloud(seed):
     bed = synth.random_cloud(600, (0, 0, 0), (0.05, 0.05, 0.05), 1.5e-3, 3.5e-3, seed, v_scale=0.02, w_scale=2.0)
@@ -29,7 +50,253 @@ def test_one_step_polydisperse_8x_multilevel():
 
 
 def test_config0_first_steps():
-    bed = synth.config0()
-    res = compare_step(bed, n_it=92, dt=1e-5, n_steps=3)
+    res = compare_step(synth.config0(), n_it=92, dt=1e-5, n_steps=3)
     assert res["pairs_equal"], res
     assert res["force_err"] <= TOL_F and res["torque_err"] <= TOL_F, res
+
+
+def test_config0s_one_step_with_history():
+    """Settled config 0 with its contact history as warm start: ~10k contacts."""
+    bed, hist = config0s()
+    res = compare_step(bed, n_it=92, dt=1e-5, hist=hist, v_imp=1e30)
+    assert res["n_contacts_ref"] > 5000
+    assert res["pairs_equal"], res
+    assert res["force_err"] <= TOL_F and res["torque_err"] <= TOL_F, res
+
+
+# ------------------------------------------------------------------ trajectories
+def _trajectory(bed, hist, steps, every, n_it, dt):
+    Wo = oracle_world(bed)
+    po = oracle_params(n_it, dt)
+    gb = gpu_bed(bed, dt=dt, n_iter=n_it)
+    if hist is not None:
+        Wo.hist = hist
+        gb.set_state(bed.x, bed.r, bed.v, bed.w, bed.gid, hist=hist)
+    order = np.argsort(bed.gid)
+    worst = 0.0
+    try:
+        for k in range(steps // every):
+            Wo.step(po, n_steps=every)
+            gb.step(every)
+            st = gb.get_state()
+            worst = max(worst, float(np.abs(st["pos"] - Wo.x[order]).max()))
+    finally:
+        gb.close()
+    return worst
+
+
+@pytest.mark.slow
+def test_trajectory_config0_1000_steps():
+    bed = synth.config0()
+    worst = _trajectory(bed, None, 1000, 100, 92, 1e-5)
+    assert worst <= 1e-4 * bed.r.mean(), worst
+
+
+@pytest.mark.slow
+def test_trajectory_config0s_1000_steps():
+    bed, hist = config0s()
+    worst = _trajectory(bed, hist, 1000, 100, 92, 1e-5)
+    assert worst <= 1e-4 * bed.r.mean(), worst
+
+
+# ------------------------------------------------------------------ edge cases
+def test_empty_bed():
+    D = dem()
+    b = D.Bed(np.zeros((0, 3)), np.zeros(0), box=dict(lo=(0, 0, 0), hi=(1, 1, 1)))
+    rep = b.step(3)
+    assert rep["n_contacts"] == 0 and rep["step"] == 3
+    assert b.get_state()["pos"].shape == (0, 3)
+    assert len(b.get_contacts()) == 0
+    b.close()
+
+
+def test_single_particle_free_flight_exact():
+    D = dem()
+    h, n = 1e-4, 200
+    x0, v0 = np.array([[0.3, 0.4, 0.5]]), np.array([[0.5, -0.2, 1.0]])
+    b = D.Bed(x0, [1e-3], v0, box=dict(lo=(0, 0, 0), hi=(1, 1, 1)), solver=dict(dt=h, n_iter=5))
+    b.step(n)
+    st = b.get_state()
+    g = np.array([0, 0, -9.81])
+    np.testing.assert_allclose(st["pos"], x0 + n * h * v0 + h * h * g * n * (n + 1) / 2, rtol=1e-12)
+    np.testing.assert_allclose(st["vel"], v0 + n * h * g, rtol=1e-12)
+    b.close()
+
+
+def test_degenerate_coincident_centres_and_outside_box():
+    """Coincident centres are counted and skipped; particles outside the container
+    (clamped grid cells) still get the exact pair set."""
+    bed = synth.random_cloud(300, (-0.01, -0.01, -0.01), (0.04, 0.04, 0.04), 1.5e-3, 3e-3, 21, v_scale=0.01)
+    bed.x[5] = bed.x[7]
+    bed.box_lo, bed.box_hi = (0.0, 0.0, 0.0), (0.03, 0.03, 0.03)
+    res = compare_step(bed, n_it=30, dt=1e-5)
+    assert res["pairs_equal"], res
+    assert res["force_err"] <= TOL_F and res["torque_err"] <= TOL_F, res
+
+
+def test_linear_model_and_planar_rolling():
+    bed = synth.random_cloud(400, (0, 0, 0), (0.04, 0.04, 0.04), 1.5e-3, 3e-3, 31, v_scale=0.02, w_scale=1.0)
+    Wo = oracle_world(bed)
+    po = O.make_params(h=1e-5, n_it=30, e_H=1.0, k_lin=2e3, rolling_dims=2)
+    gb = gpu_bed(bed, dt=1e-5, n_iter=30, hertz_exp=1.0, k_lin=2e3, rolling_dims=2)
+    c_ref, F_ref, T_ref = Wo.step(po, want_forces=True)
+    gb.step(1)
+    c = gb.get_contacts()
+    F, T = gb.get_forces()
+    gb.close()
+    from tests.parity import force_errors
+    eF, eT = force_errors(F, T, F_ref, T_ref, c_ref, bed, 2600.0, 1e-5)
+    assert np.array_equal(c["key"], c_ref["key"])
+    assert eF.max() <= TOL_F and eT.max() <= TOL_F, (eF.max(), eT.max())
+
+
+def test_newton_impact_headon():
+    D = dem()
+    r = 3e-3
+    x = np.array([[0.05, 0.05, 0.05], [0.05 + 2 * r - 1e-10, 0.05, 0.05]])
+    v = np.array([[0.3, 0, 0], [-0.1, 0, 0]])
+    b = D.Bed(x, [r, r], v, box=dict(lo=(0, 0, 0), hi=(0.1, 0.1, 0.1)), material=dict(mu_t=0, mu_r=0),
+              solver=dict(dt=1e-6, n_iter=20, gravity=(0, 0, 0)))
+    rep = b.step(1)
+    st = b.get_state()
+    b.close()
+    assert rep["impact_fired"] == 1
+    # impulses are stored in fp32 (DESIGN.md §5): the separation speed is exact to 2^-24 relative
+    assert st["vel"][1, 0] - st["vel"][0, 0] == pytest.approx(0.5 * 0.4, rel=2.0 ** -23)
+    assert st["vel"][:, 0].sum() == pytest.approx(0.2, abs=1e-15)
+
+
+def _small_bed_for_plates(seed):
+    b = synth.random_cloud(250, (0.002, 0.002, 0.002), (0.028, 0.028, 0.014), 1.5e-3, 2.5e-3, seed)
+    b.box_lo, b.box_hi = (0.0, 0.0, 0.0), (0.03, 0.03, 0.05)
+    return b
+
+
+def test_plates_kinematic_and_force_axes_vs_oracle():
+    """A grouser plate (3 boxes) pressed down kinematically and a flat plate on a force axis,
+    20 steps on both sides: pair sets every step, plate forces and positions."""
+    bed = _small_bed_for_plates(41)
+    lo = [(-0.006, -0.006, 0.0), (-0.006, -0.006, -0.003), (0.003, -0.006, -0.003)]
+    hi = [(0.006, 0.006, 0.002), (-0.004, 0.006, 0.0), (0.005, 0.006, 0.0)]
+    top = bed.x[:, 2].max() + 2.6e-3
+    P1 = O.make_plate(lo, hi, pos=(0.009, 0.015, top), mass=0.05)
+    P1.mode[2], P1.target[2], P1.vel[2] = 1, -0.05, -0.05
+    P2 = O.make_plate([(-0.004, -0.004, 0.0)], [(0.004, 0.004, 0.002)], pos=(0.022, 0.015, top - 1e-3), mass=0.01)
+    P2.mode[2], P2.target[2] = 2, -0.5
+    Wo = oracle_world(bed, plates=[P1, P2])
+    po = oracle_params(30, 1e-5)
+    gb = gpu_bed(bed, dt=1e-5, n_iter=30)
+    p1 = gb.add_plate(lo, hi, (0.009, 0.015, top), 0.05)
+    gb.drive_plate(p1, 2, 1, -0.05)
+    p2 = gb.add_plate([(-0.004, -0.004, 0.0)], [(0.004, 0.004, 0.002)], (0.022, 0.015, top - 1e-3), 0.01)
+    gb.drive_plate(p2, 2, 2, -0.5)
+    try:
+        for s in range(20):
+            c_ref, _, _ = Wo.step(po)
+            gb.step(1)
+            c = gb.get_contacts()
+            assert np.array_equal(c["key"], c_ref["key"]), s
+        g1, g2 = gb.get_plate(p1), gb.get_plate(p2)
+    finally:
+        gb.close()
+    assert (c_ref["key"] & np.uint64(0xFFFFFFFF) >= np.uint64(O.PLATE_KEY_BASE)).sum() > 0
+    assert g1["pos"][2] == pytest.approx(Wo.plates[0].pos[2], abs=1e-12)
+    scale = max(abs(Wo.plates[0].force[2]), 1e-3)
+    assert abs(g1["force"][2] - Wo.plates[0].force[2]) <= 1e-5 * scale
+    assert g2["pos"][2] == pytest.approx(Wo.plates[1].pos[2], abs=1e-9)
+
+
+def test_moving_wall_vs_oracle():
+    bed = _small_bed_for_plates(43)
+    Wo = oracle_world(bed)
+    Wo.walls[1].vel = 0.2        # +x wall moving inward
+    po = oracle_params(30, 1e-5)
+    gb = gpu_bed(bed, dt=1e-5, n_iter=30)
+    gb.drive_wall(1, 0.2)
+    try:
+        for s in range(30):
+            c_ref, _, _ = Wo.step(po)
+            gb.step(1)
+        c = gb.get_contacts()
+        st = gb.get_state()
+    finally:
+        gb.close()
+    assert np.array_equal(c["key"], c_ref["key"])
+    order = np.argsort(bed.gid)
+    assert np.abs(st["pos"] - Wo.x[order]).max() < 1e-9
+
+
+# ------------------------------------------------------------------ API behaviour
+def test_determinism_bit_identical():
+    bed = synth.random_cloud(2000, (0, 0, 0), (0.08, 0.08, 0.08), 1.5e-3, 4e-3, 51, v_scale=0.02, w_scale=1.0)
+    outs = []
+    for _ in range(2):
+        gb = gpu_bed(bed, dt=1e-5, n_iter=40)
+        gb.step(5)
+        st = gb.get_state()
+        c = gb.get_contacts()
+        gb.close()
+        outs.append((st, c))
+    for k in ("pos", "vel", "angvel"):
+        assert np.array_equal(outs[0][0][k], outs[1][0][k]), k
+    assert np.array_equal(outs[0][1]["P"], outs[1][1]["P"])
+
+
+def test_state_roundtrip_and_errors():
+    D = dem()
+    bed = synth.random_cloud(100, (0, 0, 0), (0.03, 0.03, 0.03), 1.5e-3, 3e-3, 61, v_scale=0.01)
+    gb = gpu_bed(bed, dt=1e-5, n_iter=10)
+    with pytest.raises(D.DemError) as e:
+        gb.get_forces()
+    assert e.value.status == D.DEM_ERR_STATE
+    st = gb.get_state()
+    order = np.argsort(bed.gid)
+    np.testing.assert_array_equal(st["pos"], bed.x[order])
+    np.testing.assert_array_equal(st["gid"], bed.gid[order])
+    with pytest.raises(D.DemError) as e:
+        gb.drive_wall(9, 1.0)
+    assert e.value.status == D.DEM_ERR_INVALID
+    with pytest.raises(D.DemError):
+        gb.set_solver(dt=-1.0)
+    gb.close()
+    with pytest.raises(D.DemError) as e:
+        D.Bed(bed.x, -bed.r, box=dict(lo=(0, 0, 0), hi=(1, 1, 1)))
+    assert e.value.status == D.DEM_ERR_INVALID
+
+
+# ------------------------------------------------------------------ full-size checks
+def test_full_size_sampled_pair_set_and_invariants():
+    """config 1 geometry as a jammed packing (~300k particles, bench launch configuration):
+    sampled pair sets against the oracle's brute force, cones, momentum without walls/gravity."""
+    bed = synth.banded_bed((0.4, 0.4, 0.3), [(0.0, 0.06, 2e-3), (0.06, 0.3, 4e-3)], 1001, spacing=2.0)
+    D = dem()
+    gb = D.Bed(bed.x, bed.r, bed.v, bed.w, bed.gid, solver=dict(dt=5e-6, n_iter=20, gravity=(0, 0, 0)),
+               box=dict(lo=bed.box_lo, hi=bed.box_hi, wall_mask=0))
+    rho = 2600.0
+    m = rho * np.pi * (2 * bed.r[np.argsort(bed.gid)]) ** 3 / 6
+    p_before = (m[:, None] * gb.get_state()["vel"]).sum(0)
+    gb.step(1)
+    c = gb.get_contacts()
+    st = gb.get_state()
+    gb.close()
+    # cones (fp32 impulses)
+    inv = np.argsort(bed.gid)
+    ka = (c["key"] >> np.uint64(32)).astype(np.int64)
+    kb = (c["key"] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    Rs = bed.r[inv[ka]] * bed.r[inv[kb]] / (bed.r[inv[ka]] + bed.r[inv[kb]])
+    Pn = c["P"][:, 0]
+    assert (np.linalg.norm(c["P"][:, 1:4], axis=1) <= 0.4 * Pn * (1 + 1e-6) + 1e-30).all()
+    assert (np.linalg.norm(c["P"][:, 4:7], axis=1) <= 0.1 * Rs * Pn * (1 + 1e-6) + 1e-30).all()
+    # momentum: inter-particle impulses cancel
+    p_after = (m[:, None] * st["vel"]).sum(0)
+    scale = (m[:, None] * np.abs(st["vel"])).sum()
+    assert np.abs(p_after - p_before).max() <= 1e-11 * scale
+    # sampled pair sets vs brute force on the initial state
+    rng = np.random.default_rng(5)
+    sample = rng.choice(bed.n, 400, replace=False)
+    Wo = oracle_world(bed, walls=False)
+    ref = Wo.contacts_of(sample)
+    sg = set(bed.gid[sample].tolist())
+    mine = c[np.isin(ka, list(sg)) | np.isin(kb, list(sg))]
+    np.testing.assert_array_equal(np.sort(mine["key"]), ref["key"])
+    assert len(ref) > 1000

@@ -104,7 +104,7 @@ def test_detect_examples(oracle_mod):
     c, _ = _world(oracle_mod, [[0.1, 0.2, 4e-3]], [5e-3], walls=floor).detect()
     assert len(c) == 1 and c["delta"][0] == pytest.approx(1e-3, rel=1e-12)
     np.testing.assert_allclose(c["n"][0], [0, 0, -1])
-    assert int(c["key"][0]) & 0xFFFFFFFF == oracle_mod.WALL_KEY_BASE + 0
+    assert int(c["key"][0]) & 0xFFFFFFFF == oracle_mod.WALL_KEY_BASE + 4   # floor = wall 4 (-z)
     # coincident centres are flagged and skipped
     c, nd = _world(oracle_mod, [[0, 0, 0], [0, 0, 0], [1, 1, 1]], [1e-3, 2e-3, 1e-3]).detect()
     assert len(c) == 0 and nd == 1
@@ -268,7 +268,7 @@ def test_statics_k_stack(oracle_mod):
     m, _ = oracle_mod.mass_inertia(2 * r, 2200.0)
     keys = c["key"]
     f = {int(kk): c["P"][i, 0] / h for i, kk in enumerate(keys)}
-    assert f[(0 << 32) | oracle_mod.WALL_KEY_BASE] == pytest.approx(k * m * 9.81, rel=0.01)
+    assert f[(0 << 32) | (oracle_mod.WALL_KEY_BASE + 4)] == pytest.approx(k * m * 9.81, rel=0.01)
     for i in range(k - 1):
         assert f[(i << 32) | (i + 1)] == pytest.approx((k - 1 - i) * m * 9.81, rel=0.01)
 
@@ -420,7 +420,7 @@ def test_jacobi_fixed_point_equals_lcp_enumeration(oracle_mod):
     P = _lcp_enumeration(A, q)
     keys = []
     for (i, j, *_ ) in rows:
-        keys.append((i << 32) | (j if j is not None else oracle_mod.WALL_KEY_BASE))
+        keys.append((i << 32) | (j if j is not None else oracle_mod.WALL_KEY_BASE + 4))
     order = np.argsort(keys)
     np.testing.assert_allclose(c["P"][:, 0], P[order], rtol=1e-6, atol=1e-12 * P.max())
     # warm start from a perturbed history: same fixed point
@@ -456,4 +456,4 @@ def test_kinematic_and_force_driven_plate(oracle_mod):
     m, _ = oracle_mod.mass_inertia(2 * r, 2200.0)
     assert W.plates[0].force[2] == pytest.approx(F0, rel=0.01)
     f = {int(k) & 0xFFFFFFFF: c["P"][i, 0] / h for i, k in enumerate(c["key"])}
-    assert f[oracle_mod.WALL_KEY_BASE] == pytest.approx(F0 + m * 9.81, rel=0.01)
+    assert f[oracle_mod.WALL_KEY_BASE + 4] == pytest.approx(F0 + m * 9.81, rel=0.01)
