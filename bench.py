@@ -229,7 +229,7 @@ def main():
     tf = os.path.join(ROOT, "profiles", "sweep_traffic.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get(wl)
+            traffic = json.load(open(tf))[wl]["dram_bytes_per_launch"] / 1e9   # GB per launch (ncu)
         except Exception:
             traffic = None
     out = {
@@ -245,7 +245,9 @@ def main():
         "contact_sweeps_per_s": tm["contact_sweeps"] / (ms / 1e3) * world,
         "roofline": {"bound": "hbm", "kernel": "k_sweep_tile", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
+                     "traffic_unit": "GB per launch (ncu dram read+write)",
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": sweep_ms,
+                     "alg_bytes_model": "112 B/particle + 72 B/contact per sweep (SURVEY 8d)",
                      "sweep_share_of_step": tm["ms_sweeps"] / max(tm["ms_total"], 1e-9),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "gpu_launches": int(tm["n_kernel_launches"]),

@@ -304,20 +304,37 @@ static double ord_unbits(unsigned long long u)
     std::memcpy(&x, &b, 8);
     return x;
 }
+// per-level bounding boxes and counts: shared-memory partials per block, then one global
+// atomic per block and value (min/max/count are order-independent: deterministic)
 __global__ void k_level_bbox(int64_t N, const double4 *__restrict__ pos, double rmin, int nlev,
                              unsigned long long *__restrict__ box)
 {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const double4 p = pos[i];
-    const int L = level_of(p.w, rmin, nlev);
-    unsigned long long *b = box + 8 * L;
-    const double c[3] = {p.x, p.y, p.z};
-    for (int k = 0; k < 3; k++) {
-        atomicMin(&b[k], ord_bits(c[k]));
-        atomicMax(&b[3 + k], ord_bits(c[k]));
+    __shared__ unsigned long long sb[DEM_MAX_LEVELS * 8];
+    for (int q = threadIdx.x; q < DEM_MAX_LEVELS * 8; q += blockDim.x) {
+        const int f = q & 7;
+        sb[q] = f < 3 ? ~0ULL : 0ULL;
     }
-    atomicAdd(&b[6], 1ULL);
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N) {
+        const double4 p = pos[i];
+        const int L = level_of(p.w, rmin, nlev);
+        unsigned long long *b = sb + 8 * L;
+        const double c[3] = {p.x, p.y, p.z};
+        for (int k = 0; k < 3; k++) {
+            atomicMin(&b[k], ord_bits(c[k]));
+            atomicMax(&b[3 + k], ord_bits(c[k]));
+        }
+        atomicAdd(&b[6], 1ULL);
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < nlev * 8; q += blockDim.x) {
+        const int f = q & 7;
+        if (sb[8 * (q >> 3) + 6] == 0 || f == 7) continue;
+        if (f < 3) atomicMin(&box[q], sb[q]);
+        else if (f < 6) atomicMax(&box[q], sb[q]);
+        else atomicAdd(&box[q], sb[q]);
+    }
 }
 
 static dem_status compute_grid(dem_ctx *ctx)
@@ -490,13 +507,14 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     ctx->nc = nc;
     launch_compact(ncand, ctx->cand, ctx->cflag, ctx->cscan, ctx->pos, ctx->db, sp, ctx->Pca, ctx->Pcb, ctx->cij,
                    ctx->geo, ctx->row, ctx->cdel, ctx->Pwa, ctx->Pwb, ctx->ccand, ctx->dsc, s);
+    launch_count_kinds(nc, ctx->cij, ctx->dsc, s);
     launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->inc_cnt,
                ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
     launch_prepare(N, ctx->inc_start, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], sp.rho, s);
-    launch_tile_order(N, ctx->inc_start, ctx->order, s);
+    if (sweep_uses_order()) launch_tile_order(N, ctx->inc_start, ctx->order, s);
     // impact trigger
     launch_rows(nc, 0, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
-    ctx->launches += 5;
+    ctx->launches += 6;
     CK(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(StepScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const bool impact = ctx->hsc->impact != 0 && nc > 0;

@@ -380,9 +380,22 @@ __global__ void k_compact(int64_t nc, const uint2 *__restrict__ cand, const uint
     if (m2 > lim * lim) { const double s = m2 > 0.0 ? lim / sqrt(m2) : 0.0; Pr = s * Pr; }
     Pa[c] = mkP4(Pn, Pt.x, Pt.y, Pt.z);
     Pb[c] = mkP4(Pr.x, Pr.y, Pr.z, 0);
-    if (!ext) atomicAdd(&sc->n_pp, 1u);
-    else if (ij.y & PARTNER_PLATE) atomicAdd(&sc->n_plate, 1u);
-    else atomicAdd(&sc->n_wall, 1u);
+}
+
+// per-kind contact counts: warp ballots, one atomic per warp and kind
+__global__ void k_count_kinds(int64_t nc, const uint2 *__restrict__ cij, StepScalars *sc)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t j = c < nc ? cij[c].y : 0u;
+    const bool ok = c < nc;
+    const unsigned pp = __ballot_sync(0xffffffffu, ok && !(j & PARTNER_EXT));
+    const unsigned pl = __ballot_sync(0xffffffffu, ok && (j & PARTNER_EXT) && (j & PARTNER_PLATE));
+    const unsigned wl = __ballot_sync(0xffffffffu, ok && (j & PARTNER_EXT) && !(j & PARTNER_PLATE));
+    if ((threadIdx.x & 31) == 0) {
+        if (pp) atomicAdd(&sc->n_pp, (unsigned)__popc(pp));
+        if (pl) atomicAdd(&sc->n_plate, (unsigned)__popc(pl));
+        if (wl) atomicAdd(&sc->n_wall, (unsigned)__popc(wl));
+    }
 }
 
 __global__ void k_inc_count(int64_t N, const uint32_t *__restrict__ co_start, const uint32_t *__restrict__ scan,
@@ -491,6 +504,8 @@ void launch_compact(int64_t nc, const uint2 *cand, const uint32_t *flag, const u
                     const DevBoundary *bnd, const SolveParams &sp, const P4 *Pca, const P4 *Pcb, uint2 *cij,
                     G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, StepScalars *sc, cudaStream_t s)
 { if (nc) k_compact<<<GRID(nc)>>>(nc, cand, flag, scan, pos, bnd, sp, Pca, Pcb, cij, geo, row, cdel, Pa, Pb, ccand, sc); }
+void launch_count_kinds(int64_t nc, const uint2 *cij, StepScalars *sc, cudaStream_t s)
+{ if (nc) k_count_kinds<<<GRID(nc)>>>(nc, cij, sc); }
 void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const uint32_t *scan, const uint32_t *ct_start,
                 const uint32_t *ct_list, const uint32_t *flag, uint32_t *cnt, uint32_t *inc_start, uint2 *inc,
                 void *scan_tmp, cudaStream_t s, long long *launches)

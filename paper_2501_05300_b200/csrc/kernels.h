@@ -23,6 +23,7 @@ void launch_narrow(int64_t nc, const uint2 *cand, const double4 *pos, const DevB
 void launch_compact(int64_t nc, const uint2 *cand, const uint32_t *flag, const uint32_t *scan, const double4 *pos,
                     const DevBoundary *bnd, const SolveParams &sp, const P4 *Pca, const P4 *Pcb, uint2 *cij,
                     G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, StepScalars *sc, cudaStream_t s);
+void launch_count_kinds(int64_t nc, const uint2 *cij, StepScalars *sc, cudaStream_t s);
 void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const uint32_t *scan, const uint32_t *ct_start,
                 const uint32_t *ct_list, const uint32_t *flag, uint32_t *cnt, uint32_t *inc_start, uint2 *inc,
                 void *scan_tmp, cudaStream_t s, long long *launches);
@@ -41,6 +42,7 @@ void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin
                   double4 *wout, const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
                   const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+bool sweep_uses_order();
 void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s);
 void launch_integrate(int64_t N, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
                       double rho, double *ke_part, StepScalars *sc, cudaStream_t s);

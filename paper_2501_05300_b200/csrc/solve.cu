@@ -551,6 +551,7 @@ __global__ void __launch_bounds__(TPT, SWEEP_MINB_PPT) k_sweep_ppt(int64_t N, co
     wout[i] = Wn;
 }
 
+bool sweep_uses_order() { return SWEEP_KERNEL == 2; }
 void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s)
 { if (N) k_tile_order<<<(unsigned)((N + TPT - 1) / TPT), TPT, 0, s>>>(N, inc_start, order); }
 
@@ -609,9 +610,9 @@ __global__ void k_integrate(int64_t N, double4 *__restrict__ pos, const double4 
                             const double4 *__restrict__ ang, const double4 *__restrict__ xref, double h, double rho,
                             double *__restrict__ ke_part, StepScalars *sc)
 {
-    __shared__ double sk[256];
+    __shared__ double sk[256], sd[256], sv[256];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    double ke = 0.0;
+    double ke = 0.0, disp = 0.0, vm = 0.0;
     if (i < N) {
         double4 p = pos[i];
         const double4 v = vel[i], w = ang[i];
@@ -621,28 +622,37 @@ __global__ void k_integrate(int64_t N, double4 *__restrict__ pos, const double4 
         pos[i] = p;
         const double4 r = xref[i];
         const double dx = p.x - r.x, dy = p.y - r.y, dz = p.z - r.z;
-        double disp = sqrt(dx * dx + dy * dy + dz * dz);
+        disp = sqrt(dx * dx + dy * dy + dz * dz);
         const double d = 2.0 * p.w;
         const double m = rho * 3.14159265358979323846 * d * d * d / 6.0, I = m * d * d / 10.0;
         const double v2 = v.x * v.x + v.y * v.y + v.z * v.z, w2 = w.x * w.x + w.y * w.y + w.z * w.z;
         ke = 0.5 * m * v2 + 0.5 * I * w2;
-        const double vm = sqrt(v2);
-        if (!isfinite(disp) || !isfinite(ke)) {
+        vm = sqrt(v2);
+        if (!isfinite(disp) || !isfinite(ke) || !isfinite(vm)) {
             atomicOr(&sc->nan_flag, 1u);
             disp = 0.0;
             ke = 0.0;
-        } else {
-            atomicMax(&sc->max_disp_bits, (unsigned long long)__double_as_longlong(disp));
-            atomicMax(&sc->max_v_bits, (unsigned long long)__double_as_longlong(vm));
+            vm = 0.0;
         }
     }
+    // block maxima first (non-negative doubles order like their bit patterns), one atomic per block
+    sd[threadIdx.x] = disp;
+    sv[threadIdx.x] = vm;
     sk[threadIdx.x] = ke;
     __syncthreads();
     for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sk[threadIdx.x] += sk[threadIdx.x + o];
+        if (threadIdx.x < o) {
+            sk[threadIdx.x] += sk[threadIdx.x + o];
+            sd[threadIdx.x] = fmax(sd[threadIdx.x], sd[threadIdx.x + o]);
+            sv[threadIdx.x] = fmax(sv[threadIdx.x], sv[threadIdx.x + o]);
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) ke_part[blockIdx.x] = sk[0];
+    if (threadIdx.x == 0) {
+        ke_part[blockIdx.x] = sk[0];
+        atomicMax(&sc->max_disp_bits, (unsigned long long)__double_as_longlong(sd[0]));
+        atomicMax(&sc->max_v_bits, (unsigned long long)__double_as_longlong(sv[0]));
+    }
 }
 
 __global__ void k_reduce_ke(const double *__restrict__ part, int64_t nb, StepScalars *sc)
