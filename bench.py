@@ -14,8 +14,10 @@ the bonds touch: N_c/N_p ~ 3 like a settled bed), relaxed under gravity for a fe
 steps (dt 1e-4, 20 sweeps) before the timed steps; see DESIGN.md §4 for the recipe.
 Inputs are larger than L2 (several GB per sweep) -> no L2 flush is needed between steps.
 
-N > 1: one process per GPU, each rank steps its own replica slab of the same size (weak
-scaling; the x-slab halo exchange is DESIGN.md §8 "next"), time = max over ranks.
+N > 1: one process per GPU, x-slab domain decomposition: the bed is
+N workload beds laid end to end along x (N x 8 m for config 4), rank r owns the slab
+[r L, (r+1) L) and exchanges ghost velocities with its neighbours over NCCL after every Jacobi
+sweep (weak scaling: per-GPU work fixed), time = max over ranks.
 
 --impl reference times the fp64 CPU oracle (oracle/) on a bounded sample of the same workload.
 """
@@ -55,6 +57,12 @@ def network_length(bands):
 def make_bed(wl, seed_offset=0, spacing=2.0):
     w = WORKLOADS[wl]
     return synth.banded_bed(w["dims"], w["bands"], w["seed"] + seed_offset, spacing=spacing, name=wl)
+
+
+def make_slab(wl, rank, world):
+    """Rank r's slab of the N-long bed: the workload bed (seed per rank) shifted by r L along x
+    (synth.shift_slab: gids unique over the job, box spanning all slabs)."""
+    return synth.shift_slab(make_bed(wl, seed_offset=rank), rank, world)
 
 
 def peaks():
@@ -182,9 +190,16 @@ def main():
     wl = args.workload
     w = WORKLOADS[wl]
     n_it = args.n_it or dem.plan_iterations(network_length(w["bands"]), 0.02)
-    bed_in = make_bed(wl, seed_offset=rank)
+    dcfg = None
+    if world > 1:
+        bed_in, slab = make_slab(wl, rank, world)
+        obj = [dem.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        dcfg = dict(rank=rank, world_size=world, slab=slab, transport="nccl", nccl_id=obj[0])
+    else:
+        bed_in = make_bed(wl)
     bed = dem.Bed(bed_in.x, bed_in.r, bed_in.v, bed_in.w, bed_in.gid, device=local,
-                  solver=dict(dt=1e-4, n_iter=20), box=dict(lo=bed_in.box_lo, hi=bed_in.box_hi))
+                  solver=dict(dt=1e-4, n_iter=20), box=dict(lo=bed_in.box_lo, hi=bed_in.box_hi), dist=dcfg)
     if args.settle > 0:
         bed.step(args.settle)             # coarse relaxation of the jammed packing (not timed)
     bed.set_solver(dt=w["dt"], n_iter=n_it)
@@ -219,9 +234,11 @@ def main():
     nc_mean = float(np.mean([r["n_contacts"] for r in reps]))
     imp_rate = float(np.mean([r["impact_fired"] for r in reps]))
     value = world * N * args.steps / (ms / 1e3)
-    contacts_per_s = world * nc_mean * args.steps / (ms / 1e3)
+    # reports are global with the decomposition (each contact counted once over the ranks)
+    contacts_per_s = (nc_mean if world > 1 else world * nc_mean) * args.steps / (ms / 1e3)
+    nc_rank = nc_mean / world if world > 1 else nc_mean
     sweep_ms = tm["ms_sweeps"] / max(tm["n_sweep_launches"], 1)
-    alg_bytes = ALG_B_PARTICLE * N + ALG_B_CONTACT * nc_mean
+    alg_bytes = ALG_B_PARTICLE * N + ALG_B_CONTACT * nc_rank
     pk = peaks()
     hbm = pk.get("hbm_gbs")
     achieved = alg_bytes / (sweep_ms / 1e3) / 1e9
@@ -238,12 +255,13 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "n_particles": N, "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "levels": len(w["bands"]),
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)" if world > 1
+                   else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)",
                    "precision": "fp64 state and row math; fp64 normals/rows, fp32 impulses"},
         "contacts_per_s": contacts_per_s,
-        "contact_sweeps_per_s": tm["contact_sweeps"] / (ms / 1e3) * world,
-        "roofline": {"bound": "hbm", "kernel": "k_sweep_tile", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "contact_sweeps_per_s": tm["contact_sweeps"] / (ms / 1e3) * world,   # rank-local contacts (incl. ghost copies)
+        "roofline": {"bound": "hbm", "kernel": "k_sweep_t2", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
                      "traffic_unit": "GB per launch (ncu dram read+write)",
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": sweep_ms,
@@ -258,8 +276,9 @@ def main():
     # e2e through the public API: per step H2D the drive inputs (wall velocities) and D2H the
     # whole particle state (a trajectory frame) into pinned host memory.
     if not args.no_e2e and not args.profile:
-        pin = {k: torch.empty((N, 3), dtype=torch.float64, pin_memory=True) for k in ("pos", "vel", "angvel")}
-        dev = {k: torch.empty((N, 3), dtype=torch.float64, device="cuda") for k in ("pos", "vel", "angvel")}
+        cap = int(1.2 * N) + 1024        # owned count drifts by migration across the slab faces
+        pin = {k: torch.empty((cap, 3), dtype=torch.float64, pin_memory=True) for k in ("pos", "vel", "angvel")}
+        dev = {k: torch.empty((cap, 3), dtype=torch.float64, device="cuda") for k in ("pos", "vel", "angvel")}
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
@@ -268,10 +287,10 @@ def main():
             for wall in (0, 1, 2, 3):
                 bed.drive_wall(wall, 0.0)            # H2D: boundary drive inputs
             bed.step(1)
-            bed.get_state_device(dev)
+            n_own = bed.get_state_device(dev)
             with torch.cuda.stream(stream):
                 for k in pin:
-                    pin[k].copy_(dev[k], non_blocking=True)
+                    pin[k][:n_own].copy_(dev[k][:n_own], non_blocking=True)
             stream.synchronize()
         T = time.perf_counter() - t0
         if dist:

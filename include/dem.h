@@ -101,14 +101,26 @@ typedef struct {
     dem_particles parts;
 } dem_bed_desc;
 
-/* Process / device plumbing (PyTorch provides memory, stream and process group). */
+/* Process / device plumbing (PyTorch provides memory, stream and process group) and the x-slab
+ * domain decomposition.  world_size > 1: each rank owns the
+ * particles of its slab [slab_lo, slab_hi) along x (ranks ordered by x, neighbours rank +- 1)
+ * and passes only those to dem_create_bed; the library keeps ghost copies of the neighbours'
+ * particles within 2 r_max + 2 skin of the shared faces, refreshes their velocities after every
+ * Jacobi sweep, and moves ownership at each rebuild.  create, step and destroy are then
+ * collective over the ranks. */
 typedef struct {
-    int32_t rank, world_size;  /* world_size must be 1 in this release (x-slab DD: DESIGN.md §8) */
-    const void *nccl_unique_id;        /* reserved, NULL */
+    int32_t rank, world_size;
+    const void *nccl_unique_id;        /* transport 0, world_size > 1: the 128-byte ncclUniqueId of
+                                          rank 0 (dem_nccl_unique_id), broadcast by the caller */
     void *cuda_stream;                 /* cudaStream_t all work is issued on; NULL -> own stream */
     void *(*alloc)(size_t bytes, void *alloc_ctx);   /* NULL -> cudaMalloc */
     void (*free)(void *ptr, void *alloc_ctx);
     void *alloc_ctx;
+    double slab_lo, slab_hi;           /* world_size > 1: this rank's slab along x, slab_lo < slab_hi */
+    int32_t transport;                 /* 0: NCCL, one process per GPU; 1: in-process loopback group */
+    int32_t pad0;
+    void *loopback;                    /* transport 1: dem_loopback_create handle shared by the ranks,
+                                          each rank driven by its own host thread */
 } dem_dist_desc;
 
 typedef struct {
@@ -175,7 +187,8 @@ typedef struct {
 
 /* Create a bed from particle arrays (P:155-161 beds are produced by synth/ generators).
  * Validates (DEM_ERR_INVALID): struct_size, material > 0, 0 <= nu < .5, dt > 0, n_iter >= 1,
- * radius > 0, unique gids, box lo < hi, world_size == 1.  Builds the first candidate list. */
+ * radius > 0, unique gids, box lo < hi, decomposition fields (world_size > 1: particles inside the
+ * slab; DEM_ERR_NCCL if the transport cannot be set up).  Builds the first candidate list. */
 dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, dem_ctx **out);
 
 /* Advance n_steps >= 1 time steps.  `last` (may be NULL) gets the report of the
@@ -215,6 +228,29 @@ dem_status dem_drive_wall(dem_ctx *ctx, int32_t wall, double normal_velocity);
 dem_status dem_set_timing(dem_ctx *ctx, int32_t enable);
 dem_status dem_get_timing(dem_ctx *ctx, dem_timing *out);
 dem_status dem_reset_timing(dem_ctx *ctx);
+
+/* Diagnostic (not on the stepping path): time n >= 1 Jacobi sweeps of sweep-kernel `variant`
+ * (0 shipped tile kernel k_sweep_t2, 1 cp.async pipeline, 2 particle-per-thread, 3 tile with L1
+ * prefetch, 4 first tile kernel; 10/11/12 the geometry-recomputing kernels of sweep5.cu; 20/21
+ * tile-paired with 128/256-particle tiles, 30 slot sweep; 41-43 timing experiments) on the
+ * last step's contacts, from the current velocities and the last step's final impulses.
+ * Outputs: device ms per sweep, and max |v - v_ref| / max |v_ref| after n sweeps against
+ * variant 0.  The particle state and contact getters are unchanged.  DEM_ERR_STATE before any
+ * step; DEM_ERR_INVALID for n < 1. */
+dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms_per_sweep, double *max_dv_rel);
+
+/* Owned particles of this rank (all particles with world_size 1), and owned + ghost copies. */
+int64_t dem_num_particles(const dem_ctx *ctx);
+int64_t dem_num_local(const dem_ctx *ctx);
+
+/* x-slab decomposition plumbing.  dem_nccl_unique_id writes a fresh 128-byte ncclUniqueId
+ * (rank 0 calls it; DEM_ERR_NCCL if libnccl.so.2 cannot be loaded).  dem_loopback_create
+ * returns a group through which world_size ranks of ONE process exchange ghosts with device
+ * copies after host barriers (each rank's calls from its own thread); destroy it after every
+ * rank's dem_destroy. */
+dem_status dem_nccl_unique_id(void *out128);
+void *dem_loopback_create(int32_t world_size);
+void dem_loopback_destroy(void *group);
 
 /* The cudaStream_t the context issues its work on. */
 void *dem_stream(dem_ctx *ctx);

@@ -79,6 +79,43 @@ __host__ __device__ __forceinline__ double rndP(double x)
 #endif
 }
 
+// Impulse storage: p_ld converts a stored value to double (exact), p_rnd rounds a double to the
+// storage precision, writes it to the slot and returns it as a double (the value the velocity
+// update must use so that momentum stays consistent with the stored impulses).  (An integer
+// bit-manipulation version that keeps the F2F conversions off the XU pipe was measured: the XU
+// pipe was not the limiter and it cost 36 % more instructions.)
+#ifdef DEM_P64
+__device__ __forceinline__ double p_ld(double v) { return v; }
+__device__ __forceinline__ double p_rnd(double x, double &st)
+{
+    st = x;
+    return x;
+}
+#else
+__device__ __forceinline__ double p_ld(float f) { return (double)f; }
+__device__ __forceinline__ double p_rnd(double x, float &st)
+{
+    st = (float)x;
+    return (double)st;
+}
+#endif
+
+// 256-bit global accesses (LDG.E.256 / STG.E.256 on sm_100a): one instruction and one sector
+// per lane for a 32-byte record, instead of two 128-bit accesses that each touch the sector.
+// ld4g is the non-coherent path: only for data the kernel does not write.
+__device__ __forceinline__ double4 ld4g(const double4 *p)
+{
+    double4 v;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float4 ld4g(const float4 *p) { return __ldg(p); }
+__device__ __forceinline__ void st4g(double4 *p, const double4 v)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z), "d"(v.w)
+                 : "memory");
+}
+
 struct GridLevel {
     double ox, oy, oz;     // origin
     double cell;           // cell edge = 2 r_max(L) + skin
@@ -123,7 +160,14 @@ struct SolveParams {
     double g[3];
     int rolling_dims;
     int hertz;             // 1: e_H = 5/4 (sqrt(delta)); 0: linear
+    double Cs;             // Sigma-hat constant: hertz 12 Ups/(h^2 e_H E*), linear 4 Ups/(h^2 e_H k_lin)
 };
+
+// SPOOK regularisation of the Hertz-mapped normal row in impulse units (reading R4):
+// Sigma-hat = 4 Ups/(h^2 e_H k_n delta^(2 e_H - 2)), k_n = E* sqrt(d*)/3, d* = 2 R*
+//           = Cs / sqrt(2 R* delta)                       (e_H = 5/4)
+// linear model (reading R3): Sigma-hat = 4 Ups/(h^2 e_H k_lin) = Cs
+#define spook_sigma(sp, Rs, delta) ((sp).hertz ? (sp).Cs * rsqrt64(2.0 * (Rs) * (delta)) : (sp).Cs)
 
 // per-step scalars read back by the host once or twice per step
 struct StepScalars {
@@ -151,12 +195,97 @@ __device__ __forceinline__ d3 cross(d3 a, d3 b)
     return d3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 
+// fp64 reciprocal: MUFU.RCP64H estimate + two Newton steps (relative error ~1e-16; operands
+// are positive and finite: split weights, regularised diagonals)
+__device__ __forceinline__ double rcp64(double x)
+{
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    double e = fma(-x, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-x, r, 1.0);
+    return fma(r, e, r);
+}
+
+
+// 1/sqrt(x) for x > 0: MUFU.RSQ64H estimate + two fp64 Newton steps (relative error ~1e-16)
+__device__ __forceinline__ double rsqrt64(double x)
+{
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = r * (1.5 - 0.5 * x * r * r);
+    return r * (1.5 - 0.5 * x * r * r);
+}
+
+// R* = r_a r_b / (r_a + r_b) (d* = 2 R*): one definition for every kernel
+__device__ __forceinline__ double rstar(double ra, double rb) { return ra * rb * rcp64(ra + rb); }
+
+// Geometry of an active particle pair (d2 > 0 already established by the exact predicate):
+// n = (x_b - x_a)/d, delta = r_a + r_b - d.  One instruction sequence used by the narrow phase
+// and re-evaluated by the sweeps from the same positions, so both give bit-identical n, delta.
+__device__ __forceinline__ void pair_geom(const double4 A, const double4 B, d3 &n, double &delta)
+{
+    const double dx = __dsub_rn(B.x, A.x), dy = __dsub_rn(B.y, A.y), dz = __dsub_rn(B.z, A.z);
+    const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+    const double id = rsqrt64(d2);
+    n = d3{dx * id, dy * id, dz * id};
+    delta = __dsub_rn(__dadd_rn(A.w, B.w), __dmul_rn(d2, id));
+}
+
 // exact-sequence fp64 helpers (no FMA contraction) for predicates shared bit-for-bit with
 // the fixed IEEE operation order of DESIGN.md reading R14
 __device__ __forceinline__ double dist2_rn(double dx, double dy, double dz)
 {
     return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
+
+// Wall or plate-box contact of particle A (code = partner & ~PARTNER_EXT).  Walls: signed
+// distance s = (X - p_w).n_w < r, n = -n_w, delta = r - s.  Plate boxes: closest point q of the
+// box, n = (q - X)/|q - X|, delta = r - |q - X|; centre inside (reading R19): exit through the
+// nearest face, delta = r + depth.  Returns 1 in contact, 0 not.  Also re-evaluated by the
+// sweeps (boundary positions are fixed during a step's sweeps).
+__device__ __forceinline__ int ext_geom(const double4 A, uint32_t code, const DevBoundary *bnd, d3 &n, double &delta)
+{
+    const double X[3] = {A.x, A.y, A.z};
+    const double r = A.w;
+    if (!(code & PARTNER_PLATE)) {
+        const int w = (int)code;
+        const double s = __dadd_rn(__dadd_rn(__dmul_rn(__dsub_rn(X[0], bnd->wp[w][0]), bnd->wn[w][0]),
+                                             __dmul_rn(__dsub_rn(X[1], bnd->wp[w][1]), bnd->wn[w][1])),
+                                   __dmul_rn(__dsub_rn(X[2], bnd->wp[w][2]), bnd->wn[w][2]));
+        if (!(s < r)) return 0;
+        n = d3{-bnd->wn[w][0], -bnd->wn[w][1], -bnd->wn[w][2]};
+        delta = __dsub_rn(r, s);
+        return 1;
+    }
+    const int p = (code >> 4) & 0xF, b = code & 0xF;
+    double lo[3], hi[3], dq[3];
+    for (int k = 0; k < 3; k++) {
+        lo[k] = __dadd_rn(bnd->ppos[p][k], bnd->lo[p][b][k]);
+        hi[k] = __dadd_rn(bnd->ppos[p][k], bnd->hi[p][b][k]);
+        const double q = X[k] < lo[k] ? lo[k] : (X[k] > hi[k] ? hi[k] : X[k]);
+        dq[k] = __dsub_rn(q, X[k]);
+    }
+    const double d2 = dist2_rn(dq[0], dq[1], dq[2]);
+    if (d2 > 0.0) {
+        if (!(d2 < __dmul_rn(r, r))) return 0;
+        const double d = __dsqrt_rn(d2);
+        n = d3{__ddiv_rn(dq[0], d), __ddiv_rn(dq[1], d), __ddiv_rn(dq[2], d)};
+        delta = __dsub_rn(r, d);
+        return 1;
+    }
+    double best = INFINITY, sg = 1.0;
+    int bk = 0;
+    for (int k = 0; k < 3; k++) {
+        const double dl = __dsub_rn(X[k], lo[k]), dh = __dsub_rn(hi[k], X[k]);
+        if (dl < best) { best = dl; bk = k; sg = 1.0; }
+        if (dh < best) { best = dh; bk = k; sg = -1.0; }
+    }
+    n = d3{bk == 0 ? sg : 0.0, bk == 1 ? sg : 0.0, bk == 2 ? sg : 0.0};
+    delta = __dadd_rn(r, best);
+    return 1;
+}
+
 
 __host__ __device__ __forceinline__ int level_of(double r, double rmin, int nlev)
 {

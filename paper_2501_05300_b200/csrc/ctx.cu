@@ -19,6 +19,7 @@
 #include "../../include/dem.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "dist.h"
 
 static thread_local std::string g_create_err;
 
@@ -94,6 +95,15 @@ struct dem_ctx {
     bool need_rebuild = true;
     bool have_step = false;
     dem_step_report last{};
+    // x-slab decomposition: owned particles [0, N_own), ghosts after
+    int rank = 0, G = 1;
+    Transport *tp = nullptr;
+    double slab_lo = -INFINITY, slab_hi = INFINITY, band_w = 0.0;
+    int64_t N_own = 0, capN = 0;
+    uint8_t *own = nullptr;      // per local particle: 1 owned, 0 ghost (world_size > 1 only)
+    int64_t n_send[2] = {0, 0}, n_recv[2] = {0, 0}, cap_halo[2] = {0, 0};
+    uint32_t *send_pre[2] = {nullptr, nullptr}, *send_idx[2] = {nullptr, nullptr}, *recv_idx[2] = {nullptr, nullptr};
+    double4 *hs[2] = {nullptr, nullptr}, *hr[2] = {nullptr, nullptr};
     // timing
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -102,6 +112,7 @@ struct dem_ctx {
 };
 
 // ------------------------------------------------------------------ helpers
+#define OWN(ctx) ((ctx)->G > 1 ? (const uint8_t *)(ctx)->own : (const uint8_t *)nullptr)
 #define CK(call)                                                                      \
     do {                                                                              \
         cudaError_t e_ = (call);                                                      \
@@ -192,14 +203,22 @@ static void setup_solve_params(dem_ctx *ctx)
     for (int k = 0; k < 3; k++) sp.g[k] = so.gravity[k];
     sp.rolling_dims = so.rolling_dims == 2 ? 2 : 3;
     sp.hertz = so.hertz_exp == 1.0 ? 0 : 1;
+    sp.Cs = sp.hertz ? 12.0 * sp.Ups / (sp.h * sp.h * sp.e_H * sp.Es) : 4.0 * sp.Ups / (sp.h * sp.h * sp.e_H * sp.k_lin);
 }
 
 // radii -> levels (factor-2 size classes), per-level r_max, skin
-static void setup_levels(dem_ctx *ctx, const std::vector<double> &r)
+static dem_status setup_levels(dem_ctx *ctx, const std::vector<double> &r)
 {
     double rmin = INFINITY, rmax = 0;
     for (double x : r) { rmin = std::min(rmin, x); rmax = std::max(rmax, x); }
-    if (r.empty()) { rmin = 1e-3; rmax = 1e-3; }
+    if (ctx->G > 1) {
+        // every rank takes the same size classes, skin and ghost band (global radius range)
+        double v[2] = {-rmin, rmax};
+        if (!ctx->tp->allreduce_f64(v, 2, 1, ctx->s, ctx->err)) return DEM_ERR_NCCL;
+        rmin = -v[0];
+        rmax = v[1];
+    }
+    if (!(rmin <= rmax)) { rmin = 1e-3; rmax = 1e-3; }
     int nlev = 1;
     double t = rmin;
     while (nlev < DEM_MAX_LEVELS && rmax >= t * 2.0) { t *= 2.0; nlev++; }
@@ -210,9 +229,18 @@ static void setup_levels(dem_ctx *ctx, const std::vector<double> &r)
         ctx->rmax_lv[L] = std::max(ctx->rmax_lv[L], x);
         ctx->lv_present[L] = true;
     }
+    if (ctx->G > 1) {
+        // cell sizes from the global per-level maxima: ghosts and migrants of any size class fit
+        if (!ctx->tp->allreduce_f64(ctx->rmax_lv, DEM_MAX_LEVELS, 1, ctx->s, ctx->err)) return DEM_ERR_NCCL;
+        for (int L = 0; L < DEM_MAX_LEVELS; L++) ctx->lv_present[L] = ctx->rmax_lv[L] > 0.0;
+    }
     ctx->grid.nlev = nlev;
     ctx->grid.rmin = rmin;
     ctx->grid.skin = ctx->sol.skin > 0 ? ctx->sol.skin : 0.1 * rmin;
+    // ghost band: any partner of an owned particle within r_a + r_b + skin, plus one skin of margin
+    // so that pairs about to meet carry their history across the faces
+    ctx->band_w = 2.0 * rmax + 2.0 * ctx->grid.skin;
+    return DEM_OK;
 }
 
 static void setup_walls(dem_ctx *ctx)
@@ -237,25 +265,31 @@ static dem_status upload_boundary(dem_ctx *ctx)
     return DEM_OK;
 }
 
-// allocate particle-sized arrays
-static dem_status alloc_particles(dem_ctx *ctx)
+// (re)allocate the particle-sized arrays for capacity cap (contents are not preserved)
+static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
 {
-    const size_t N = (size_t)ctx->N + 1;
-    TRY(A(ctx, &ctx->pos, N)); TRY(A(ctx, &ctx->pos2, N));
-    TRY(A(ctx, &ctx->vel[0], N)); TRY(A(ctx, &ctx->vel[1], N));
-    TRY(A(ctx, &ctx->ang[0], N)); TRY(A(ctx, &ctx->ang[1], N));
-    TRY(A(ctx, &ctx->vel2, N)); TRY(A(ctx, &ctx->ang2, N));
-    TRY(A(ctx, &ctx->xref, N)); TRY(A(ctx, &ctx->pos_prev, N));
-    TRY(A(ctx, &ctx->vel_prev, N)); TRY(A(ctx, &ctx->ang_prev, N));
-    TRY(A(ctx, &ctx->gid, N)); TRY(A(ctx, &ctx->gid2, N)); TRY(A(ctx, &ctx->gid_sorted, N));
-    TRY(A(ctx, &ctx->co_start, N + 1)); TRY(A(ctx, &ctx->ct_cnt, N + 1)); TRY(A(ctx, &ctx->ct_start, N + 1));
-    TRY(A(ctx, &ctx->ct_cursor, N + 1)); TRY(A(ctx, &ctx->inc_cnt, N + 1)); TRY(A(ctx, &ctx->inc_start, N + 1)); TRY(A(ctx, &ctx->order, N + 1));
+    double4 **d4[] = {&ctx->pos, &ctx->pos2, &ctx->vel[0], &ctx->vel[1], &ctx->ang[0], &ctx->ang[1], &ctx->vel2,
+                      &ctx->ang2, &ctx->xref, &ctx->pos_prev, &ctx->vel_prev, &ctx->ang_prev};
+    uint32_t **u4[] = {&ctx->gid, &ctx->gid2, &ctx->gid_sorted, &ctx->co_start, &ctx->ct_cnt, &ctx->ct_start,
+                       &ctx->ct_cursor, &ctx->inc_cnt, &ctx->inc_start, &ctx->order};
+    const size_t N = (size_t)cap + 1;
+    for (auto q : d4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N)); }
+    for (auto q : u4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N + 1)); }
+    dfree(ctx, ctx->ke_part);
+    ctx->ke_part = nullptr;
+    dfree(ctx, ctx->own);
+    ctx->own = nullptr;
+    TRY(A(ctx, &ctx->own, N));
     TRY(A(ctx, &ctx->ke_part, N / 256 + 2));
-    TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
-    TRY(A(ctx, &ctx->db, 1));
-    TRY(A(ctx, &ctx->pacc, 3 * DEM_MAX_PLATES));
-    TRY(A(ctx, &ctx->pcount, DEM_MAX_PLATES));
-    TRY(A(ctx, &ctx->dsc, 1));
+    if (!ctx->lvbox) {
+        TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
+        TRY(A(ctx, &ctx->db, 1));
+        TRY(A(ctx, &ctx->pacc, 3 * DEM_MAX_PLATES));
+        TRY(A(ctx, &ctx->pcount, DEM_MAX_PLATES));
+        TRY(A(ctx, &ctx->dsc, 1));
+    }
+    ctx->capN = cap;
+    ctx->cap_keys = 0;          // key/scan scratch is sized from capN at the next ensure_keys
     return DEM_OK;
 }
 
@@ -384,6 +418,12 @@ static dem_status compute_grid(dem_ctx *ctx)
     }
     for (int L = ctx->nlev; L < DEM_MAX_LEVELS; L++) g.lv[L].present = 0;
     g.bits = bits;
+    if (getenv("DEM_DEBUG")) {
+        for (int L = 0; L < ctx->nlev; L++)
+            fprintf(stderr, "[dem r%d N=%lld own=%lld] level %d cell %.6g n %d %d %d o %.6g %.6g %.6g bits %d rmax %.6g\n",
+                    ctx->rank, (long long)ctx->N, (long long)ctx->N_own, L, g.lv[L].cell, g.lv[L].nx, g.lv[L].ny,
+                    g.lv[L].nz, g.lv[L].ox, g.lv[L].oy, g.lv[L].oz, bits, g.lv[L].rmax);
+    }
     ctx->ncells = off;
     if (off > ctx->cap_cells) {
         uint64_t cap = off + off / 4 + 64;
@@ -420,21 +460,180 @@ static dem_status export_history(dem_ctx *ctx)
         ctx->launches += 2;
     }
     ctx->nh = nh;
+    if (getenv("DEM_DEBUG")) fprintf(stderr, "[dem r%d] export history: ncand %lld nh %u\n", ctx->rank, (long long)nc, nh);
+    return DEM_OK;
+}
+
+// ------------------------------------------------------------------ x-slab decomposition
+static dem_status grow_halo(dem_ctx *ctx, int k, int64_t n)
+{
+    if (n <= ctx->cap_halo[k]) return DEM_OK;
+    const int64_t cap = n + n / 4 + 256;
+    TRY(regrow(ctx, &ctx->send_pre[k], cap)); TRY(regrow(ctx, &ctx->send_idx[k], cap)); TRY(regrow(ctx, &ctx->recv_idx[k], cap));
+    TRY(regrow(ctx, &ctx->hs[k], 4 * cap)); TRY(regrow(ctx, &ctx->hr[k], 4 * cap));
+    ctx->cap_halo[k] = cap;
+    return DEM_OK;
+}
+
+static dem_status xchg(dem_ctx *ctx, const void *const snd[2], const size_t sb[2], void *const rcv[2], const size_t rb[2])
+{
+    if (!ctx->tp->exchange(snd, sb, rcv, rb, ctx->s, ctx->err)) return DEM_ERR_NCCL;
+    return DEM_OK;
+}
+
+// ghost velocities (v, c/m; w, c/I) from their owners, after every update of the velocities
+static dem_status halo(dem_ctx *ctx, double4 *vel, double4 *ang)
+{
+    if (ctx->G == 1) return DEM_OK;
+    for (int k = 0; k < 2; k++) launch_pack_halo(ctx->n_send[k], ctx->send_idx[k], vel, ang, ctx->hs[k], ctx->s);
+    const void *snd[2] = {ctx->hs[0], ctx->hs[1]};
+    void *rcv[2] = {ctx->hr[0], ctx->hr[1]};
+    const size_t sb[2] = {(size_t)ctx->n_send[0] * 64, (size_t)ctx->n_send[1] * 64};
+    const size_t rb[2] = {(size_t)ctx->n_recv[0] * 64, (size_t)ctx->n_recv[1] * 64};
+    TRY(xchg(ctx, snd, sb, rcv, rb));
+    for (int k = 0; k < 2; k++) launch_unpack_halo(ctx->n_recv[k], ctx->recv_idx[k], ctx->hr[k], vel, ang, ctx->s);
+    ctx->launches += 4;
+    return DEM_OK;
+}
+
+// At a rebuild: ownership by slab, then the ghost bands of both neighbours.  A particle that
+// crossed into a neighbour's slab was a ghost there with a bit-identical state (ghosts move with
+// their owners' velocities), so it is simply owned there from now on: no particle is shipped
+// except as a band copy.  Owned particles come first, ghosts after (left band, right band).
+static dem_status redistribute(dem_ctx *ctx)
+{
+    cudaStream_t s = ctx->s;
+    const int64_t N = ctx->N;
+    uint32_t *flag = nullptr, *scan = nullptr, *idx = nullptr, *tg = nullptr;
+    double4 *tp = nullptr, *tv = nullptr, *tw = nullptr;
+    TRY(A(ctx, &flag, N + 2)); TRY(A(ctx, &scan, N + 2)); TRY(A(ctx, &idx, N + 2)); TRY(A(ctx, &tg, N + 2));
+    TRY(A(ctx, &tp, N + 1)); TRY(A(ctx, &tv, N + 1)); TRY(A(ctx, &tw, N + 1));
+    // 1. owned = x in [slab_lo, slab_hi), compacted in the current order
+    // the outer ranks own everything beyond the box faces too: no particle can be orphaned
+    const double own_lo = ctx->rank == 0 ? -INFINITY : ctx->slab_lo;
+    const double own_hi = ctx->rank == ctx->G - 1 ? INFINITY : ctx->slab_hi;
+    launch_slab_flags(N, ctx->pos, own_lo, own_hi, flag, s);
+    scan_u32(flag, scan, N, ctx->scan_tmp, s, &ctx->launches);
+    uint32_t n_own = 0;
+    CK(cudaMemcpyAsync(&n_own, scan + N, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    launch_compact_idx(N, flag, scan, idx, s);
+    launch_gather_state(n_own, idx, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->gid, tp, tv, tw, tg, s);
+    // 2. bands of the owned set facing each neighbour
+    const int has[2] = {ctx->rank > 0, ctx->rank < ctx->G - 1};
+    uint32_t *fb[2] = {flag, idx};                    // reuse the scratch (n_own <= N)
+    launch_band_flags(n_own, tp, ctx->slab_lo + ctx->band_w, ctx->slab_hi - ctx->band_w, has[0], has[1], fb[0], fb[1], s);
+    uint32_t nsend[2] = {0, 0};
+    uint32_t *bscan2 = nullptr;
+    TRY(A(ctx, &bscan2, N + 2));
+    uint32_t *bscan[2] = {scan, bscan2};
+    for (int k = 0; k < 2; k++) {
+        scan_u32(fb[k], bscan[k], n_own, ctx->scan_tmp, s, &ctx->launches);
+        CK(cudaMemcpyAsync(&nsend[k], bscan[k] + n_own, 4, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    // 3. band sizes to the neighbours
+    unsigned long long *cnt = nullptr;
+    TRY(A(ctx, &cnt, 4));
+    const unsigned long long hc[2] = {nsend[0], nsend[1]};
+    CK(cudaMemcpyAsync(cnt, hc, 16, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(cnt + 2, 0, 16, s));
+    {
+        const void *snd[2] = {cnt, cnt + 1};
+        void *rcv[2] = {cnt + 2, cnt + 3};
+        const size_t sb[2] = {has[0] ? 8u : 0u, has[1] ? 8u : 0u};
+        TRY(xchg(ctx, snd, sb, rcv, sb));
+    }
+    unsigned long long rc[2] = {0, 0};
+    CK(cudaMemcpyAsync(rc, cnt + 2, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, cnt);
+    // 4. band lists (halo buffers sized for both directions first: growing reallocates them)
+    for (int k = 0; k < 2; k++) {
+        TRY(grow_halo(ctx, k, std::max<int64_t>(nsend[k], (int64_t)rc[k])));
+        launch_compact_idx(n_own, fb[k], bscan[k], ctx->send_pre[k], s);
+        launch_pack_band(nsend[k], ctx->send_pre[k], tp, tv, tw, tg, ctx->hs[k], s);
+    }
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, bscan2);
+    {
+        const void *snd[2] = {ctx->hs[0], ctx->hs[1]};
+        void *rcv[2] = {ctx->hr[0], ctx->hr[1]};
+        const size_t sb[2] = {(size_t)nsend[0] * 128, (size_t)nsend[1] * 128};
+        const size_t rb[2] = {(size_t)rc[0] * 128, (size_t)rc[1] * 128};
+        TRY(xchg(ctx, snd, sb, rcv, rb));
+    }
+    // 5. new local set: owned, left ghosts, right ghosts
+    const int64_t Nn = (int64_t)n_own + (int64_t)rc[0] + (int64_t)rc[1];
+    if (Nn > ctx->capN) {
+        CK(cudaStreamSynchronize(s));
+        TRY(alloc_particles(ctx, Nn + Nn / 4 + 1024));
+    }
+    ctx->cur = 0;
+    CK(cudaMemcpyAsync(ctx->pos, tp, n_own * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->vel[0], tv, n_own * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->ang[0], tw, n_own * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ctx->gid, tg, n_own * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    int64_t off = n_own;
+    for (int k = 0; k < 2; k++) {
+        launch_unpack_band(rc[k], ctx->hr[k], ctx->pos + off, ctx->vel[0] + off, ctx->ang[0] + off, ctx->gid + off, s);
+        off += rc[k];
+    }
+    CK(cudaStreamSynchronize(s));
+    for (void *q : {(void *)flag, (void *)scan, (void *)idx, (void *)tg, (void *)tp, (void *)tv, (void *)tw}) dfree(ctx, q);
+    ctx->N = Nn;
+    ctx->N_own = n_own;
+    for (int k = 0; k < 2; k++) { ctx->n_send[k] = nsend[k]; ctx->n_recv[k] = (int64_t)rc[k]; }
+    ctx->launches += 8;
+    return DEM_OK;
+}
+
+// after the rebuild's sort (perm: new -> old): owned flags, halo index lists in sorted positions,
+// owned gids in order (owned and ghost particles stay interleaved in the Morton order)
+static dem_status finish_decomposition(dem_ctx *ctx, const uint32_t *perm)
+{
+    cudaStream_t s = ctx->s;
+    const int64_t N = ctx->N;
+    uint32_t *inv = nullptr;
+    TRY(A(ctx, &inv, N + 1));
+    launch_own_flags(N, perm, (uint32_t)ctx->N_own, ctx->own, s);
+    launch_inv_perm(N, perm, inv, s);
+    int64_t off = ctx->N_own;
+    for (int k = 0; k < 2; k++) {
+        launch_map_idx(ctx->n_send[k], ctx->send_pre[k], 0u, inv, ctx->send_idx[k], s);
+        launch_map_idx(ctx->n_recv[k], nullptr, (uint32_t)off, inv, ctx->recv_idx[k], s);
+        off += ctx->n_recv[k];
+    }
+    // gid-sorted owned ids (getters report owned particles in gid order)
+    if (ctx->N_own) {
+        launch_gid_keys(N, ctx->gid, ctx->own, ctx->keys[0], ctx->vals[0], s);
+        radix_sort_u64(ctx->keys, ctx->vals, N, 33, ctx->sort_tmp, s, &ctx->launches);
+        launch_keys_to_u32(ctx->N_own, ctx->keys[0], ctx->gid_sorted, s);
+    }
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, inv);
+    ctx->launches += 6;
     return DEM_OK;
 }
 
 static dem_status rebuild(dem_ctx *ctx)
 {
     cudaStream_t s = ctx->s;
-    const int64_t N = ctx->N;
     if (!ctx->hist_pending) TRY(export_history(ctx));
     ctx->hist_pending = false;
+    if (ctx->G > 1) {
+        TRY(ensure_keys(ctx, std::max<int64_t>(ctx->N, 1)));
+        TRY(redistribute(ctx));
+    } else {
+        ctx->N_own = ctx->N;
+    }
+    const int64_t N = ctx->N;
     TRY(ensure_keys(ctx, std::max<int64_t>(N, 1)));
     TRY(compute_grid(ctx));
     // (a) level + Morton keys, stable radix sort, permutation of the SoA state
     if (N) {
         launch_keys(N, ctx->pos, ctx->grid, ctx->keys[0], ctx->vals[0], s);
-        int nbits = 3 * ctx->grid.bits + 3;
+        const int nbits = 3 * ctx->grid.bits + 3;
         radix_sort_u64(ctx->keys, ctx->vals, N, nbits, ctx->sort_tmp, s, &ctx->launches);
         launch_permute(N, ctx->vals[0], ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->gid, ctx->pos2, ctx->vel2,
                        ctx->ang2, ctx->gid2, s);
@@ -447,6 +646,7 @@ static dem_status rebuild(dem_ctx *ctx)
         CK(cudaMemsetAsync(ctx->cstart, 0, ctx->ncells * sizeof(uint32_t), s));
         CK(cudaMemsetAsync(ctx->cend, 0, ctx->ncells * sizeof(uint32_t), s));
         launch_cells(N, ctx->keys[0], ctx->grid, ctx->cstart, ctx->cend, s);
+        if (ctx->G > 1) TRY(finish_decomposition(ctx, ctx->vals[0]));   // reuses keys/vals after the cells
         // multi-level broad phase: count, scan, fill
         launch_broad(false, N, ctx->pos, ctx->grid, ctx->cstart, ctx->cend, ctx->db, ctx->co_start, nullptr, s);
         ctx->launches += 2;
@@ -480,7 +680,6 @@ static dem_status rebuild(dem_ctx *ctx)
 static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
 {
     cudaStream_t s = ctx->s;
-    const int64_t N = ctx->N;
     const SolveParams &sp = ctx->sp;
     std::memset(rep, 0, sizeof(*rep));
     tstart(ctx, 0);
@@ -488,6 +687,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         TRY(rebuild(ctx));
         rep->rebuilt = 1;
     }
+    const int64_t N = ctx->N;          // after the rebuild: the decomposition changes the local count
     tstart(ctx, 1);
     const DevBoundary hb_prev = ctx->hb;
     if (N) {
@@ -507,17 +707,23 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     ctx->nc = nc;
     launch_compact(ncand, ctx->cand, ctx->cflag, ctx->cscan, ctx->pos, ctx->db, sp, ctx->Pca, ctx->Pcb, ctx->cij,
                    ctx->geo, ctx->row, ctx->cdel, ctx->Pwa, ctx->Pwb, ctx->ccand, ctx->dsc, s);
-    launch_count_kinds(nc, ctx->cij, ctx->dsc, s);
+    launch_count_kinds(nc, OWN(ctx), ctx->cij, ctx->gid, ctx->dsc, s);
     launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->inc_cnt,
                ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
     launch_prepare(N, ctx->inc_start, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], sp.rho, s);
+    TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));      // ghosts' weights c/m, c/I from their owners
     if (sweep_uses_order()) launch_tile_order(N, ctx->inc_start, ctx->order, s);
     // impact trigger
     launch_rows(nc, 0, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
     ctx->launches += 6;
     CK(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(StepScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    const bool impact = ctx->hsc->impact != 0 && nc > 0;
+    bool impact = ctx->hsc->impact != 0 && nc > 0;
+    if (ctx->G > 1) {
+        double f = impact ? 1.0 : 0.0;
+        if (!ctx->tp->allreduce_f64(&f, 1, 1, s, ctx->err)) return DEM_ERR_NCCL;
+        impact = f > 0.0;
+    }
     tstart(ctx, 2);
     const int n_imp = ctx->sol.n_iter_impact > 0 ? ctx->sol.n_iter_impact : ctx->sol.n_iter;
     if (impact) {
@@ -530,6 +736,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
                          ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row_imp, ctx->Pa[pi],
                          ctx->Pb[pi], ctx->Pa[pi ^ 1], ctx->Pb[pi ^ 1], ctx->db, sp, s);
             ctx->cur ^= 1;
+            TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
         }
         ctx->launches += n_imp;
         ctx->tm.n_sweep_launches += n_imp;
@@ -543,6 +750,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
                  nullptr, ctx->db, sp, s);
     ctx->cur ^= 1;
     ctx->launches += 2;
+    TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
     tstart(ctx, 3);
     const int n_it = ctx->sol.n_iter;
     const P4 *pin_a = ctx->Pwa, *pin_b = ctx->Pwb;
@@ -552,6 +760,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
                      ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
                      ctx->db, sp, s);
         ctx->cur ^= 1;
+        TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
         pin_a = oa;
         pin_b = ob;
     }
@@ -563,15 +772,48 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     ctx->Pfa = (P4 *)pin_a;
     ctx->Pfb = (P4 *)pin_b;
     // integrate, plates and walls
-    launch_integrate(N, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->xref, sp.h, sp.rho, ctx->ke_part, ctx->dsc, s);
-    launch_plates(nc, ctx->cij, ctx->geo, ctx->Pfa, ctx->pacc, ctx->pcount, ctx->db, sp.h, ctx->dsc, s);
+    launch_integrate(N, OWN(ctx), ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->xref, sp.h, sp.rho, ctx->ke_part,
+                     ctx->dsc, s);
+    launch_plate_sum(nc, OWN(ctx), ctx->cij, ctx->geo, ctx->Pfa, ctx->pacc, ctx->pcount, s);
+    if (ctx->G > 1 && ctx->hb.n_plates > 0) {
+        // plate reactions: exact int64 sums over the ranks (each contact counted by its owner)
+        unsigned long long acc[3 * DEM_MAX_PLATES];
+        unsigned int pc[DEM_MAX_PLATES];
+        CK(cudaMemcpyAsync(acc, ctx->pacc, sizeof(acc), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(pc, ctx->pcount, sizeof(pc), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        long long v[4 * DEM_MAX_PLATES];
+        for (int q = 0; q < 3 * DEM_MAX_PLATES; q++) v[q] = (long long)acc[q];
+        for (int q = 0; q < DEM_MAX_PLATES; q++) v[3 * DEM_MAX_PLATES + q] = pc[q];
+        if (!ctx->tp->allreduce_i64(v, 4 * DEM_MAX_PLATES, 0, s, ctx->err)) return DEM_ERR_NCCL;
+        for (int q = 0; q < 3 * DEM_MAX_PLATES; q++) acc[q] = (unsigned long long)v[q];
+        for (int q = 0; q < DEM_MAX_PLATES; q++) pc[q] = (unsigned int)v[3 * DEM_MAX_PLATES + q];
+        CK(cudaMemcpyAsync(ctx->pacc, acc, sizeof(acc), cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(ctx->pcount, pc, sizeof(pc), cudaMemcpyHostToDevice, s));
+    }
+    launch_boundary(ctx->db, ctx->pacc, ctx->pcount, sp.h, ctx->dsc, s);
     ctx->launches += (N ? 2 : 0) + (nc ? 2 : 1);
     CK(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(StepScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&ctx->hb, ctx->db, sizeof(DevBoundary), cudaMemcpyDeviceToHost, s));
     tstart(ctx, 5);
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
-    const StepScalars sc = *ctx->hsc;
+    StepScalars sc = *ctx->hsc;
+    if (ctx->G > 1) {
+        // global report and decisions: every rank takes the same rollback / rebuild branch
+        double mx[3], sm[5];
+        std::memcpy(&mx[0], &sc.max_disp_bits, 8);
+        std::memcpy(&mx[1], &sc.max_v_bits, 8);
+        mx[2] = sc.nan_flag ? 1.0 : 0.0;
+        sm[0] = sc.ke; sm[1] = sc.n_pp; sm[2] = sc.n_wall; sm[3] = sc.n_plate; sm[4] = sc.n_degenerate;
+        if (!ctx->tp->allreduce_f64(mx, 3, 1, s, ctx->err) || !ctx->tp->allreduce_f64(sm, 5, 0, s, ctx->err))
+            return DEM_ERR_NCCL;
+        std::memcpy(&sc.max_disp_bits, &mx[0], 8);
+        std::memcpy(&sc.max_v_bits, &mx[1], 8);
+        sc.nan_flag = mx[2] > 0.0 ? 1u : 0u;
+        sc.ke = sm[0];
+        sc.n_pp = (unsigned)sm[1]; sc.n_wall = (unsigned)sm[2]; sc.n_plate = (unsigned)sm[3]; sc.n_degenerate = (unsigned)sm[4];
+    }
     if (sc.nan_flag) {
         // atomic step: restore the state of the step start
         if (N) {
@@ -605,7 +847,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     ctx->step++;
     rep->step = ctx->step;
     rep->time = ctx->hb.time;
-    rep->n_contacts = nc;
+    rep->n_contacts = ctx->G > 1 ? (int64_t)sc.n_pp + sc.n_wall + sc.n_plate : (int64_t)nc;
     rep->n_pp = sc.n_pp;
     rep->n_wall = sc.n_wall;
     rep->n_plate = sc.n_plate;
@@ -642,18 +884,23 @@ static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, con
         if (!(r[i] > 0) || !std::isfinite(r[i])) { ctx->err = "radius must be positive and finite"; return DEM_ERR_INVALID; }
         for (int k = 0; k < 3; k++) if (!std::isfinite(x[3 * i + k])) { ctx->err = "non-finite position"; return DEM_ERR_INVALID; }
         if (g[i] >= PLATE_KEY_BASE) { ctx->err = "gid must be < 2^32-4096"; return DEM_ERR_INVALID; }
+        if (ctx->G > 1 && !((ctx->rank == 0 || x[3 * i] >= ctx->slab_lo) && (ctx->rank == ctx->G - 1 || x[3 * i] < ctx->slab_hi))) {
+            ctx->err = "particle outside this rank's slab [slab_lo, slab_hi)";
+            return DEM_ERR_INVALID;
+        }
     }
     std::vector<uint32_t> gs(g);
     std::sort(gs.begin(), gs.end());
     for (int64_t i = 1; i < n; i++) if (gs[i] == gs[i - 1]) { ctx->err = "duplicate gid"; return DEM_ERR_INVALID; }
     if (first) {
         ctx->N = n;
-        TRY(alloc_particles(ctx));
+        ctx->N_own = n;
+        TRY(alloc_particles(ctx, n));
     } else if (n != ctx->N) {
         ctx->err = "set_state: particle count differs from create";
         return DEM_ERR_INVALID;
     }
-    setup_levels(ctx, r);
+    TRY(setup_levels(ctx, r));
     // stage host copies into device buffers, then convert to the internal layout
     double *dx = nullptr, *dr = nullptr, *dv = nullptr, *dw = nullptr;
     uint32_t *dg = nullptr;
@@ -702,8 +949,11 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
     }
     if (desc->parts.n >= (int64_t)0x7FFFFFFF) { g_create_err = "too many particles for one context"; return DEM_ERR_INVALID; }
     if (dist && dist->world_size > 1) {
-        g_create_err = "world_size > 1: x-slab decomposition is not available in this release";
-        return DEM_ERR_INVALID;
+        if (dist->rank < 0 || dist->rank >= dist->world_size || !(dist->slab_lo < dist->slab_hi) ||
+            (dist->transport != 0 && dist->transport != 1) || (dist->transport == 1 && !dist->loopback)) {
+            g_create_err = "invalid decomposition (rank, slab_lo < slab_hi, transport 0 NCCL | 1 loopback)";
+            return DEM_ERR_INVALID;
+        }
     }
     dem_ctx *ctx = new dem_ctx();
     ctx->mat = desc->mat;
@@ -719,6 +969,20 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
         ctx->own_stream = true;
     }
     if (dist && dist->alloc && dist->free) { ctx->ualloc = dist->alloc; ctx->ufree = dist->free; ctx->actx = dist->alloc_ctx; }
+    if (dist && dist->world_size > 1) {
+        ctx->G = dist->world_size;
+        ctx->rank = dist->rank;
+        ctx->slab_lo = dist->slab_lo;
+        ctx->slab_hi = dist->slab_hi;
+        std::string err;
+        ctx->tp = dist->transport == 1 ? make_loop_transport(ctx->rank, (LoopGroup *)dist->loopback, err)
+                                       : make_nccl_transport(ctx->rank, ctx->G, dist->nccl_unique_id, err);
+        if (!ctx->tp) {
+            g_create_err = err;
+            dem_destroy(ctx);
+            return DEM_ERR_NCCL;
+        }
+    }
     setup_solve_params(ctx);
     setup_walls(ctx);
     for (int e = 0; e < 8; e++) cudaEventCreate(&ctx->ev[e]);
@@ -771,13 +1035,13 @@ dem_status dem_set_solver(dem_ctx *ctx, const dem_solver *so)
 dem_status dem_get_state(dem_ctx *ctx, dem_state_view *v)
 {
     if (!ctx || !v) return DEM_ERR_INVALID;
-    if (v->n < ctx->N) { ctx->err = "state view too small"; v->n = ctx->N; return DEM_ERR_INVALID; }
-    const int64_t N = ctx->N;
+    if (v->n < ctx->N_own) { ctx->err = "state view too small"; v->n = ctx->N_own; return DEM_ERR_INVALID; }
+    const int64_t N = ctx->N_own;        // owned particles (all of them with world_size 1)
     v->n = N;
     if (!N) return DEM_OK;
     cudaStream_t s = ctx->s;
     if (v->on_device) {
-        launch_to_gid_order(N, ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], v->pos,
+        launch_to_gid_order(ctx->N, N, OWN(ctx), ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], v->pos,
                             v->vel, v->angvel, v->radius, v->gid, s);
         ctx->launches++;
         CK(cudaStreamSynchronize(s));
@@ -787,7 +1051,7 @@ dem_status dem_get_state(dem_ctx *ctx, dem_state_view *v)
     uint32_t *dg = nullptr;
     TRY(A(ctx, &d, 10 * N));
     TRY(A(ctx, &dg, N));
-    launch_to_gid_order(N, ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], d, d + 3 * N,
+    launch_to_gid_order(ctx->N, N, OWN(ctx), ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], d, d + 3 * N,
                         d + 6 * N, d + 9 * N, dg, s);
     ctx->launches++;
     if (v->pos) CK(cudaMemcpyAsync(v->pos, d, 3 * N * 8, cudaMemcpyDeviceToHost, s));
@@ -804,6 +1068,7 @@ dem_status dem_get_state(dem_ctx *ctx, dem_state_view *v)
 dem_status dem_set_state(dem_ctx *ctx, const dem_state_view *st, const dem_contact_view *hist)
 {
     if (!ctx || !st) return DEM_ERR_INVALID;
+    if (ctx->G > 1) { ctx->err = "dem_set_state needs world_size 1"; return DEM_ERR_INVALID; }
     if (st->n != ctx->N || (st->n && (!st->pos || !st->radius))) { ctx->err = "set_state: bad view"; return DEM_ERR_INVALID; }
     // history: sorted by key on the host, uploaded for the next rebuild's sorted-key lookup
     std::vector<uint64_t> hk;
@@ -848,13 +1113,21 @@ dem_status dem_get_contacts(dem_ctx *ctx, dem_contact_view *v)
 {
     if (!ctx || !v) return DEM_ERR_INVALID;
     if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
-    const int64_t nc = ctx->nc;
+    const int64_t ncl = ctx->nc;
+    cudaStream_t s = ctx->s;
+    // contacts this rank reports (all with world_size 1): owner of the smaller gid / the particle
+    unsigned int *dcnt = nullptr, hcnt = 0;
+    TRY(A(ctx, &dcnt, 1));
+    CK(cudaMemsetAsync(dcnt, 0, 4, s));
+    launch_contact_keys(ncl, OWN(ctx), ctx->cij, ctx->gid, ctx->keys[0], ctx->vals[0], dcnt, s);
+    CK(cudaMemcpyAsync(&hcnt, dcnt, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, dcnt);
+    const int64_t nc = hcnt;
     if (v->n < nc) { v->n = nc; ctx->err = "contact view too small"; return DEM_ERR_INVALID; }
     v->n = nc;
     if (!nc) return DEM_OK;
-    cudaStream_t s = ctx->s;
-    launch_contact_keys(nc, ctx->cij, ctx->gid, ctx->keys[0], ctx->vals[0], s);
-    radix_sort_u64(ctx->keys, ctx->vals, nc, 64, ctx->sort_tmp, s, &ctx->launches);
+    radix_sort_u64(ctx->keys, ctx->vals, ncl, 64, ctx->sort_tmp, s, &ctx->launches);
     double *d = nullptr;
     TRY(A(ctx, &d, 11 * nc));
     launch_contact_out(nc, ctx->vals[0], ctx->cij, ctx->gid, ctx->geo, ctx->cdel, ctx->Pfa, ctx->Pfb, d, d + 3 * nc, d + 4 * nc, s);
@@ -873,19 +1146,19 @@ dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device)
 {
     if (!ctx) return DEM_ERR_INVALID;
     if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
-    const int64_t N = ctx->N;
+    const int64_t N = ctx->N, Nown = ctx->N_own;
     if (!N) return DEM_OK;
     cudaStream_t s = ctx->s;
     launch_sweep(SWEEP_MODE_FORCES, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
                  ctx->inc, ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, nullptr, nullptr, ctx->db, ctx->sp, s);
     double *d = nullptr;
     TRY(A(ctx, &d, 6 * N));
-    launch_to_gid_order(N, ctx->gid, ctx->gid_sorted, ctx->vel2, ctx->ang2, nullptr, d, d + 3 * N, nullptr, nullptr,
+    launch_to_gid_order(N, Nown, OWN(ctx), ctx->gid, ctx->gid_sorted, ctx->vel2, ctx->ang2, nullptr, d, d + 3 * Nown, nullptr, nullptr,
                         nullptr, s);
     ctx->launches += 2;
     cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-    if (F) CK(cudaMemcpyAsync(F, d, 3 * N * 8, k, s));
-    if (T) CK(cudaMemcpyAsync(T, d + 3 * N, 3 * N * 8, k, s));
+    if (F) CK(cudaMemcpyAsync(F, d, 3 * Nown * 8, k, s));
+    if (T) CK(cudaMemcpyAsync(T, d + 3 * Nown, 3 * Nown * 8, k, s));
     CK(cudaStreamSynchronize(s));
     dfree(ctx, d);
     return DEM_OK;
@@ -985,7 +1258,120 @@ dem_status dem_reset_timing(dem_ctx *ctx)
     return DEM_OK;
 }
 
+// Diagnostic: time n Jacobi sweeps of one sweep-kernel variant on the last step's contact set
+// (inputs: the current velocities, the last step's final impulses, main-stage rows) and report
+// the max velocity difference after n sweeps against the shipped kernel (variant 0).
+// Leaves the particle state and the last step's contact getters untouched.
+dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms_per_sweep, double *max_dv_rel)
+{
+    if (!ctx || n < 1) return DEM_ERR_INVALID;
+    if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
+    if (ctx->G > 1) { ctx->err = "dem_bench_sweeps needs world_size 1"; return DEM_ERR_INVALID; }
+    const int64_t N = ctx->N, nc = ctx->nc;
+    cudaStream_t s = ctx->s;
+    double *cb = nullptr;
+    double4 *ref = nullptr;
+    unsigned long long *md = nullptr;
+    TRY(A(ctx, &cb, nc + 1));
+    TRY(A(ctx, &ref, N + 1));
+    TRY(A(ctx, &md, 2));
+    launch_row_bias(nc, ctx->row, cb, s);
+    launch_tile_order(N, ctx->inc_start, ctx->order, s);
+    // tile-paired incidence (variants 20/21: tiles of 128/256 particles)
+    uint32_t *ca6 = nullptr, *bs6 = nullptr, *xc6 = nullptr, *xs6 = nullptr, *bsl6 = nullptr;
+    uint2 *xl6 = nullptr;
+    unsigned int *mb6 = nullptr, maxb = 0;
+    const int tile6 = variant == 21 ? 256 : 128;
+    if (variant >= 20) {
+        TRY(A(ctx, &ca6, N + 2)); TRY(A(ctx, &bs6, N + 2)); TRY(A(ctx, &xc6, N + 2)); TRY(A(ctx, &xs6, N + 2));
+        TRY(A(ctx, &bsl6, nc + 1)); TRY(A(ctx, &xl6, nc + 1)); TRY(A(ctx, &mb6, 1));
+        launch_inc6(N, tile6, ctx->co_start, ctx->cscan, ctx->inc_start, ctx->inc, ca6, bs6, xc6, xs6, bsl6, xl6, mb6,
+                    ctx->scan_tmp, s, &ctx->launches);
+        CK(cudaMemcpyAsync(&maxb, mb6, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    uint4 *xl8 = nullptr;
+    if (variant == 30) {
+        TRY(A(ctx, &xl8, nc + 1));
+        launch_inc8(N, ctx->co_start, ctx->cscan, ctx->inc_start, ctx->inc, ca6, bs6, xc6, xs6, bsl6, xl8, mb6,
+                    ctx->scan_tmp, s, &ctx->launches);
+        CK(cudaMemcpyAsync(&maxb, mb6, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    P4 *spa = ctx->Pfa == ctx->Pa[0] ? ctx->Pa[1] : ctx->Pa[0];
+    P4 *spb = ctx->Pfb == ctx->Pb[0] ? ctx->Pb[1] : ctx->Pb[0];
+    double4 *vbuf[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel2}, *wbuf[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang2};
+    float ms = 0.f;
+    double4 *vres = nullptr;
+    for (int pass = 0; pass < 2; pass++) {
+        const int var = pass == 0 ? 0 : variant;
+        CK(cudaMemcpyAsync(ctx->Pwa, ctx->Pfa, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->Pwb, ctx->Pfb, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
+        const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
+        P4 *pai = ctx->Pwa, *pbi = ctx->Pwb, *pao = spa, *pbo = spb;
+        cudaEventRecord(ctx->ev[6], s);
+        for (int it = 0; it < n; it++) {
+            double4 *vo = vbuf[it & 1], *wo = wbuf[it & 1];
+            if (var < 10 || var >= 40) {
+                set_sweep_variant(var);
+                launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, vi, wi, vo, wo, ctx->inc_start, ctx->inc, ctx->geo, ctx->row,
+                             pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
+            } else if (var == 30) {
+                launch_sweep8(N, maxb, vi, wi, vo, wo, ca6, bs6, xs6, xl8, ctx->cij, bsl6, ctx->geo, ctx->row, pai, pbi, pao,
+                              pbo, ctx->db, ctx->sp, s);
+            } else if (var >= 20) {
+                launch_sweep6(tile6, false, N, maxb, ctx->pos_prev, vi, wi, vo, wo, ca6, bs6, xs6, xl6, ctx->cij, bsl6, cb,
+                              pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
+            } else {
+                // geometry from the positions the step's sweeps saw (before integration)
+                launch_sweep5(var - 10, false, N, ctx->order, ctx->pos_prev, vi, wi, vo, wo, ctx->inc_start, ctx->inc, cb,
+                              pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
+            }
+            vi = vo; wi = wo;
+            std::swap(pai, pao);
+            std::swap(pbi, pbo);
+            vres = vo;
+        }
+        cudaEventRecord(ctx->ev[7], s);
+        set_sweep_variant(0);
+        CK(cudaGetLastError());
+        if (pass == 0) CK(cudaMemcpyAsync(ref, vres, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+        cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
+    }
+    launch_maxdiff(N, vres, ref, md, s);
+    unsigned long long h[2] = {0, 0};
+    CK(cudaMemcpyAsync(h, md, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double d, m;
+    std::memcpy(&d, &h[0], 8);
+    std::memcpy(&m, &h[1], 8);
+    if (ms_per_sweep) *ms_per_sweep = ms / n;
+    if (max_dv_rel) *max_dv_rel = m > 0 ? d / m : d;
+    dfree(ctx, cb);
+    dfree(ctx, ref);
+    dfree(ctx, md);
+    for (void *q : {(void *)ca6, (void *)bs6, (void *)xc6, (void *)xs6, (void *)bsl6, (void *)xl6, (void *)mb6, (void *)xl8}) dfree(ctx, q);
+    return DEM_OK;
+}
+
 void *dem_stream(dem_ctx *ctx) { return ctx ? (void *)ctx->s : nullptr; }
+
+int64_t dem_num_particles(const dem_ctx *ctx) { return ctx ? ctx->N_own : -1; }
+
+int64_t dem_num_local(const dem_ctx *ctx) { return ctx ? ctx->N : -1; }
+
+void *dem_loopback_create(int32_t world_size) { return world_size >= 1 ? (void *)new LoopGroup(world_size) : nullptr; }
+
+void dem_loopback_destroy(void *group) { delete (LoopGroup *)group; }
+
+dem_status dem_nccl_unique_id(void *out128)
+{
+    if (!out128) return DEM_ERR_INVALID;
+    std::string err;
+    if (!nccl_unique_id(out128, err)) { g_create_err = err; return DEM_ERR_NCCL; }
+    return DEM_OK;
+}
 
 dem_status dem_destroy(dem_ctx *ctx)
 {
@@ -997,6 +1383,7 @@ dem_status dem_destroy(dem_ctx *ctx)
     if (ctx->hsc) cudaFreeHost(ctx->hsc);
     if (ctx->hnc) cudaFreeHost(ctx->hnc);
     if (ctx->own_stream && ctx->s) cudaStreamDestroy(ctx->s);
+    delete ctx->tp;
     delete ctx;
     return DEM_OK;
 }

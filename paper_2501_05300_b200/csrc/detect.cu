@@ -20,6 +20,8 @@
 
 // ------------------------------------------------------------------ exact contact geometry
 // Returns 1 contact, 0 none, -1 degenerate (coincident centres, flagged and skipped).
+// The predicate is exact fp64 with a fixed operation order (reading R14); n and delta of an
+// active pair come from pair_geom, the sequence the sweeps re-evaluate (common.cuh).
 __device__ __forceinline__ int contact_geom(uint2 ij, const double4 *__restrict__ pos, const DevBoundary *bnd,
                                             d3 &n, double &delta)
 {
@@ -31,51 +33,10 @@ __device__ __forceinline__ int contact_geom(uint2 ij, const double4 *__restrict_
         const double R = __dadd_rn(A.w, B.w);
         if (!(d2 < __dmul_rn(R, R))) return 0;
         if (d2 == 0.0) return -1;
-        const double d = __dsqrt_rn(d2);
-        n = mk(__ddiv_rn(dx, d), __ddiv_rn(dy, d), __ddiv_rn(dz, d));
-        delta = __dsub_rn(R, d);
+        pair_geom(A, B, n, delta);
         return 1;
     }
-    const uint32_t code = ij.y & ~PARTNER_EXT;
-    const double X[3] = {A.x, A.y, A.z};
-    const double r = A.w;
-    if (!(code & PARTNER_PLATE)) {
-        const int w = (int)code;
-        const double s = __dadd_rn(__dadd_rn(__dmul_rn(__dsub_rn(X[0], bnd->wp[w][0]), bnd->wn[w][0]),
-                                             __dmul_rn(__dsub_rn(X[1], bnd->wp[w][1]), bnd->wn[w][1])),
-                                   __dmul_rn(__dsub_rn(X[2], bnd->wp[w][2]), bnd->wn[w][2]));
-        if (!(s < r)) return 0;
-        n = mk(-bnd->wn[w][0], -bnd->wn[w][1], -bnd->wn[w][2]);
-        delta = __dsub_rn(r, s);
-        return 1;
-    }
-    const int p = (code >> 4) & 0xF, b = code & 0xF;
-    double lo[3], hi[3], dq[3];
-    for (int k = 0; k < 3; k++) {
-        lo[k] = __dadd_rn(bnd->ppos[p][k], bnd->lo[p][b][k]);
-        hi[k] = __dadd_rn(bnd->ppos[p][k], bnd->hi[p][b][k]);
-        const double q = X[k] < lo[k] ? lo[k] : (X[k] > hi[k] ? hi[k] : X[k]);
-        dq[k] = __dsub_rn(q, X[k]);
-    }
-    const double d2 = dist2_rn(dq[0], dq[1], dq[2]);
-    if (d2 > 0.0) {
-        if (!(d2 < __dmul_rn(r, r))) return 0;
-        const double d = __dsqrt_rn(d2);
-        n = mk(__ddiv_rn(dq[0], d), __ddiv_rn(dq[1], d), __ddiv_rn(dq[2], d));
-        delta = __dsub_rn(r, d);
-        return 1;
-    }
-    // centre inside the box (reading R19): exit through the nearest face
-    double best = INFINITY, sg = 1.0;
-    int bk = 0;
-    for (int k = 0; k < 3; k++) {
-        const double dl = __dsub_rn(X[k], lo[k]), dh = __dsub_rn(hi[k], X[k]);
-        if (dl < best) { best = dl; bk = k; sg = 1.0; }
-        if (dh < best) { best = dh; bk = k; sg = -1.0; }
-    }
-    n = mk(bk == 0 ? sg : 0.0, bk == 1 ? sg : 0.0, bk == 2 ? sg : 0.0);
-    delta = __dadd_rn(r, best);
-    return 1;
+    return ext_geom(A, ij.y & ~PARTNER_EXT, bnd, n, delta);
 }
 
 // ------------------------------------------------------------------ rebuild kernels
@@ -357,7 +318,7 @@ __global__ void k_compact(int64_t nc, const uint2 *__restrict__ cand, const uint
     const double ra = pos[ij.x].w;
     const bool ext = (ij.y & PARTNER_EXT) != 0;
     const double rb = ext ? 0.0 : pos[ij.y].w;
-    const double Rs = ext ? ra : ra * rb / (ra + rb);
+    const double Rs = ext ? ra : rstar(ra, rb);
     cij[c] = ij;
     double mt, mr;
     partner_mu(ij.y, sp, bnd, mt, mr);
@@ -383,11 +344,19 @@ __global__ void k_compact(int64_t nc, const uint2 *__restrict__ cand, const uint
 }
 
 // per-kind contact counts: warp ballots, one atomic per warp and kind
-__global__ void k_count_kinds(int64_t nc, const uint2 *__restrict__ cij, StepScalars *sc)
+// A contact is counted by the rank that owns its particle with the smaller gid (boundary
+// contacts: the rank owning the particle), so sums over ranks count each contact once.
+__global__ void k_count_kinds(int64_t nc, const uint8_t *__restrict__ own, const uint2 *__restrict__ cij,
+                              const uint32_t *__restrict__ gid, StepScalars *sc)
 {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t j = c < nc ? cij[c].y : 0u;
-    const bool ok = c < nc;
+    const uint2 ij = c < nc ? cij[c] : make_uint2(0, 0);
+    const uint32_t j = ij.y;
+    bool ok = c < nc;
+    if (ok) {
+        const uint32_t o = (j & PARTNER_EXT) ? ij.x : (gid[ij.x] < gid[j] ? ij.x : j);
+        ok = !own || own[o];
+    }
     const unsigned pp = __ballot_sync(0xffffffffu, ok && !(j & PARTNER_EXT));
     const unsigned pl = __ballot_sync(0xffffffffu, ok && (j & PARTNER_EXT) && (j & PARTNER_PLATE));
     const unsigned wl = __ballot_sync(0xffffffffu, ok && (j & PARTNER_EXT) && !(j & PARTNER_PLATE));
@@ -427,14 +396,21 @@ __global__ void k_inc_fill(int64_t N, const uint32_t *__restrict__ co_start, con
 
 // ------------------------------------------------------------------ output helpers
 // contacts -> public keys (canonical orientation), values = contact index
-__global__ void k_contact_keys(int64_t nc, const uint2 *__restrict__ cij, const uint32_t *__restrict__ gid,
-                               uint64_t *__restrict__ keys, uint32_t *__restrict__ vals)
+// contacts reported by this rank (owner of the smaller gid; boundary contacts: the particle's
+// owner) get their public key, the others sort last (key ~0); cnt counts the reported ones
+__global__ void k_contact_keys(int64_t nc, const uint8_t *__restrict__ own, const uint2 *__restrict__ cij,
+                               const uint32_t *__restrict__ gid, uint64_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                               unsigned int *cnt)
 {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nc) return;
     bool flip;
-    keys[c] = cand_key(cij[c], gid, flip);
+    const uint2 ij = cij[c];
+    const uint32_t o = (ij.y & PARTNER_EXT) ? ij.x : (gid[ij.x] < gid[ij.y] ? ij.x : ij.y);
+    const bool mine = !own || own[o];
+    keys[c] = mine ? cand_key(ij, gid, flip) : ~0ull;
     vals[c] = (uint32_t)c;
+    if (mine) atomicAdd(cnt, 1u);
 }
 
 __global__ void k_contact_out(int64_t nc, const uint32_t *__restrict__ vals, const uint2 *__restrict__ cij,
@@ -504,8 +480,8 @@ void launch_compact(int64_t nc, const uint2 *cand, const uint32_t *flag, const u
                     const DevBoundary *bnd, const SolveParams &sp, const P4 *Pca, const P4 *Pcb, uint2 *cij,
                     G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, StepScalars *sc, cudaStream_t s)
 { if (nc) k_compact<<<GRID(nc)>>>(nc, cand, flag, scan, pos, bnd, sp, Pca, Pcb, cij, geo, row, cdel, Pa, Pb, ccand, sc); }
-void launch_count_kinds(int64_t nc, const uint2 *cij, StepScalars *sc, cudaStream_t s)
-{ if (nc) k_count_kinds<<<GRID(nc)>>>(nc, cij, sc); }
+void launch_count_kinds(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, StepScalars *sc, cudaStream_t s)
+{ if (nc) k_count_kinds<<<GRID(nc)>>>(nc, own, cij, gid, sc); }
 void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const uint32_t *scan, const uint32_t *ct_start,
                 const uint32_t *ct_list, const uint32_t *flag, uint32_t *cnt, uint32_t *inc_start, uint2 *inc,
                 void *scan_tmp, cudaStream_t s, long long *launches)
@@ -515,8 +491,9 @@ void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const ui
     if (N) k_inc_fill<<<GRID(N)>>>(N, co_start, cand, scan, ct_start, ct_list, flag, inc_start, inc);
     *launches += 2;
 }
-void launch_contact_keys(int64_t nc, const uint2 *cij, const uint32_t *gid, uint64_t *keys, uint32_t *vals, cudaStream_t s)
-{ if (nc) k_contact_keys<<<GRID(nc)>>>(nc, cij, gid, keys, vals); }
+void launch_contact_keys(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, uint64_t *keys, uint32_t *vals,
+                         unsigned int *cnt, cudaStream_t s)
+{ if (nc) k_contact_keys<<<GRID(nc)>>>(nc, own, cij, gid, keys, vals, cnt); }
 void launch_contact_out(int64_t nc, const uint32_t *vals, const uint2 *cij, const uint32_t *gid, const G4 *geo,
                         const double *cdel, const P4 *Pa, const P4 *Pb, double *nrm, double *delta, double *P, cudaStream_t s)
 { if (nc) k_contact_out<<<GRID(nc)>>>(nc, vals, cij, gid, geo, cdel, Pa, Pb, nrm, delta, P); }

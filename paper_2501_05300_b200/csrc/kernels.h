@@ -23,11 +23,12 @@ void launch_narrow(int64_t nc, const uint2 *cand, const double4 *pos, const DevB
 void launch_compact(int64_t nc, const uint2 *cand, const uint32_t *flag, const uint32_t *scan, const double4 *pos,
                     const DevBoundary *bnd, const SolveParams &sp, const P4 *Pca, const P4 *Pcb, uint2 *cij,
                     G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, StepScalars *sc, cudaStream_t s);
-void launch_count_kinds(int64_t nc, const uint2 *cij, StepScalars *sc, cudaStream_t s);
+void launch_count_kinds(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, StepScalars *sc, cudaStream_t s);
 void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const uint32_t *scan, const uint32_t *ct_start,
                 const uint32_t *ct_list, const uint32_t *flag, uint32_t *cnt, uint32_t *inc_start, uint2 *inc,
                 void *scan_tmp, cudaStream_t s, long long *launches);
-void launch_contact_keys(int64_t nc, const uint2 *cij, const uint32_t *gid, uint64_t *keys, uint32_t *vals, cudaStream_t s);
+void launch_contact_keys(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, uint64_t *keys, uint32_t *vals,
+                         unsigned int *cnt, cudaStream_t s);
 void launch_contact_out(int64_t nc, const uint32_t *vals, const uint2 *cij, const uint32_t *gid, const G4 *geo,
                         const double *cdel, const P4 *Pa, const P4 *Pb, double *nrm, double *delta, double *P, cudaStream_t s);
 
@@ -44,14 +45,51 @@ void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin
                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
 bool sweep_uses_order();
 void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s);
-void launch_integrate(int64_t N, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
+void launch_integrate(int64_t N, const uint8_t *own, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
                       double rho, double *ke_part, StepScalars *sc, cudaStream_t s);
-void launch_plates(int64_t nc, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
-                   unsigned int *pcount, DevBoundary *bnd, double h, StepScalars *sc, cudaStream_t s);
+void launch_plate_sum(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
+                      unsigned int *pcount, cudaStream_t s);
+void launch_boundary(DevBoundary *bnd, const unsigned long long *acc, const unsigned int *pcount, double h, StepScalars *sc,
+                     cudaStream_t s);
 void launch_scatter_P(int64_t nc, const uint32_t *ccand, const P4 *Pa, const P4 *Pb, P4 *Pca, P4 *Pcb,
                       cudaStream_t s);
-void launch_to_gid_order(int64_t N, const uint32_t *gid, const uint32_t *gid_sorted, const double4 *a,
+void launch_to_gid_order(int64_t N, int64_t n_sorted, const uint8_t *own, const uint32_t *gid, const uint32_t *gid_sorted, const double4 *a,
                          const double4 *b, const double4 *c, double *oa, double *ob, double *oc, double *orad,
                          uint32_t *ogid, cudaStream_t s);
 void launch_load_state(int64_t N, const double *x, const double *r, const double *v, const double *w,
                        const uint32_t *gid_in, double4 *pos, double4 *vel, double4 *ang, uint32_t *gid, cudaStream_t s);
+void set_sweep_variant(int v);      // 0 k_sweep_tile, 1 k_sweep_pipe, 2 k_sweep_ppt (bench/diagnostics)
+
+// sweep5.cu: sweeps re-evaluating the contact geometry from positions (cb = SPOOK bias per contact)
+enum { SWEEP5_PPT = 0, SWEEP5_PPT_PF = 1, SWEEP5_TILE = 2 };
+void launch_sweep5(int kind, bool impact, int64_t N, const uint32_t *order, const double4 *pos, const double4 *vin,
+                   const double4 *win, double4 *vout, double4 *wout, const uint32_t *inc_start, const uint2 *inc,
+                   const double *cb, const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
+                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+void launch_row_bias(int64_t nc, const R4 *row, double *cb, cudaStream_t s);
+void launch_maxdiff(int64_t N, const double4 *a, const double4 *b, unsigned long long *out, cudaStream_t s);
+
+// sweep6.cu: tile-paired sweep (intra-tile contacts evaluated once) and its per-step incidence
+void launch_inc6(int64_t N, int tile, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start,
+                 const uint2 *inc, uint32_t *ca, uint32_t *bstart, uint32_t *xcnt, uint32_t *xstart, uint32_t *bslot,
+                 uint2 *xlist, unsigned int *max_b, void *scan_tmp, cudaStream_t s, long long *launches);
+size_t sweep6_smem_bytes(int tile, unsigned max_b);
+void launch_sweep6(int tile, bool impact, int64_t N, unsigned max_b, const double4 *pos, const double4 *vin,
+                   const double4 *win, double4 *vout, double4 *wout, const uint32_t *ca, const uint32_t *bstart,
+                   const uint32_t *xstart, const uint2 *xlist, const uint2 *cij, const uint32_t *bslot,
+                   const double *cb, const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
+                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+// sweep6.cu (v8): slot sweep, block-strided items, no segmented scan
+void launch_inc8(int64_t N, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start, const uint2 *inc,
+                 uint32_t *ca, uint32_t *bstart, uint32_t *xcnt, uint32_t *xstart, uint32_t *bslot, uint4 *xlist,
+                 unsigned int *max_slots, void *scan_tmp, cudaStream_t s, long long *launches);
+size_t sweep8_smem_bytes(unsigned max_slots);
+void launch_sweep8(int64_t N, unsigned max_slots, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
+                   const uint32_t *ca, const uint32_t *bstart, const uint32_t *xstart, const uint4 *xlist,
+                   const uint2 *cij, const uint32_t *bslot, const G4 *geo, const R4 *row, const P4 *Pa_in,
+                   const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+// sweep_t2.cu: tile sweep with 256-bit records and conflict-free shared staging
+void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
+                     const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row, const P4 *Pa_in,
+                     const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp,
+                     cudaStream_t s);

@@ -17,47 +17,13 @@
 //  k_plate_sum + k_boundary   int64 fixed-point plate reactions, plate drives, moving walls
 #include "common.cuh"
 #include "kernels.h"
+#include "sweep_core.cuh"
 
-__device__ __forceinline__ d3 xyz(double4 a) { return mk(a.x, a.y, a.z); }
-
-// fp64 reciprocal: MUFU.RCP64H estimate + two Newton steps (relative error ~1e-16; operands
-// are positive and finite: split weights, regularised diagonals)
-__device__ __forceinline__ double rcp64(double x)
-{
-    double r;
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-    double e = fma(-x, r, 1.0);
-    r = fma(r, e, r);
-    e = fma(-x, r, 1.0);
-    return fma(r, e, r);
-}
-
-// factor that scales a vector of squared length m2 onto the ball of radius lim (1 inside):
-// MUFU.RSQ64H estimate + two fp64 Newton steps, branch-free, full fp64 exponent range
-__device__ __forceinline__ double clamp_scale(double m2, double lim)
-{
-    const bool out = m2 > lim * lim;
-    const double q = out ? m2 : 1.0;
-    double r;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
-    r = r * (1.5 - 0.5 * q * r * r);
-    r = r * (1.5 - 0.5 * q * r * r);
-    return out ? lim * r : 1.0;
-}
 
 __device__ __forceinline__ void boundary_vel(uint32_t p, const DevBoundary *__restrict__ bnd, d3 &v, double &mt)
 {
-    const uint32_t code = p & ~PARTNER_EXT;
-    if (code & PARTNER_PLATE) {
-        const int q = (code >> 4) & 0xF;
-        v = mk(bnd->pvel[q][0], bnd->pvel[q][1], bnd->pvel[q][2]);
-        mt = bnd->pmu_t[q];
-    } else {
-        const int w = (int)code;
-        const double s = bnd->wvel[w];
-        v = mk(s * bnd->wn[w][0], s * bnd->wn[w][1], s * bnd->wn[w][2]);
-        mt = bnd->wall_mu_t;
-    }
+    double mr;
+    boundary_body(p, bnd, v, mt, mr);
 }
 
 __global__ void k_prepare(int64_t N, const uint32_t *__restrict__ inc_start, const double4 *__restrict__ pos,
@@ -99,76 +65,12 @@ __global__ void k_rows(int64_t nc, int mode, const uint2 *__restrict__ cij, cons
     }
     // SPOOK: Sigma-hat = 4 Ups / (h^2 e_H k_n delta^(2 e_H - 2)), b = (4 Ups/h)(delta/e_H) + Ups u_n
     const double delta = cdel[c];
-    double S;
-    if (sp.hertz) {
-        const double ra = pos[ij.x].w;
-        const double Rs = ext ? ra : ra * pos[ij.y].w / (ra + pos[ij.y].w);
-        const double kn = sp.Es * sqrt(2.0 * Rs) / 3.0;        // k_n = E* sqrt(d*)/3, d* = 2 R*
-        S = 4.0 * sp.Ups / (sp.h * sp.h * sp.e_H * kn * sqrt(delta));
-    } else {
-        S = 4.0 * sp.Ups / (sp.h * sp.h * sp.e_H * sp.k_lin);
-    }
+    const double ra = pos[ij.x].w;
+    const double S = spook_sigma(sp, ext ? ra : rstar(ra, pos[ij.y].w), delta);
     row[c] = mkR4(S, 4.0 * sp.Ups / sp.h * (delta / sp.e_H) + sp.Ups * un, rw.z, rw.w);
 }
 
 // ------------------------------------------------------------------ the Jacobi sweep
-// One half-contact: contact c seen from `self`.  Canonical orientation: a = cij.x, b = cij.y.
-// Returns the contribution to self (dL linear, dA angular impulse) and the new impulse.
-struct HalfOut {
-    d3 dL, dA;
-    P4 Pa, Pb;
-};
-
-__device__ __forceinline__ HalfOut half_contact(const double4 VA, const double4 WA, const double4 VB, const double4 WB,
-                                                bool isB, double mt, const G4 g, const R4 rw, const P4 pa,
-                                                const P4 pb, int rolling_dims)
-{
-    // VA..WB are body a's and body b's states in the canonical orientation, selected by
-    // address by the caller: one instruction stream for both ends -> bit-identical result
-    const d3 n = mk(g.x, g.y, g.z);
-    const double mrRs = g.w;                     // mu_r R*
-    const double la = rw.z, lb = rw.w;           // lever arms l_a = la n, l_b = -lb n
-    const double wA = VA.w, wtA = WA.w, wB = VB.w, wtB = WB.w;
-    const double Dn = wA + wB;
-    const double Dt = Dn + la * la * wtA + lb * lb * wtB;
-    const double Dr = wtA + wtB;
-    const d3 dv = xyz(VB) - xyz(VA);
-    // 1. normal row (P:117 under SPOOK): P_n' = max(0, P_n - (u_n + S P_n - b)/(D_n + S)).
-    //    Its velocity update is along n and drops out of the tangential projection below.
-    const double S = rw.x, b = rw.y, Pn0 = pa.x;
-    double Pn = Pn0 - (dot(n, dv) + S * Pn0 - b) * rcp64(Dn + S);
-    Pn = rndP(Pn > 0.0 ? Pn : 0.0);
-    const double dPn = Pn - Pn0;
-    // 2. friction (disc of radius mu_t P_n', maximum dissipation P:123-125):
-    //    u = (v_b + w_b x l_b) - (v_a + w_a x l_a) = dv - (lb w_b + la w_a) x n
-    const d3 oA = xyz(WA), oB = xyz(WB);
-    const d3 u = dv - cross(lb * oB + la * oA, n);
-    const d3 ut = u - dot(u, n) * n;
-    const d3 Pt0 = mk(pa.y, pa.z, pa.w);
-    d3 Pt = Pt0 - rcp64(Dt) * ut;
-    Pt = clamp_scale(dot(Pt, Pt), mt * Pn) * Pt;
-    const P4 PaN = mkP4(Pn, Pt.x, Pt.y, Pt.z);
-    const d3 dPt = mk(PaN.y, PaN.z, PaN.w) - Pt0;
-    const d3 nxdPt = cross(n, dPt);
-    // 3. rolling (ball of radius mu_r R* P_n', readings R7/R8) on the spins updated by
-    //    the friction increment: w_b - w_a + (wtA la - wtB lb) n x dPt
-    d3 ur = (oB - oA) + (wtA * la - wtB * lb) * nxdPt;
-    if (rolling_dims == 2) ur = ur - dot(ur, n) * n;
-    const d3 Pr0 = mk(pb.x, pb.y, pb.z);
-    d3 Pr = Pr0 - rcp64(Dr) * ur;
-    Pr = clamp_scale(dot(Pr, Pr), mrRs * Pn) * Pr;
-    const P4 PbN = mkP4(Pr.x, Pr.y, Pr.z, 0);
-    const d3 dPr = mk(PbN.x, PbN.y, PbN.z) - Pr0;
-    // 4. contribution to self: a gets -(dPn n + dPt), -(la n x dPt + dPr);
-    //                          b gets +(dPn n + dPt), -lb n x dPt + dPr
-    HalfOut o;
-    const d3 L = dPn * n + dPt;
-    o.dL = isB ? L : mk(-L.x, -L.y, -L.z);
-    o.dA = isB ? ((-lb) * nxdPt + dPr) : mk(-(la * nxdPt.x + dPr.x), -(la * nxdPt.y + dPr.y), -(la * nxdPt.z + dPr.z));
-    o.Pa = PaN;
-    o.Pb = PbN;
-    return o;
-}
 
 constexpr int TP = 128;
 constexpr int NW = TP / 32;
@@ -182,7 +84,7 @@ constexpr int NW = TP / 32;
 #define SWEEP_MINB_PPT 4
 #endif
 #ifndef SWEEP_KERNEL
-#define SWEEP_KERNEL 0      // 0: k_sweep_tile (default, fastest measured), 1: k_sweep_pipe, 2: k_sweep_ppt
+#define SWEEP_KERNEL 0      // 0: k_sweep_t2 (default, fastest measured), 1: k_sweep_pipe, 2: k_sweep_ppt, 4: k_sweep_tile
 #endif
 
 // Tile sweep: the block stages the tile's states and CSR offsets in shared memory once; each
@@ -192,6 +94,23 @@ constexpr int NW = TP / 32;
 // depth is the longest segment of the chunk, and each segment's last lane adds the sum to the
 // owner's warp-private shared accumulator (one writer per particle per chunk): a fixed
 // summation order, hence deterministic, and no float atomics.
+__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+
+// EXP (timing experiments only): 1 no contact math, 2 no contact-record loads, 3 neither
+// contact-record nor partner global loads (math on shared memory only)
+__device__ __forceinline__ HalfOut fake_half(const double4 VA, const double4 WA, const double4 VB, const double4 WB,
+                                             const G4 g, const R4 rw, const P4 pa, const P4 pb)
+{
+    HalfOut o;
+    o.dL = mk(1e-30 * (VA.x + VB.x + g.x + rw.x + pa.x), 1e-30 * (VA.y + WB.y + g.y + rw.y + pb.x),
+              1e-30 * (WA.z + VB.z + g.z + rw.z + pa.y));
+    o.dA = mk(1e-30 * (WA.x + g.w + rw.w + pa.z), 1e-30 * (WB.x + pa.w + pb.y), 1e-30 * pb.z);
+    o.Pa = pa;
+    o.Pb = pb;
+    return o;
+}
+
+template <bool PF, int EXP = 0>
 __global__ void __launch_bounds__(TP, SWEEP_MINB) k_sweep_tile(int64_t N, const double4 *__restrict__ vin,
                                                       const double4 *__restrict__ win, double4 *__restrict__ vout,
                                                       double4 *__restrict__ wout, const uint32_t *__restrict__ inc_start,
@@ -224,14 +143,28 @@ __global__ void __launch_bounds__(TP, SWEEP_MINB) k_sweep_tile(int64_t N, const 
     const uint32_t s_me = me < hi_p ? sI[me] : 0u, e_me = me < hi_p ? sI[me + 1] : 0u;
     if (lo_p < np) {
         const uint32_t k0 = sI[lo_p], k1 = sI[hi_p];
-        uint2 ent_next = make_uint2(0, 0);
+        uint2 ent_next = make_uint2(0, 0), ent_nn = make_uint2(0, 0);
         if (k0 + lane < k1) ent_next = inc[k0 + lane];
+        if (PF && k0 + 32 + lane < k1) ent_nn = inc[k0 + 32 + lane];
         int carry = 0;                               // owner (warp-local) of the chunk's lane 0
         for (uint32_t kb = k0; kb < k1; kb += 32) {
             const uint32_t k = kb + lane;
             const bool valid = k < k1;
             const uint2 ent = ent_next;
-            if (kb + 32 + lane < k1) ent_next = inc[kb + 32 + lane];     // prefetch the next chunk
+            if (PF) {
+                // L1 prefetch of the next chunk's contact records and partner states while this
+                // chunk computes; incidence two chunks ahead in registers
+                ent_next = ent_nn;
+                if (kb + 32 + lane < k1) {
+                    const uint32_t c2 = ent_next.x & ~B_SIDE, p2 = ent_next.y;
+                    pf_l1(&geo[c2]); pf_l1(&row[c2]); pf_l1(&Pa_in[c2]); pf_l1(&Pb_in[c2]);
+                    if (!(p2 & PARTNER_EXT)) {
+                        const int64_t pl = (int64_t)p2 - p0;
+                        if (pl < 0 || pl >= np) { pf_l1(&vin[p2]); pf_l1(&win[p2]); }
+                    }
+                }
+                if (kb + 64 + lane < k1) ent_nn = inc[kb + 64 + lane];
+            } else if (kb + 32 + lane < k1) ent_next = inc[kb + 32 + lane];     // prefetch the next chunk
             // segment starts of this chunk (nonempty particles whose CSR range starts here)
             const bool starts = e_me > s_me && s_me >= kb && s_me < kb + 32;
             const unsigned smask = __reduce_or_sync(0xffffffffu, starts ? (1u << (s_me - kb)) : 0u);
@@ -249,7 +182,7 @@ __global__ void __launch_bounds__(TP, SWEEP_MINB) k_sweep_tile(int64_t N, const 
                 const double4 *pPV, *pPW;
                 double mt;
                 if (!(p & PARTNER_EXT)) {
-                    const int64_t pl = (int64_t)p - p0;
+                    const int64_t pl = EXP == 3 ? (int64_t)(p & (TP - 1)) : (int64_t)p - p0;
                     if (pl >= 0 && pl < np) { pPV = &sV[pl]; pPW = &sW[pl]; }
                     else { pPV = &vin[p]; pPW = &win[p]; }
                     mt = sp.mu_t;
@@ -261,8 +194,21 @@ __global__ void __launch_bounds__(TP, SWEEP_MINB) k_sweep_tile(int64_t N, const 
                     pPW = &sZero;
                 }
                 const double4 *pSV = &sV[o], *pSW = &sW[o];
-                const HalfOut r = half_contact(*(isB ? pPV : pSV), *(isB ? pPW : pSW), *(isB ? pSV : pPV),
-                                               *(isB ? pSW : pPW), isB, mt, geo[c], row[c], Pa_in[c], Pb_in[c],
+                G4 gc;
+                R4 rc;
+                P4 pac, pbc;
+                if (EXP >= 2) {
+                    gc = mkG4(0.6, 0.0, 0.8, 1e-4 + 1e-12 * c);
+                    rc = mkR4(1e5, 1e-3, 1e-3, 1e-3);
+                    pac = mkP4(1e-6, 0, 0, 0);
+                    pbc = mkP4(0, 0, 0, 0);
+                } else {
+                    gc = geo[c]; rc = row[c]; pac = Pa_in[c]; pbc = Pb_in[c];
+                }
+                const HalfOut r = EXP == 1 ? fake_half(*(isB ? pPV : pSV), *(isB ? pPW : pSW), *(isB ? pSV : pPV),
+                                                       *(isB ? pSW : pPW), gc, rc, pac, pbc)
+                                           : half_contact(*(isB ? pPV : pSV), *(isB ? pPW : pSW), *(isB ? pSV : pPV),
+                                               *(isB ? pSW : pPW), isB, mt, gc, rc, pac, pbc,
                                                sp.rolling_dims);
                 if (!isB) {
                     Pa_out[c] = r.Pa;
@@ -551,7 +497,9 @@ __global__ void __launch_bounds__(TPT, SWEEP_MINB_PPT) k_sweep_ppt(int64_t N, co
     wout[i] = Wn;
 }
 
-bool sweep_uses_order() { return SWEEP_KERNEL == 2; }
+static int g_sweep_variant = SWEEP_KERNEL;
+void set_sweep_variant(int v) { g_sweep_variant = v; }
+bool sweep_uses_order() { return g_sweep_variant == 2; }
 void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s)
 { if (N) k_tile_order<<<(unsigned)((N + TPT - 1) / TPT), TPT, 0, s>>>(N, inc_start, order); }
 
@@ -606,7 +554,7 @@ __global__ void k_apply(int64_t N, const double4 *__restrict__ vin, const double
 }
 
 // x^{k+1} = x^k + h v^{k+1} + reductions for the report and the rebuild trigger
-__global__ void k_integrate(int64_t N, double4 *__restrict__ pos, const double4 *__restrict__ vel,
+__global__ void k_integrate(int64_t N, const uint8_t *__restrict__ own, double4 *__restrict__ pos, const double4 *__restrict__ vel,
                             const double4 *__restrict__ ang, const double4 *__restrict__ xref, double h, double rho,
                             double *__restrict__ ke_part, StepScalars *sc)
 {
@@ -634,6 +582,7 @@ __global__ void k_integrate(int64_t N, double4 *__restrict__ pos, const double4 
             ke = 0.0;
             vm = 0.0;
         }
+        if (own && !own[i]) { disp = 0.0; ke = 0.0; vm = 0.0; }    // ghosts: reported by their owner
     }
     // block maxima first (non-negative doubles order like their bit patterns), one atomic per block
     sd[threadIdx.x] = disp;
@@ -670,12 +619,13 @@ __global__ void k_reduce_ke(const double *__restrict__ part, int64_t nb, StepSca
 }
 
 // plate reaction: F_p = (1/h) sum_{c in p} (P_n n + P_t), int64 fixed point (order-free, exact)
-__global__ void k_plate_sum(int64_t nc, const uint2 *__restrict__ cij, const G4 *__restrict__ geo,
+__global__ void k_plate_sum(int64_t nc, const uint8_t *__restrict__ own, const uint2 *__restrict__ cij, const G4 *__restrict__ geo,
                             const P4 *__restrict__ Pa, unsigned long long *__restrict__ acc,
                             unsigned int *__restrict__ pcount)
 {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nc) return;
+    if (own && !own[cij[c].x]) return;                   // a ghost's plate contact: its owner adds it
     const uint32_t j = cij[c].y;
     if ((j & (PARTNER_EXT | PARTNER_PLATE)) != (PARTNER_EXT | PARTNER_PLATE)) return;
     const int q = (j >> 4) & 0xF;
@@ -737,15 +687,15 @@ __global__ void k_scatter_P(int64_t nc, const uint32_t *__restrict__ ccand, cons
 }
 
 // sorted order -> ascending-gid order (rank of gid in the sorted gid list)
-__global__ void k_to_gid_order(int64_t N, const uint32_t *__restrict__ gid, const uint32_t *__restrict__ gid_sorted,
+__global__ void k_to_gid_order(int64_t N, const uint8_t *__restrict__ own, const uint32_t *__restrict__ gid, const uint32_t *__restrict__ gid_sorted,
                                const double4 *__restrict__ a, const double4 *__restrict__ b,
                                const double4 *__restrict__ c, double *__restrict__ oa, double *__restrict__ ob,
-                               double *__restrict__ oc, double *__restrict__ orad, uint32_t *__restrict__ ogid)
+                               double *__restrict__ oc, double *__restrict__ orad, uint32_t *__restrict__ ogid, int64_t n_sorted)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N) return;
+    if (i >= N || (own && !own[i])) return;         // ghosts are reported by their owner
     const uint32_t gv = gid[i];
-    int64_t lo = 0, hi = N;
+    int64_t lo = 0, hi = n_sorted;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (gid_sorted[mid] < gv) lo = mid + 1; else hi = mid;
@@ -788,10 +738,10 @@ void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin
                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s)
 {
     if (!N) return;
-    if (mode == SWEEP_MODE_SWEEP && SWEEP_KERNEL == 2) {
+    if (mode == SWEEP_MODE_SWEEP && g_sweep_variant == 2) {
         k_sweep_ppt<<<(unsigned)((N + TPT - 1) / TPT), TPT, 0, s>>>(N, order, vin, win, vout, wout, inc_start, inc, geo,
                                                                     row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
-    } else if (mode == SWEEP_MODE_SWEEP && SWEEP_KERNEL == 1) {
+    } else if (mode == SWEEP_MODE_SWEEP && g_sweep_variant == 1) {
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(k_sweep_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem));
@@ -799,36 +749,41 @@ void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin
         }
         k_sweep_pipe<<<(unsigned)((N + TPP - 1) / TPP), TPP, sizeof(PipeSmem), s>>>(
             N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
-    } else if (mode == SWEEP_MODE_SWEEP)
-        k_sweep_tile<<<(unsigned)((N + TP - 1) / TP), TP, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, geo, row,
+    } else if (mode == SWEEP_MODE_SWEEP && g_sweep_variant == 0)
+        launch_sweep_t2(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp, s);
+    else if (mode == SWEEP_MODE_SWEEP)
+        (g_sweep_variant == 3 ? k_sweep_tile<true> : g_sweep_variant == 41 ? k_sweep_tile<false, 1> :
+         g_sweep_variant == 42 ? k_sweep_tile<false, 2> : g_sweep_variant == 43 ? k_sweep_tile<false, 3> : k_sweep_tile<false>)<<<(unsigned)((N + TP - 1) / TP), TP, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, geo, row,
                                                                   Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
     else if (mode == SWEEP_MODE_APPLY)
         k_apply<SWEEP_MODE_APPLY><<<GRID(N)>>>(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, sp);
     else
         k_apply<SWEEP_MODE_FORCES><<<GRID(N)>>>(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, sp);
 }
-void launch_integrate(int64_t N, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
+void launch_integrate(int64_t N, const uint8_t *own, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
                       double rho, double *ke_part, StepScalars *sc, cudaStream_t s)
 {
     if (!N) return;
     const int64_t nb = (N + 255) / 256;
-    k_integrate<<<GRID(N)>>>(N, pos, vel, ang, xref, h, rho, ke_part, sc);
+    k_integrate<<<GRID(N)>>>(N, own, pos, vel, ang, xref, h, rho, ke_part, sc);
     k_reduce_ke<<<1, 256, 0, s>>>(ke_part, nb, sc);
 }
-void launch_plates(int64_t nc, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
-                   unsigned int *pcount, DevBoundary *bnd, double h, StepScalars *sc, cudaStream_t s)
+void launch_plate_sum(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
+                      unsigned int *pcount, cudaStream_t s)
 {
     cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 3 * DEM_MAX_PLATES, s);
     cudaMemsetAsync(pcount, 0, sizeof(unsigned int) * DEM_MAX_PLATES, s);
-    if (nc) k_plate_sum<<<GRID(nc)>>>(nc, cij, geo, Pa, acc, pcount);
-    k_boundary<<<1, 32, 0, s>>>(bnd, acc, pcount, h, sc);
+    if (nc) k_plate_sum<<<GRID(nc)>>>(nc, own, cij, geo, Pa, acc, pcount);
 }
+void launch_boundary(DevBoundary *bnd, const unsigned long long *acc, const unsigned int *pcount, double h, StepScalars *sc,
+                     cudaStream_t s)
+{ k_boundary<<<1, 32, 0, s>>>(bnd, acc, pcount, h, sc); }
 void launch_scatter_P(int64_t nc, const uint32_t *ccand, const P4 *Pa, const P4 *Pb, P4 *Pca, P4 *Pcb, cudaStream_t s)
 { if (nc) k_scatter_P<<<GRID(nc)>>>(nc, ccand, Pa, Pb, Pca, Pcb); }
-void launch_to_gid_order(int64_t N, const uint32_t *gid, const uint32_t *gid_sorted, const double4 *a,
+void launch_to_gid_order(int64_t N, int64_t n_sorted, const uint8_t *own, const uint32_t *gid, const uint32_t *gid_sorted, const double4 *a,
                          const double4 *b, const double4 *c, double *oa, double *ob, double *oc, double *orad,
                          uint32_t *ogid, cudaStream_t s)
-{ if (N) k_to_gid_order<<<GRID(N)>>>(N, gid, gid_sorted, a, b, c, oa, ob, oc, orad, ogid); }
+{ if (N) k_to_gid_order<<<GRID(N)>>>(N, own, gid, gid_sorted, a, b, c, oa, ob, oc, orad, ogid, n_sorted); }
 void launch_load_state(int64_t N, const double *x, const double *r, const double *v, const double *w,
                        const uint32_t *gid_in, double4 *pos, double4 *vel, double4 *ang, uint32_t *gid, cudaStream_t s)
 { if (N) k_load_state<<<GRID(N)>>>(N, x, r, v, w, gid_in, pos, vel, ang, gid); }

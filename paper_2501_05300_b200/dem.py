@@ -63,7 +63,9 @@ FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
 
 class DistDesc(C.Structure):
     _fields_ = [("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_void_p),
-                ("cuda_stream", C.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p)]
+                ("cuda_stream", C.c_void_p), ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_ctx", C.c_void_p),
+                ("slab_lo", C.c_double), ("slab_hi", C.c_double), ("transport", C.c_int32), ("pad0", C.c_int32),
+                ("loopback", C.c_void_p)]
 
 
 class StepReport(C.Structure):
@@ -110,7 +112,8 @@ CONTACT_DTYPE = np.dtype([("key", "<u8"), ("n", "<f8", (3,)), ("delta", "<f8"), 
 # every symbol include/dem.h declares (checked by tests/test_boundary.py)
 EXPORTS = ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts", "dem_get_forces",
            "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_set_timing", "dem_get_timing",
-           "dem_reset_timing", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
+           "dem_reset_timing", "dem_bench_sweeps", "dem_num_particles", "dem_num_local", "dem_nccl_unique_id",
+           "dem_loopback_create", "dem_loopback_destroy", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
            "dem_contact_network_length", "dem_plan_iterations", "dem_plan_timestep"]
 
 _lib = None
@@ -138,6 +141,17 @@ def lib():
         L.dem_set_timing.argtypes = [vp, i32]
         L.dem_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.dem_reset_timing.argtypes = [vp]
+        L.dem_bench_sweeps.argtypes = [vp, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.dem_num_particles.argtypes = [vp]
+        L.dem_num_particles.restype = C.c_int64
+        L.dem_num_local.argtypes = [vp]
+        L.dem_num_local.restype = C.c_int64
+        L.dem_nccl_unique_id.argtypes = [vp]
+        L.dem_nccl_unique_id.restype = C.c_int
+        L.dem_loopback_create.argtypes = [i32]
+        L.dem_loopback_create.restype = vp
+        L.dem_loopback_destroy.argtypes = [vp]
+        L.dem_loopback_destroy.restype = None
         L.dem_stream.argtypes = [vp]
         L.dem_stream.restype = vp
         L.dem_destroy.argtypes = [vp]
@@ -153,7 +167,7 @@ def lib():
         L.dem_plan_timestep.restype = d
         for f in ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts",
                   "dem_get_forces", "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall",
-                  "dem_set_timing", "dem_get_timing", "dem_reset_timing", "dem_destroy"]:
+                  "dem_set_timing", "dem_get_timing", "dem_reset_timing", "dem_bench_sweeps", "dem_destroy"]:
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -176,6 +190,37 @@ def plan_timestep(d, eps, rho, sigma):
     return lib().dem_plan_timestep(d, eps, rho, sigma)
 
 
+# ---------------------------------------------------------------- x-slab decomposition plumbing
+def nccl_unique_id():
+    """A fresh ncclUniqueId (128 bytes) for rank 0 to broadcast (torch.distributed)."""
+    buf = (C.c_ubyte * 128)()
+    st = lib().dem_nccl_unique_id(buf)
+    if st != DEM_OK:
+        raise DemError(st, lib().dem_last_error(None).decode())
+    return bytes(buf)
+
+
+class LoopbackGroup:
+    """world_size ranks inside one process (one host thread per rank) exchanging ghosts with
+    device copies: the decomposition on a single GPU (include/dem.h)."""
+
+    def __init__(self, world_size):
+        self.world_size = world_size
+        self.handle = lib().dem_loopback_create(world_size)
+
+    def close(self):
+        if self.handle:
+            lib().dem_loopback_destroy(self.handle)
+            self.handle = None
+
+
+def slab_bounds(x, world_size, lo, hi):
+    """Slab faces at particle-count quantiles of x; outer faces at the box."""
+    import numpy as _np
+    q = _np.quantile(_np.asarray(x, float), _np.arange(1, world_size) / world_size) if world_size > 1 else []
+    return [lo] + [float(v) for v in q] + [hi]
+
+
 # ---------------------------------------------------------------- bed
 def _ptr(a):
     return None if a is None else a.ctypes.data
@@ -192,7 +237,10 @@ class Bed:
     """One DEM context (one GPU).  Host arrays in, host arrays out, gid order."""
 
     def __init__(self, pos, radius, vel=None, angvel=None, gid=None, *, material=None, solver=None, box=None,
-                 stream=None, torch_allocator=True, device=0):
+                 stream=None, torch_allocator=True, device=0, dist=None):
+        """dist (x-slab decomposition, include/dem.h): dict(rank, world_size, slab=(lo, hi),
+        transport='nccl' with nccl_id=<128 bytes of rank 0> | 'loopback' with group=LoopbackGroup);
+        pos... are then this rank's particles (inside its slab)."""
         import torch  # plumbing: stream + caching allocator
         self._torch = torch
         torch.cuda.set_device(device)
@@ -229,8 +277,17 @@ class Bed:
         desc.parts.pos, desc.parts.radius = _ptr(pos), _ptr(radius)
         desc.parts.vel, desc.parts.angvel, desc.parts.gid = _ptr(vel), _ptr(angvel), _ptr(gid)
         desc.parts.on_device = 0
+        dcfg = dist
         dist = DistDesc()
         dist.rank, dist.world_size = 0, 1
+        if dcfg and dcfg.get("world_size", 1) > 1:
+            dist.rank, dist.world_size = int(dcfg["rank"]), int(dcfg["world_size"])
+            dist.slab_lo, dist.slab_hi = float(dcfg["slab"][0]), float(dcfg["slab"][1])
+            if dcfg.get("transport", "nccl") == "loopback":
+                dist.transport, dist.loopback = 1, dcfg["group"].handle
+            else:
+                self._nccl_id = (C.c_ubyte * 128).from_buffer_copy(dcfg["nccl_id"])
+                dist.transport, dist.nccl_unique_id = 0, C.cast(self._nccl_id, C.c_void_p)
         dist.cuda_stream = self.stream.cuda_stream
         if torch_allocator:
             dev, strm = device, self.stream.cuda_stream
@@ -291,9 +348,18 @@ class Bed:
                 setattr(s, k, v)
         self._check(lib().dem_set_solver(self._h, C.byref(s)))
 
+    @property
+    def n_owned(self):
+        """Particles this rank owns now (all of them with world_size 1)."""
+        return int(lib().dem_num_particles(self._h))
+
+    @property
+    def n_local(self):
+        return int(lib().dem_num_local(self._h))
+
     # -- state
     def get_state(self):
-        n = self.n
+        n = self.n_owned
         out = {k: np.empty((n, 3)) for k in ("pos", "vel", "angvel")}
         out["radius"] = np.empty(n)
         out["gid"] = np.empty(n, dtype=np.uint32)
@@ -302,9 +368,12 @@ class Bed:
         return out
 
     def get_state_device(self, out):
-        """out: dict of torch CUDA tensors pos/vel/angvel (n,3) float64, radius (n,) f64, gid (n,) int32."""
-        v = StateView(self.n, *(out[k].data_ptr() if k in out else None for k in ("pos", "vel", "angvel", "radius", "gid")), 1, 0)
+        """out: dict of torch CUDA tensors pos/vel/angvel (cap,3) float64, radius (cap,) f64, gid (cap,)
+        int32 with cap >= n_owned; fills the first n_owned rows (gid order) and returns n_owned."""
+        cap = min(int(t.shape[0]) for t in out.values())
+        v = StateView(cap, *(out[k].data_ptr() if k in out else None for k in ("pos", "vel", "angvel", "radius", "gid")), 1, 0)
         self._check(lib().dem_get_state(self._h, C.byref(v)))
+        return int(v.n)
 
     def set_state(self, pos, radius, vel=None, angvel=None, gid=None, hist=None):
         pos, radius = _f64(pos, (-1, 3)), _f64(radius)
@@ -340,8 +409,9 @@ class Bed:
         return out
 
     def get_forces(self):
-        F = np.empty((self.n, 3))
-        T = np.empty((self.n, 3))
+        n = self.n_owned
+        F = np.empty((n, 3))
+        T = np.empty((n, 3))
         self._check(lib().dem_get_forces(self._h, F.ctypes.data, T.ctypes.data, 0))
         return F, T
 
@@ -372,6 +442,12 @@ class Bed:
 
     def reset_timing(self):
         self._check(lib().dem_reset_timing(self._h))
+
+    def bench_sweeps(self, variant, n):
+        """Diagnostic: (ms per sweep, max relative |dv| vs the shipped kernel) of a sweep variant."""
+        ms, dv = C.c_double(), C.c_double()
+        self._check(lib().dem_bench_sweeps(self._h, variant, n, C.byref(ms), C.byref(dv)))
+        return ms.value, dv.value
 
     def timing(self):
         t = Timing()

@@ -195,3 +195,20 @@ def random_cloud(n, box_lo, box_hi, r_min, r_max, seed, v_scale=0.0, w_scale=0.0
     w = rng.normal(0.0, 1.0, size=(n, 3)) * w_scale
     gid = rng.permutation(n).astype(np.uint32)
     return Bed(x=x, r=r, v=v, w=w, gid=gid, box_lo=tuple(lo), box_hi=tuple(hi), name="cloud")
+
+
+# ----------------------------------------------------------------------------- x-slab pieces
+
+def shift_slab(bed: Bed, rank: int, world: int) -> tuple:
+    """Rank r's piece of a bed made of `world` copies of `bed`'s box laid end to end along x
+    (each copy generated with its own seed by the caller): positions shifted by r L, gids offset
+    by r n (unique over the job), box spanning all pieces.  Returns (bed, (slab_lo, slab_hi))."""
+    L = bed.box_hi[0] - bed.box_lo[0]
+    x = bed.x.copy()
+    x[:, 0] += rank * L
+    gid = (bed.gid.astype(np.int64) + rank * bed.n).astype(np.uint32)
+    lo = bed.box_lo[0] + rank * L
+    out = Bed(x=x, r=bed.r, v=bed.v, w=bed.w, gid=gid, box_lo=bed.box_lo,
+              box_hi=(bed.box_lo[0] + world * L,) + tuple(bed.box_hi[1:]), name=f"{bed.name}-slab{rank}of{world}",
+              meta=dict(bed.meta))
+    return out, (lo, lo + L)

@@ -128,3 +128,50 @@ def compare_step(bed, n_it=30, dt=1e-5, with_walls=True, hist=None, material=Non
     res["detail"] = {"eF": eF, "eT": eT, "c_ref": c_ref, "c_gpu": c_gpu, "state": st, "ref_x": Wo.x[order],
                      "ref_v": Wo.v[order], "ref_w": Wo.w[order]}
     return res
+
+
+def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bounds=None):
+    """Run bed split into G x-slabs as G loopback ranks of this process (one host thread each,
+    include/dem.h dem_loopback_create), n_steps; returns merged state (gid order), the merged
+    contact list (key order), per-rank reports and the slab bounds."""
+    import threading
+
+    from paper_2501_05300_b200 import dem
+    lo, hi = box["lo"], box["hi"]
+    if bounds is None:
+        bounds = dem.slab_bounds(bed.x[:, 0], G, lo[0], hi[0])
+    grp = dem.LoopbackGroup(G)
+    res = [None] * G
+    err = [None] * G
+
+    def rank_main(r):
+        try:
+            m = (bed.x[:, 0] >= bounds[r]) & (bed.x[:, 0] < bounds[r + 1])
+            b = dem.Bed(bed.x[m], bed.r[m], bed.v[m], bed.w[m], bed.gid[m], solver=solver, box=box, material=material,
+                        dist=dict(rank=r, world_size=G, slab=(bounds[r], bounds[r + 1]), transport="loopback",
+                                  group=grp))
+            pids = [b.add_plate(**p) for p in plates]
+            reps = [b.step(1) for _ in range(n_steps)]
+            res[r] = dict(state=b.get_state(), contacts=b.get_contacts(), forces=b.get_forces(), reports=reps,
+                          plates=[b.get_plate(p) for p in pids], n_local=b.n_local, n_owned=b.n_owned)
+            b.close()
+        except Exception as e:   # noqa: BLE001 -- surfaced by the caller
+            err[r] = e
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    grp.close()
+    for e in err:
+        if e is not None:
+            raise e
+    st = {k: np.concatenate([r["state"][k] for r in res]) for k in res[0]["state"]}
+    o = np.argsort(st["gid"])
+    st = {k: v[o] for k, v in st.items()}
+    F = np.concatenate([r["forces"][0] for r in res])[o]
+    T = np.concatenate([r["forces"][1] for r in res])[o]
+    c = np.concatenate([r["contacts"] for r in res])
+    c = c[np.argsort(c["key"], kind="stable")]
+    return dict(state=st, forces=(F, T), contacts=c, ranks=res, bounds=bounds)
