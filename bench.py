@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no baseline, no clocks")
+    ap.add_argument("--decompose", action="store_true",
+                    help="run the x-slab decomposition (NCCL transport) even at N = 1 (code-path check)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -191,10 +193,11 @@ def main():
     w = WORKLOADS[wl]
     n_it = args.n_it or dem.plan_iterations(network_length(w["bands"]), 0.02)
     dcfg = None
-    if world > 1:
+    if world > 1 or args.decompose:
         bed_in, slab = make_slab(wl, rank, world)
         obj = [dem.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
+        if dist:
+            dist.broadcast_object_list(obj, src=0)
         dcfg = dict(rank=rank, world_size=world, slab=slab, transport="nccl", nccl_id=obj[0])
     else:
         bed_in = make_bed(wl)
@@ -255,8 +258,8 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "n_particles": N, "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "levels": len(w["bands"]),
-                   "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)" if world > 1
-                   else "single GPU",
+                   "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)"
+                   if (world > 1 or args.decompose) else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)",
                    "precision": "fp64 state and row math; fp64 normals/rows, fp32 impulses"},
         "contacts_per_s": contacts_per_s,

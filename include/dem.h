@@ -107,7 +107,9 @@ typedef struct {
  * and passes only those to dem_create_bed; the library keeps ghost copies of the neighbours'
  * particles within 2 r_max + 2 skin of the shared faces, refreshes their velocities after every
  * Jacobi sweep, and moves ownership at each rebuild.  create, step and destroy are then
- * collective over the ranks. */
+ * collective over the ranks.  The outer faces of rank 0 and rank world_size-1 are open (they own
+ * whatever lies beyond the box).  world_size 1 with a transport (nccl_unique_id or loopback set)
+ * runs the decomposed code path on one rank with no neighbours (transport self-test). */
 typedef struct {
     int32_t rank, world_size;
     const void *nccl_unique_id;        /* transport 0, world_size > 1: the 128-byte ncclUniqueId of

@@ -112,7 +112,7 @@ struct dem_ctx {
 };
 
 // ------------------------------------------------------------------ helpers
-#define OWN(ctx) ((ctx)->G > 1 ? (const uint8_t *)(ctx)->own : (const uint8_t *)nullptr)
+#define OWN(ctx) ((ctx)->tp ? (const uint8_t *)(ctx)->own : (const uint8_t *)nullptr)
 #define CK(call)                                                                      \
     do {                                                                              \
         cudaError_t e_ = (call);                                                      \
@@ -211,7 +211,7 @@ static dem_status setup_levels(dem_ctx *ctx, const std::vector<double> &r)
 {
     double rmin = INFINITY, rmax = 0;
     for (double x : r) { rmin = std::min(rmin, x); rmax = std::max(rmax, x); }
-    if (ctx->G > 1) {
+    if (ctx->tp) {
         // every rank takes the same size classes, skin and ghost band (global radius range)
         double v[2] = {-rmin, rmax};
         if (!ctx->tp->allreduce_f64(v, 2, 1, ctx->s, ctx->err)) return DEM_ERR_NCCL;
@@ -229,7 +229,7 @@ static dem_status setup_levels(dem_ctx *ctx, const std::vector<double> &r)
         ctx->rmax_lv[L] = std::max(ctx->rmax_lv[L], x);
         ctx->lv_present[L] = true;
     }
-    if (ctx->G > 1) {
+    if (ctx->tp) {
         // cell sizes from the global per-level maxima: ghosts and migrants of any size class fit
         if (!ctx->tp->allreduce_f64(ctx->rmax_lv, DEM_MAX_LEVELS, 1, ctx->s, ctx->err)) return DEM_ERR_NCCL;
         for (int L = 0; L < DEM_MAX_LEVELS; L++) ctx->lv_present[L] = ctx->rmax_lv[L] > 0.0;
@@ -484,7 +484,7 @@ static dem_status xchg(dem_ctx *ctx, const void *const snd[2], const size_t sb[2
 // ghost velocities (v, c/m; w, c/I) from their owners, after every update of the velocities
 static dem_status halo(dem_ctx *ctx, double4 *vel, double4 *ang)
 {
-    if (ctx->G == 1) return DEM_OK;
+    if (!ctx->tp) return DEM_OK;
     for (int k = 0; k < 2; k++) launch_pack_halo(ctx->n_send[k], ctx->send_idx[k], vel, ang, ctx->hs[k], ctx->s);
     const void *snd[2] = {ctx->hs[0], ctx->hs[1]};
     void *rcv[2] = {ctx->hr[0], ctx->hr[1]};
@@ -621,7 +621,7 @@ static dem_status rebuild(dem_ctx *ctx)
     cudaStream_t s = ctx->s;
     if (!ctx->hist_pending) TRY(export_history(ctx));
     ctx->hist_pending = false;
-    if (ctx->G > 1) {
+    if (ctx->tp) {
         TRY(ensure_keys(ctx, std::max<int64_t>(ctx->N, 1)));
         TRY(redistribute(ctx));
     } else {
@@ -646,7 +646,7 @@ static dem_status rebuild(dem_ctx *ctx)
         CK(cudaMemsetAsync(ctx->cstart, 0, ctx->ncells * sizeof(uint32_t), s));
         CK(cudaMemsetAsync(ctx->cend, 0, ctx->ncells * sizeof(uint32_t), s));
         launch_cells(N, ctx->keys[0], ctx->grid, ctx->cstart, ctx->cend, s);
-        if (ctx->G > 1) TRY(finish_decomposition(ctx, ctx->vals[0]));   // reuses keys/vals after the cells
+        if (ctx->tp) TRY(finish_decomposition(ctx, ctx->vals[0]));   // reuses keys/vals after the cells
         // multi-level broad phase: count, scan, fill
         launch_broad(false, N, ctx->pos, ctx->grid, ctx->cstart, ctx->cend, ctx->db, ctx->co_start, nullptr, s);
         ctx->launches += 2;
@@ -719,7 +719,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     CK(cudaMemcpyAsync(ctx->hsc, ctx->dsc, sizeof(StepScalars), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     bool impact = ctx->hsc->impact != 0 && nc > 0;
-    if (ctx->G > 1) {
+    if (ctx->tp) {
         double f = impact ? 1.0 : 0.0;
         if (!ctx->tp->allreduce_f64(&f, 1, 1, s, ctx->err)) return DEM_ERR_NCCL;
         impact = f > 0.0;
@@ -775,7 +775,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     launch_integrate(N, OWN(ctx), ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->xref, sp.h, sp.rho, ctx->ke_part,
                      ctx->dsc, s);
     launch_plate_sum(nc, OWN(ctx), ctx->cij, ctx->geo, ctx->Pfa, ctx->pacc, ctx->pcount, s);
-    if (ctx->G > 1 && ctx->hb.n_plates > 0) {
+    if (ctx->tp && ctx->hb.n_plates > 0) {
         // plate reactions: exact int64 sums over the ranks (each contact counted by its owner)
         unsigned long long acc[3 * DEM_MAX_PLATES];
         unsigned int pc[DEM_MAX_PLATES];
@@ -799,7 +799,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     CK(cudaStreamSynchronize(s));
     CK(cudaGetLastError());
     StepScalars sc = *ctx->hsc;
-    if (ctx->G > 1) {
+    if (ctx->tp) {
         // global report and decisions: every rank takes the same rollback / rebuild branch
         double mx[3], sm[5];
         std::memcpy(&mx[0], &sc.max_disp_bits, 8);
@@ -847,7 +847,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     ctx->step++;
     rep->step = ctx->step;
     rep->time = ctx->hb.time;
-    rep->n_contacts = ctx->G > 1 ? (int64_t)sc.n_pp + sc.n_wall + sc.n_plate : (int64_t)nc;
+    rep->n_contacts = ctx->tp ? (int64_t)sc.n_pp + sc.n_wall + sc.n_plate : (int64_t)nc;
     rep->n_pp = sc.n_pp;
     rep->n_wall = sc.n_wall;
     rep->n_plate = sc.n_plate;
@@ -884,7 +884,7 @@ static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, con
         if (!(r[i] > 0) || !std::isfinite(r[i])) { ctx->err = "radius must be positive and finite"; return DEM_ERR_INVALID; }
         for (int k = 0; k < 3; k++) if (!std::isfinite(x[3 * i + k])) { ctx->err = "non-finite position"; return DEM_ERR_INVALID; }
         if (g[i] >= PLATE_KEY_BASE) { ctx->err = "gid must be < 2^32-4096"; return DEM_ERR_INVALID; }
-        if (ctx->G > 1 && !((ctx->rank == 0 || x[3 * i] >= ctx->slab_lo) && (ctx->rank == ctx->G - 1 || x[3 * i] < ctx->slab_hi))) {
+        if (ctx->tp && !((ctx->rank == 0 || x[3 * i] >= ctx->slab_lo) && (ctx->rank == ctx->G - 1 || x[3 * i] < ctx->slab_hi))) {
             ctx->err = "particle outside this rank's slab [slab_lo, slab_hi)";
             return DEM_ERR_INVALID;
         }
@@ -948,8 +948,11 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
         return DEM_ERR_INVALID;
     }
     if (desc->parts.n >= (int64_t)0x7FFFFFFF) { g_create_err = "too many particles for one context"; return DEM_ERR_INVALID; }
-    if (dist && dist->world_size > 1) {
-        if (dist->rank < 0 || dist->rank >= dist->world_size || !(dist->slab_lo < dist->slab_hi) ||
+    // decomposition active: world_size > 1, or any explicit transport (one rank over NCCL/loopback
+    // runs the same decomposed code path with no neighbours: the transport self-test)
+    const bool decomposed = dist && (dist->world_size > 1 || dist->nccl_unique_id || dist->loopback);
+    if (decomposed) {
+        if (dist->world_size < 1 || dist->rank < 0 || dist->rank >= dist->world_size || !(dist->slab_lo < dist->slab_hi) ||
             (dist->transport != 0 && dist->transport != 1) || (dist->transport == 1 && !dist->loopback)) {
             g_create_err = "invalid decomposition (rank, slab_lo < slab_hi, transport 0 NCCL | 1 loopback)";
             return DEM_ERR_INVALID;
@@ -969,7 +972,7 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
         ctx->own_stream = true;
     }
     if (dist && dist->alloc && dist->free) { ctx->ualloc = dist->alloc; ctx->ufree = dist->free; ctx->actx = dist->alloc_ctx; }
-    if (dist && dist->world_size > 1) {
+    if (decomposed) {
         ctx->G = dist->world_size;
         ctx->rank = dist->rank;
         ctx->slab_lo = dist->slab_lo;
@@ -1068,7 +1071,7 @@ dem_status dem_get_state(dem_ctx *ctx, dem_state_view *v)
 dem_status dem_set_state(dem_ctx *ctx, const dem_state_view *st, const dem_contact_view *hist)
 {
     if (!ctx || !st) return DEM_ERR_INVALID;
-    if (ctx->G > 1) { ctx->err = "dem_set_state needs world_size 1"; return DEM_ERR_INVALID; }
+    if (ctx->tp) { ctx->err = "dem_set_state needs world_size 1"; return DEM_ERR_INVALID; }
     if (st->n != ctx->N || (st->n && (!st->pos || !st->radius))) { ctx->err = "set_state: bad view"; return DEM_ERR_INVALID; }
     // history: sorted by key on the host, uploaded for the next rebuild's sorted-key lookup
     std::vector<uint64_t> hk;
@@ -1266,7 +1269,7 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
 {
     if (!ctx || n < 1) return DEM_ERR_INVALID;
     if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
-    if (ctx->G > 1) { ctx->err = "dem_bench_sweeps needs world_size 1"; return DEM_ERR_INVALID; }
+    if (ctx->tp) { ctx->err = "dem_bench_sweeps needs world_size 1"; return DEM_ERR_INVALID; }
     const int64_t N = ctx->N, nc = ctx->nc;
     cudaStream_t s = ctx->s;
     double *cb = nullptr;

@@ -280,7 +280,7 @@ class Bed:
         dcfg = dist
         dist = DistDesc()
         dist.rank, dist.world_size = 0, 1
-        if dcfg and dcfg.get("world_size", 1) > 1:
+        if dcfg:                   # decomposed (world_size 1 with a transport: the transport self-test)
             dist.rank, dist.world_size = int(dcfg["rank"]), int(dcfg["world_size"])
             dist.slab_lo, dist.slab_hi = float(dcfg["slab"][0]), float(dcfg["slab"][1])
             if dcfg.get("transport", "nccl") == "loopback":

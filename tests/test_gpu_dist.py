@@ -89,3 +89,29 @@ def test_loopback_plate_reaction_summed_over_ranks():
         p = r["plates"][0]
         assert p["n_contacts"] == ref["plates"][0]["n_contacts"]
         assert np.abs(np.array(p["force"]) - f_ref).max() <= 1e-7 * np.abs(f_ref).max()
+
+
+@pytest.mark.parametrize("transport", ["nccl", "loopback"])
+def test_single_rank_transport_selftest_bit_identical(transport):
+    """world_size 1 over a real transport (NCCL communicator of one rank, or a loopback group of
+    one) runs the decomposed code path -- ownership pass, band exchange with no neighbours,
+    allreduces -- and must reproduce the undecomposed context bit for bit."""
+    D = dem()
+    bed, box = drifting_bed(drift=1.0, seed=7)
+    solver = dict(dt=2e-5, n_iter=20)
+    ref = single(bed, 6, solver, box)
+    grp = D.LoopbackGroup(1) if transport == "loopback" else None
+    cfg = dict(rank=0, world_size=1, slab=(0.0, 0.12), transport=transport)
+    if grp:
+        cfg["group"] = grp
+    else:
+        cfg["nccl_id"] = D.nccl_unique_id()
+    b = D.Bed(bed.x, bed.r, bed.v, bed.w, bed.gid, solver=solver, box=box, dist=cfg)
+    reps = [b.step(1) for _ in range(6)]
+    st = b.get_state()
+    b.close()
+    if grp:
+        grp.close()
+    for k in ("pos", "vel", "angvel"):
+        assert np.array_equal(st[k], ref["state"][k]), k
+    assert [r["n_contacts"] for r in reps] == [r["n_contacts"] for r in ref["reports"]]
