@@ -1293,6 +1293,19 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
         CK(cudaMemcpyAsync(&maxb, mb6, 4, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
+    uint4 *xl9 = nullptr;
+    unsigned int caps9[3] = {0, 0, 0};
+    if (variant == 50) {
+        TRY(A(ctx, &ca6, N + 2)); TRY(A(ctx, &xc6, N + 2)); TRY(A(ctx, &xs6, N + 2)); TRY(A(ctx, &xl9, nc + 1));
+        TRY(A(ctx, &mb6, 3));
+        launch_inc9(N, ctx->co_start, ctx->cscan, ctx->inc_start, ctx->inc, ca6, xc6, xs6, xl9, mb6, ctx->scan_tmp, s,
+                    &ctx->launches);
+        CK(cudaMemcpyAsync(caps9, mb6, 12, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (getenv("DEM_DEBUG"))
+            fprintf(stderr, "[dem] sweep9 tile %d caps A %u X %u smem %zu B\n", sweep9_tile(), caps9[0], caps9[1],
+                    sweep9_smem_bytes(caps9[0], caps9[1], caps9[2]));
+    }
     uint4 *xl8 = nullptr;
     if (variant == 30) {
         TRY(A(ctx, &xl8, nc + 1));
@@ -1310,15 +1323,48 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
         const int var = pass == 0 ? 0 : variant;
         CK(cudaMemcpyAsync(ctx->Pwa, ctx->Pfa, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(ctx->Pwb, ctx->Pfb, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
+        if (var >= 60) {
+            // layout experiment: P8 / VW interleaved records (sweep_t2.cu, run_sweep_t3)
+            void *scr = nullptr;
+            double4 *r3 = nullptr;
+            TRY(dalloc(ctx, &scr, (size_t)nc * 64 + (size_t)N * 128 + 1024));
+            TRY(A(ctx, &r3, N + 1));
+            P4 *pa2[2] = {ctx->Pwa, spa}, *pb2[2] = {ctx->Pwb, spb};
+            run_sweep_t3(var - 60, n, N, nc, ctx->vel[ctx->cur], ctx->ang[ctx->cur], vbuf, wbuf, ctx->inc_start, ctx->inc,
+                         ctx->geo, ctx->row, pa2, pb2, scr, ctx->db, ctx->sp, s, r3, ctx->ev[6], ctx->ev[7]);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(s));
+            cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
+            vres = r3;
+            launch_maxdiff(N, vres, ref, md, s);
+            unsigned long long h3[2] = {0, 0};
+            CK(cudaMemcpyAsync(h3, md, sizeof(h3), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            double d3v, m3;
+            std::memcpy(&d3v, &h3[0], 8);
+            std::memcpy(&m3, &h3[1], 8);
+            if (ms_per_sweep) *ms_per_sweep = ms / n;
+            if (max_dv_rel) *max_dv_rel = m3 > 0 ? d3v / m3 : d3v;
+            dfree(ctx, scr);
+            dfree(ctx, r3);
+            dfree(ctx, cb); dfree(ctx, ref); dfree(ctx, md);
+            for (void *q : {(void *)ca6, (void *)bs6, (void *)xc6, (void *)xs6, (void *)bsl6, (void *)xl6, (void *)mb6,
+                            (void *)xl8, (void *)xl9})
+                dfree(ctx, q);
+            return DEM_OK;
+        }
         const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
         P4 *pai = ctx->Pwa, *pbi = ctx->Pwb, *pao = spa, *pbo = spb;
         cudaEventRecord(ctx->ev[6], s);
         for (int it = 0; it < n; it++) {
             double4 *vo = vbuf[it & 1], *wo = wbuf[it & 1];
-            if (var < 10 || var >= 40) {
+            if (var < 10 || (var >= 40 && var < 50)) {
                 set_sweep_variant(var);
                 launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, vi, wi, vo, wo, ctx->inc_start, ctx->inc, ctx->geo, ctx->row,
                              pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
+            } else if (var == 50) {
+                launch_sweep9(N, caps9[0], caps9[1], caps9[2], vi, wi, vo, wo, ca6, xs6, xl9, ctx->inc_start, ctx->inc, ctx->cij,
+                              ctx->geo, ctx->row, pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
             } else if (var == 30) {
                 launch_sweep8(N, maxb, vi, wi, vo, wo, ca6, bs6, xs6, xl8, ctx->cij, bsl6, ctx->geo, ctx->row, pai, pbi, pao,
                               pbo, ctx->db, ctx->sp, s);
@@ -1354,7 +1400,7 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     dfree(ctx, cb);
     dfree(ctx, ref);
     dfree(ctx, md);
-    for (void *q : {(void *)ca6, (void *)bs6, (void *)xc6, (void *)xs6, (void *)bsl6, (void *)xl6, (void *)mb6, (void *)xl8}) dfree(ctx, q);
+    for (void *q : {(void *)ca6, (void *)bs6, (void *)xc6, (void *)xs6, (void *)bsl6, (void *)xl6, (void *)mb6, (void *)xl8, (void *)xl9}) dfree(ctx, q);
     return DEM_OK;
 }
 

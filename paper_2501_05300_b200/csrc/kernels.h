@@ -93,3 +93,18 @@ void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 
                      const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row, const P4 *Pa_in,
                      const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp,
                      cudaStream_t s);
+// sweep9.cu: staged tile sweep (each contact once per tile, cp.async staging, reduction from increments)
+void launch_inc9(int64_t N, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start, const uint2 *inc,
+                 uint32_t *ca, uint32_t *xcnt, uint32_t *xstart, uint4 *xlist, unsigned int *caps, void *scan_tmp,
+                 cudaStream_t s, long long *launches);
+size_t sweep9_smem_bytes(unsigned capA, unsigned capX, unsigned capI);
+int sweep9_tile();
+void launch_sweep9(int64_t N, unsigned capA, unsigned capX, unsigned capI, const double4 *vin, const double4 *win, double4 *vout,
+                   double4 *wout, const uint32_t *ca, const uint32_t *xstart, const uint4 *xlist,
+                   const uint32_t *inc_start, const uint2 *inc, const uint2 *cij, const G4 *geo, const R4 *row,
+                   const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd,
+                   const SolveParams &sp, cudaStream_t s);
+void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin, const double4 *win, double4 *vbuf[2],
+                  double4 *wbuf[2], const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
+                  P4 *Pa[2], P4 *Pb[2], void *scratch, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s,
+                  double4 *vres, cudaEvent_t e0, cudaEvent_t e1);

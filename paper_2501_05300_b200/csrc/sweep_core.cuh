@@ -26,6 +26,64 @@ struct ContactOut {
     P4 Pa, Pb;       // new impulses (P_n, P_t) / (P_r, 0)
 };
 
+#ifdef DEM_F32MATH
+// Experimental (precision study): the projected update in fp32 arithmetic.  The
+// cancelling differences (v_b - v_a, lever-arm spin sums, w_b - w_a) are formed in fp64 first;
+// impulses are fp32 storage anyway; increments are returned in fp64 for the fp64 accumulation.
+struct f3 { float x, y, z; };
+__device__ __forceinline__ f3 f3m(float x, float y, float z) { return f3{x, y, z}; }
+__device__ __forceinline__ f3 operator+(f3 a, f3 b) { return f3{a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ f3 operator-(f3 a, f3 b) { return f3{a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ f3 operator*(float s, f3 a) { return f3{s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ float dotf(f3 a, f3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ f3 crossf(f3 a, f3 b) { return f3{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+__device__ __forceinline__ f3 tof(d3 a) { return f3{(float)a.x, (float)a.y, (float)a.z}; }
+__device__ __forceinline__ d3 tod(f3 a) { return d3{(double)a.x, (double)a.y, (double)a.z}; }
+__device__ __forceinline__ float rcpf(float x) { float r = __frcp_rn(x); return r; }
+__device__ __forceinline__ float clampf(float m2, float lim) { return m2 > lim * lim ? lim * rsqrtf(m2) : 1.0f; }
+
+__device__ __forceinline__ ContactOut contact_core(const double4 VA, const double4 WA, const double4 VB,
+                                                   const double4 WB, double mt_, const d3 n_, double mrRs_, double S_,
+                                                   double b_, double la_, double lb_, const P4 pa, const P4 pb,
+                                                   int rolling_dims)
+{
+    const f3 n = tof(n_);
+    const float la = (float)la_, lb = (float)lb_, S = (float)S_, b = (float)b_, mt = (float)mt_, mrRs = (float)mrRs_;
+    const float wA = (float)VA.w, wtA = (float)WA.w, wB = (float)VB.w, wtB = (float)WB.w;
+    const float Dn = wA + wB;
+    const float Dt = Dn + la * la * wtA + lb * lb * wtB;
+    const float Dr = wtA + wtB;
+    const f3 dv = tof(xyz(VB) - xyz(VA));
+    const f3 lw = tof(lb_ * xyz(WB) + la_ * xyz(WA));
+    const f3 dw = tof(xyz(WB) - xyz(WA));
+    ContactOut o;
+    const float Pn0 = pa.x;
+    float Pn = Pn0 - (dotf(n, dv) + S * Pn0 - b) * rcpf(Dn + S);
+    Pn = Pn > 0.0f ? Pn : 0.0f;
+    o.Pa.x = Pn;
+    const f3 u = dv - crossf(lw, n);
+    const f3 ut = u - dotf(u, n) * n;
+    const f3 Pt0 = f3m(pa.y, pa.z, pa.w);
+    f3 Pt = Pt0 - rcpf(Dt) * ut;
+    Pt = clampf(dotf(Pt, Pt), mt * Pn) * Pt;
+    o.Pa.y = Pt.x; o.Pa.z = Pt.y; o.Pa.w = Pt.z;
+    const f3 dPt = Pt - Pt0;
+    const f3 nxdPt = crossf(n, dPt);
+    f3 ur = dw + (wtA * la - wtB * lb) * nxdPt;
+    if (rolling_dims == 2) ur = ur - dotf(ur, n) * n;
+    const f3 Pr0 = f3m(pb.x, pb.y, pb.z);
+    f3 Pr = Pr0 - rcpf(Dr) * ur;
+    Pr = clampf(dotf(Pr, Pr), mrRs * Pn) * Pr;
+    o.Pb.x = Pr.x; o.Pb.y = Pr.y; o.Pb.z = Pr.z; o.Pb.w = 0.0f;
+    // increments from the stored (fp32) impulses, exact in fp64
+    const double dPn = (double)Pn - (double)Pn0;
+    const d3 dPtd = d3{(double)Pt.x - (double)Pt0.x, (double)Pt.y - (double)Pt0.y, (double)Pt.z - (double)Pt0.z};
+    o.nxdPt = cross(n_, dPtd);
+    o.dPr = d3{(double)Pr.x - (double)Pr0.x, (double)Pr.y - (double)Pr0.y, (double)Pr.z - (double)Pr0.z};
+    o.L = dPn * n_ + dPtd;
+    return o;
+}
+#else
 // Contact (a, b) in the canonical orientation.  VA..WB are body a's and body b's states
 // (.w = mass-splitting weights c/m, c/I); S = Sigma-hat, b = SPOOK bias (reading R4);
 // mrRs = mu_r R*.  Every kernel that evaluates a contact from both ends passes the same
@@ -69,6 +127,7 @@ __device__ __forceinline__ ContactOut contact_core(const double4 VA, const doubl
     o.L = dPn * n + dPt;
     return o;
 }
+#endif
 
 // One half-contact: contact (a, b) seen from self (isB: self is body b).
 __device__ __forceinline__ HalfOut half_core(const double4 VA, const double4 WA, const double4 VB, const double4 WB,

@@ -12,7 +12,7 @@
 #include "sweep_core.cuh"
 
 #ifndef SWEEPT2_MINB
-#define SWEEPT2_MINB 5
+#define SWEEPT2_MINB 6
 #endif
 constexpr int TT = 128;
 constexpr int NWT = TT / 32;
@@ -131,4 +131,183 @@ void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 
 {
     if (N) k_sweep_t2<<<(unsigned)((N + TT - 1) / TT), TT, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, geo, row,
                                                                    Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
+}
+
+// ==================================================================== layout experiment (t3)
+// The t2 kernel with (P8) the two impulse records of a contact interleaved in one 32-byte slot
+// (one 256-bit load and store instead of two 128-bit ones) and (VW) a particle's v and w
+// interleaved in one 64-byte record (both gathers hit one cache line).  Diagnostic only: the
+// bench converts the layouts before timing (dem_bench_sweeps variants 60-63).
+struct __align__(32) P8 { float4 a, b; };
+struct __align__(32) VW { double4 v, w; };
+
+__device__ __forceinline__ P8 ldP8(const P8 *p)
+{
+    P8 r;
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y), "=f"(r.b.z), "=f"(r.b.w)
+        : "l"(p));
+    return r;
+}
+__device__ __forceinline__ void stP8(P8 *p, const float4 a, const float4 b)
+{
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(a.z),
+                 "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
+                 : "memory");
+}
+
+template <bool USE_P8, bool USE_VW>
+__global__ void __launch_bounds__(TT, SWEEPT2_MINB)
+    k_sweep_t3(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win, double4 *__restrict__ vout,
+               double4 *__restrict__ wout, const VW *__restrict__ vwin, VW *__restrict__ vwout,
+               const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc, const G4 *__restrict__ geo,
+               const R4 *__restrict__ row, const P4 *__restrict__ Pa_in, const P4 *__restrict__ Pb_in,
+               P4 *__restrict__ Pa_out, P4 *__restrict__ Pb_out, const P8 *__restrict__ P8in, P8 *__restrict__ P8out,
+               const DevBoundary *__restrict__ bnd, SolveParams sp)
+{
+    __shared__ double2 sVa[TT], sVb[TT], sWa[TT], sWb[TT];
+    __shared__ double sAcc[NWT][6][32];
+    __shared__ uint8_t sOwn[NWT][32];
+    __shared__ uint32_t sI[TT + 1];
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t p0 = (int64_t)blockIdx.x * TT;
+    const int np = (int)min((int64_t)TT, N - p0);
+    if (t < np) {
+        double4 v, o;
+        if (USE_VW) { v = ld4g(&vwin[p0 + t].v); o = ld4g(&vwin[p0 + t].w); }
+        else { v = ld4g(&vin[p0 + t]); o = ld4g(&win[p0 + t]); }
+        sVa[t] = make_double2(v.x, v.y); sVb[t] = make_double2(v.z, v.w);
+        sWa[t] = make_double2(o.x, o.y); sWb[t] = make_double2(o.z, o.w);
+    }
+    for (int q = t; q <= np; q += TT) sI[q] = inc_start[p0 + q];
+#pragma unroll
+    for (int f = 0; f < 6; f++) sAcc[w][f][lane] = 0.0;
+    __syncthreads();
+    const int lo_p = 32 * w, hi_p = min(32 * w + 32, np);
+    const int me = lo_p + lane;
+    const uint32_t s_me = me < hi_p ? sI[me] : 0u, e_me = me < hi_p ? sI[me + 1] : 0u;
+    if (lo_p < np) {
+        const uint32_t k0 = sI[lo_p], k1 = sI[hi_p];
+        uint2 ent_next = make_uint2(0, 0);
+        if (k0 + lane < k1) ent_next = inc[k0 + lane];
+        int carry = 0;
+        for (uint32_t kb = k0; kb < k1; kb += 32) {
+            const uint32_t k = kb + lane;
+            const bool valid = k < k1;
+            const uint2 ent = ent_next;
+            if (kb + 32 + lane < k1) ent_next = inc[kb + 32 + lane];
+            const bool starts = e_me > s_me && s_me >= kb && s_me < kb + 32;
+            const unsigned smask = __reduce_or_sync(0xffffffffu, starts ? (1u << (s_me - kb)) : 0u);
+            if (starts) sOwn[w][s_me - kb] = (uint8_t)lane;
+            __syncwarp();
+            const unsigned le = smask & (0xffffffffu >> (31 - lane));
+            const int sstart = le ? 31 - __clz(le) : 0;
+            const int owner = le ? (int)sOwn[w][sstart] : carry;
+            double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
+            if (valid) {
+                const int o = lo_p + owner;
+                const uint32_t c = ent.x & ~B_SIDE;
+                const bool isB = (ent.x & B_SIDE) != 0;
+                const uint32_t p = ent.y;
+                const G4 g = ld4g(&geo[c]);
+                const R4 rw = ld4g(&row[c]);
+                P4 pa, pb;
+                if (USE_P8) { const P8 q = ldP8(&P8in[c]); pa = q.a; pb = q.b; }
+                else { pa = Pa_in[c]; pb = Pb_in[c]; }
+                double4 VP, WP;
+                double mt = sp.mu_t;
+                if (!(p & PARTNER_EXT)) {
+                    const int64_t pl = (int64_t)p - p0;
+                    if (pl >= 0 && pl < np) { VP = cat2(sVa[pl], sVb[pl]); WP = cat2(sWa[pl], sWb[pl]); }
+                    else if (USE_VW) { VP = ld4g(&vwin[p].v); WP = ld4g(&vwin[p].w); }
+                    else { VP = ld4g(&vin[p]); WP = ld4g(&win[p]); }
+                } else {
+                    d3 bv;
+                    double mr;
+                    boundary_body(p, bnd, bv, mt, mr);
+                    VP = make_double4(bv.x, bv.y, bv.z, 0.0);
+                    WP = make_double4(0.0, 0.0, 0.0, 0.0);
+                }
+                const double4 VS = cat2(sVa[o], sVb[o]), WS = cat2(sWa[o], sWb[o]);
+                const HalfOut r = half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt, g, rw,
+                                               pa, pb, sp.rolling_dims);
+                if (!isB) {
+                    if (USE_P8) stP8(&P8out[c], r.Pa, r.Pb);
+                    else { Pa_out[c] = r.Pa; Pb_out[c] = r.Pb; }
+                }
+                v0 = r.dL.x; v1 = r.dL.y; v2 = r.dL.z; v3 = r.dA.x; v4 = r.dA.y; v5 = r.dA.z;
+            }
+            const int dist = valid ? lane - sstart : 0;
+            const int maxd = __reduce_max_sync(0xffffffffu, dist);
+            for (int d = 1; d <= maxd; d <<= 1) {
+                const double u0 = __shfl_up_sync(0xffffffffu, v0, d), u1 = __shfl_up_sync(0xffffffffu, v1, d);
+                const double u2 = __shfl_up_sync(0xffffffffu, v2, d), u3 = __shfl_up_sync(0xffffffffu, v3, d);
+                const double u4 = __shfl_up_sync(0xffffffffu, v4, d), u5 = __shfl_up_sync(0xffffffffu, v5, d);
+                if (lane - d >= sstart) { v0 += u0; v1 += u1; v2 += u2; v3 += u3; v4 += u4; v5 += u5; }
+            }
+            const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1);
+            if (seg_end) {
+                sAcc[w][0][owner] += v0; sAcc[w][1][owner] += v1; sAcc[w][2][owner] += v2;
+                sAcc[w][3][owner] += v3; sAcc[w][4][owner] += v4; sAcc[w][5][owner] += v5;
+            }
+            carry = __shfl_sync(0xffffffffu, owner, 31);
+            __syncwarp();
+        }
+    }
+    if (me < hi_p) {
+        double4 V = cat2(sVa[me], sVb[me]), W = cat2(sWa[me], sWb[me]);
+        const uint32_t cnt = e_me - s_me;
+        if (cnt) {
+            const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
+            V.x += im * sAcc[w][0][lane]; V.y += im * sAcc[w][1][lane]; V.z += im * sAcc[w][2][lane];
+            W.x += iI * sAcc[w][3][lane]; W.y += iI * sAcc[w][4][lane]; W.z += iI * sAcc[w][5][lane];
+        }
+        if (USE_VW) { st4g(&vwout[p0 + me].v, V); st4g(&vwout[p0 + me].w, W); }
+        else { st4g(&vout[p0 + me], V); st4g(&wout[p0 + me], W); }
+    }
+}
+
+__global__ void k_pack_p8(int64_t nc, const P4 *__restrict__ a, const P4 *__restrict__ b, P8 *__restrict__ o)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < nc) { o[c].a = a[c]; o[c].b = b[c]; }
+}
+__global__ void k_pack_vw(int64_t n, const double4 *__restrict__ v, const double4 *__restrict__ w, VW *__restrict__ o,
+                          double4 *__restrict__ vback)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (vback) { vback[i] = o[i].v; return; }     // unpack direction: v of VW -> vback
+    o[i].v = v[i];
+    o[i].w = w[i];
+}
+
+// t3 experiment driver: n sweeps from (vin, win, Pa, Pb); the final v written back to vres
+void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin, const double4 *win, double4 *vbuf[2],
+                  double4 *wbuf[2], const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
+                  P4 *Pa[2], P4 *Pb[2], void *scratch, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s,
+                  double4 *vres, cudaEvent_t e0, cudaEvent_t e1)
+{
+    const bool p8 = variant & 1, vw = (variant >> 1) & 1;
+    P8 *q[2] = {(P8 *)scratch, (P8 *)scratch + nc};
+    VW *u[2] = {(VW *)(q[1] + nc), (VW *)(q[1] + nc) + N};
+    const unsigned gb = (unsigned)((N + TT - 1) / TT);
+    k_pack_p8<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(nc, Pa[0], Pb[0], q[0]);
+    k_pack_vw<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(N, vin, win, u[0], nullptr);
+    cudaEventRecord(e0, s);
+    const double4 *vi = vin, *wi = win;
+    for (int it = 0; it < n; it++) {
+        const int a = it & 1, b = a ^ 1;
+#define T3ARGS N, vi, wi, vbuf[a], wbuf[a], u[a], u[b], inc_start, inc, geo, row, Pa[a], Pb[a], Pa[b], Pb[b], q[a], q[b], bnd, sp
+        if (p8 && vw) k_sweep_t3<true, true><<<gb, TT, 0, s>>>(T3ARGS);
+        else if (p8) k_sweep_t3<true, false><<<gb, TT, 0, s>>>(T3ARGS);
+        else if (vw) k_sweep_t3<false, true><<<gb, TT, 0, s>>>(T3ARGS);
+        else k_sweep_t3<false, false><<<gb, TT, 0, s>>>(T3ARGS);
+#undef T3ARGS
+        vi = vbuf[a]; wi = wbuf[a];
+    }
+    cudaEventRecord(e1, s);
+    const int last = (n - 1) & 1;
+    if (vw) k_pack_vw<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(N, nullptr, nullptr, u[last ^ 1], vres);
+    else cudaMemcpyAsync(vres, vbuf[last], N * sizeof(double4), cudaMemcpyDeviceToDevice, s);
 }
