@@ -65,6 +65,14 @@ def make_slab(wl, rank, world):
     return synth.shift_slab(make_bed(wl, seed_offset=rank), rank, world)
 
 
+def device_generator(wl):
+    """The workload bed as an on-device generator (include/dem.h dem_generator, kind bands): the
+    same lattice recipe as synth.banded_bed (tests/test_boundary.py checks the site counts)."""
+    w = WORKLOADS[wl]
+    return dict(kind="bands", bands=[(b, r) for (_, b, r) in w["bands"]], spacing_factor=2.0, pos_jitter=0.01,
+                size_jitter=0.10, seed=w["seed"])
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -192,17 +200,19 @@ def main():
     wl = args.workload
     w = WORKLOADS[wl]
     n_it = args.n_it or dem.plan_iterations(network_length(w["bands"]), 0.02)
+    # the bed is generated on the device (dem_generator): N workload beds end to end along x for
+    # N ranks, rank r generating the sites of its slab [r L, (r+1) L) under global gids
+    L = w["dims"][0]
+    box = dict(lo=(0.0, 0.0, 0.0), hi=(world * L, w["dims"][1], w["dims"][2]))
+    gen = device_generator(wl)
     dcfg = None
     if world > 1 or args.decompose:
-        bed_in, slab = make_slab(wl, rank, world)
         obj = [dem.nccl_unique_id() if rank == 0 else None]
         if dist:
             dist.broadcast_object_list(obj, src=0)
-        dcfg = dict(rank=rank, world_size=world, slab=slab, transport="nccl", nccl_id=obj[0])
-    else:
-        bed_in = make_bed(wl)
-    bed = dem.Bed(bed_in.x, bed_in.r, bed_in.v, bed_in.w, bed_in.gid, device=local,
-                  solver=dict(dt=1e-4, n_iter=20), box=dict(lo=bed_in.box_lo, hi=bed_in.box_hi), dist=dcfg)
+        dcfg = dict(rank=rank, world_size=world, slab=(rank * L, (rank + 1) * L), transport="nccl", nccl_id=obj[0])
+    bed = dem.Bed(generator=gen, device=local, solver=dict(dt=1e-4, n_iter=20), box=box, dist=dcfg)
+    N_total = dem.generator_count(gen, box)
     if args.settle > 0:
         bed.step(args.settle)             # coarse relaxation of the jammed packing (not timed)
     bed.set_solver(dt=w["dt"], n_iter=n_it)
@@ -233,7 +243,7 @@ def main():
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    N = bed_in.n
+    N = N_total / world                 # particles per rank (value counts all of them)
     nc_mean = float(np.mean([r["n_contacts"] for r in reps]))
     imp_rate = float(np.mean([r["impact_fired"] for r in reps]))
     value = world * N * args.steps / (ms / 1e3)
@@ -256,7 +266,7 @@ def main():
         "metric": "particle-steps/s", "value": value, "unit": "particle-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl, "n_particles": N, "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
+        "config": {"workload": wl, "n_particles": int(N_total), "generator": "on-device (dem_generator)", "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "levels": len(w["bands"]),
                    "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)"
                    if (world > 1 or args.decompose) else "single GPU",
@@ -301,7 +311,7 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             T = float(t.item())
         out["e2e"] = {"value": world * N * args.steps / T, "unit": "particle-steps/s",
-                      "h2d_bytes_per_step": 4 * 5336, "d2h_bytes_per_step": 72 * N,
+                      "h2d_bytes_per_step": 4 * 5336, "d2h_bytes_per_step": int(72 * N),
                       "what": "per step: wall-drive inputs H2D, full particle state (pos, vel, angvel) D2H to pinned host"}
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         out["cpu_baseline"] = cpu_baseline(wl, n_it, w["dt"])

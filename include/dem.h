@@ -93,12 +93,44 @@ typedef struct {
     int32_t pad0;
 } dem_particles;
 
+/* On-device bed generator (refinement profiles P:65-78, Eq. 1 and Fig. 2; size
+ * jitter P:161).  The bed fills the box from the bottom face up to the top face; depth is
+ * measured down from box.hi[2].
+ *   kind 0 bands: band k spans depths [band_bottom_depth[k-1], band_bottom_depth[k]) (band 0
+ *          from depth 0) with nominal radius band_r_nom[k]; an FCC lattice per band with
+ *          nearest-neighbour distance spacing_factor * r_nom, kept 1.1 r_nom from the band faces
+ *          and the walls.
+ *   kind 1 linear profile (Eq. 1): d(depth) = d_min + gamma depth, capped at d_max; square
+ *          lattice planes from the bottom up, in-plane spacing spacing_factor * r(z), vertical gap
+ *          spacing_factor (r_k + r_k+1) / 2.
+ *   kind 2 layer schedule (Fig. 2): layers n = 0, 1, ... from the top with d_n = d_min ratio_r^n
+ *          and thickness eta d_n while d_n < d_max, d_max below; generated as kind 0 bands.
+ * Jitter: each coordinate += pos_jitter r_nom U(-1, 1), radius = r_nom U(1 - size_jitter,
+ * 1 + size_jitter), from Philox4x32-10 keyed by seed with counter gid.  gids run plane by plane
+ * from the bottom (then lattice sub-grid, y, x).  With world_size > 1 every rank generates the
+ * sites of its slab (by lattice x; the outer slabs are open) under their global gids, so the
+ * union over ranks is the single-rank bed.  Velocities start at zero. */
+typedef struct {
+    int32_t kind;                      /* 0 bands, 1 linear profile, 2 layer schedule */
+    int32_t n_bands;                   /* kind 0: number of bands (<= 64) */
+    const double *band_bottom_depth;   /* kind 0: n_bands increasing depths [m] (host memory) */
+    const double *band_r_nom;          /* kind 0: n_bands nominal radii [m] (host memory) */
+    double d_min, gamma, d_max;        /* kinds 1, 2: diameters [m], gamma = dd/ddepth */
+    double ratio_r, eta;               /* kind 2: size ratio between layers > 1, layer thickness / d */
+    double spacing_factor;             /* lattice distance / r_nom; 2.25 leaves every pair apart */
+    double pos_jitter, size_jitter;    /* 0.01 and 0.10 */
+    uint64_t seed;
+} dem_generator;
+
 typedef struct {
     size_t struct_size;        /* sizeof(dem_bed_desc): ABI version check */
     dem_material mat;
     dem_solver solver;
     dem_box box;
-    dem_particles parts;
+    dem_particles parts;       /* source 0 */
+    int32_t source;            /* 0: the particle arrays, 1: the generator */
+    int32_t pad0;
+    dem_generator gen;         /* source 1 */
 } dem_bed_desc;
 
 /* Process / device plumbing (PyTorch provides memory, stream and process group) and the x-slab
@@ -261,6 +293,11 @@ dem_status dem_destroy(dem_ctx *ctx);
 
 /* Last error message of ctx (ctx == NULL: of the last failed create on this thread). */
 const char *dem_last_error(const dem_ctx *ctx);
+
+/* Host-only: number of particles the generator places in [slab_lo, slab_hi) of the lattice x
+ * (pass -INFINITY, INFINITY for the whole bed).  DEM_ERR_INVALID for bad parameters. */
+dem_status dem_generator_count(const dem_generator *gen, const dem_box *box, double slab_lo, double slab_hi,
+                               int64_t *n);
 
 /* ---- host-only planner helpers, pure functions ---- */
 /* Eq. 1: d(z) = d_min + gamma z for z < z_max = (d_max - d_min)/gamma, else d_max. */

@@ -143,6 +143,12 @@ static dem_status dalloc(dem_ctx *ctx, void **p, size_t bytes)
     *p = q;
     return DEM_OK;
 }
+static void dfree(dem_ctx *ctx, void *p);
+static void *ctx_alloc(size_t bytes, void *c)
+{
+    void *p = nullptr;
+    return dalloc((dem_ctx *)c, &p, bytes) == DEM_OK ? p : nullptr;
+}
 static void dfree(dem_ctx *ctx, void *p)
 {
     if (!p) return;
@@ -868,7 +874,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
 
 // ------------------------------------------------------------------ state loading
 static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, const double *rad, const double *vel,
-                                 const double *ang, const uint32_t *gid, int on_device, bool first)
+                                 const double *ang, const uint32_t *gid, int on_device, bool first, bool check_slab = true)
 {
     // validate on the host
     std::vector<double> r(n), x(3 * n);
@@ -884,7 +890,7 @@ static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, con
         if (!(r[i] > 0) || !std::isfinite(r[i])) { ctx->err = "radius must be positive and finite"; return DEM_ERR_INVALID; }
         for (int k = 0; k < 3; k++) if (!std::isfinite(x[3 * i + k])) { ctx->err = "non-finite position"; return DEM_ERR_INVALID; }
         if (g[i] >= PLATE_KEY_BASE) { ctx->err = "gid must be < 2^32-4096"; return DEM_ERR_INVALID; }
-        if (ctx->tp && !((ctx->rank == 0 || x[3 * i] >= ctx->slab_lo) && (ctx->rank == ctx->G - 1 || x[3 * i] < ctx->slab_hi))) {
+        if (check_slab && ctx->tp && !((ctx->rank == 0 || x[3 * i] >= ctx->slab_lo) && (ctx->rank == ctx->G - 1 || x[3 * i] < ctx->slab_hi))) {
             ctx->err = "particle outside this rank's slab [slab_lo, slab_hi)";
             return DEM_ERR_INVALID;
         }
@@ -943,7 +949,8 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
     }
     for (int k = 0; k < 3; k++)
         if (!(desc->box.lo[k] < desc->box.hi[k])) { g_create_err = "box lo must be < hi"; return DEM_ERR_INVALID; }
-    if (desc->parts.n < 0 || (desc->parts.n > 0 && (!desc->parts.pos || !desc->parts.radius))) {
+    if (desc->source != 0 && desc->source != 1) { g_create_err = "source must be 0 (particles) or 1 (generator)"; return DEM_ERR_INVALID; }
+    if (desc->source == 0 && (desc->parts.n < 0 || (desc->parts.n > 0 && (!desc->parts.pos || !desc->parts.radius)))) {
         g_create_err = "particle arrays missing";
         return DEM_ERR_INVALID;
     }
@@ -996,7 +1003,26 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
         return DEM_ERR_CUDA;
     }
     const dem_particles &p = desc->parts;
-    dem_status st = load_particles(ctx, p.n, p.pos, p.radius, p.vel, p.angvel, p.gid, p.on_device, true);
+    dem_status st;
+    if (desc->source == 1) {
+        // on-device generator: this rank's sites (outer slabs open), then the standard load
+        const double lo = (!ctx->tp || ctx->rank == 0) ? -INFINITY : ctx->slab_lo;
+        const double hi = (!ctx->tp || ctx->rank == ctx->G - 1) ? INFINITY : ctx->slab_hi;
+        double *gx = nullptr, *gr = nullptr;
+        uint32_t *gg = nullptr;
+        int64_t gn = 0;
+        std::string gerr;
+        if (!generate_bed(desc->gen, desc->box, lo, hi, ctx_alloc, ctx, ctx->s, &gx, &gr, &gg, &gn, gerr)) {
+            ctx->err = gerr;
+            st = DEM_ERR_INVALID;
+        } else {
+            // jittered sites may sit a hair outside the slab: the first rebuild assigns them
+            st = load_particles(ctx, gn, gx, gr, nullptr, nullptr, gg, 1, true, false);
+        }
+        for (void *q : {(void *)gx, (void *)gr, (void *)gg}) dfree(ctx, q);
+    } else {
+        st = load_particles(ctx, p.n, p.pos, p.radius, p.vel, p.angvel, p.gid, p.on_device, true);
+    }
     if (st == DEM_OK) st = upload_boundary(ctx);
     if (st == DEM_OK) st = rebuild(ctx);
     if (st != DEM_OK) {

@@ -1,5 +1,8 @@
 // kernels.h -- host launchers of the device kernels (detect.cu, solve.cu); internal to libdem.so.
 #pragma once
+#include <string>
+
+#include "../../include/dem.h"
 #include "common.cuh"
 
 // detect.cu
@@ -108,3 +111,7 @@ void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin,
                   double4 *wbuf[2], const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
                   P4 *Pa[2], P4 *Pb[2], void *scratch, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s,
                   double4 *vres, cudaEvent_t e0, cudaEvent_t e1);
+// generate.cu: on-device bed generator (include/dem.h dem_generator)
+bool generate_bed(const dem_generator &g, const dem_box &box, double slab_lo, double slab_hi,
+                  void *(*alloc)(size_t, void *), void *actx, cudaStream_t s, double **x, double **r, uint32_t **gid,
+                  int64_t *n, std::string &err);

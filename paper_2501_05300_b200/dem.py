@@ -52,9 +52,16 @@ class Particles(C.Structure):
                 ("angvel", C.c_void_p), ("gid", C.c_void_p), ("on_device", C.c_int32), ("pad0", C.c_int32)]
 
 
+class Generator(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("n_bands", C.c_int32), ("band_bottom_depth", C.c_void_p),
+                ("band_r_nom", C.c_void_p), ("d_min", C.c_double), ("gamma", C.c_double), ("d_max", C.c_double),
+                ("ratio_r", C.c_double), ("eta", C.c_double), ("spacing_factor", C.c_double),
+                ("pos_jitter", C.c_double), ("size_jitter", C.c_double), ("seed", C.c_uint64)]
+
+
 class BedDesc(C.Structure):
     _fields_ = [("struct_size", C.c_size_t), ("mat", Material), ("solver", Solver), ("box", Box),
-                ("parts", Particles)]
+                ("parts", Particles), ("source", C.c_int32), ("pad0", C.c_int32), ("gen", Generator)]
 
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
@@ -113,7 +120,7 @@ CONTACT_DTYPE = np.dtype([("key", "<u8"), ("n", "<f8", (3,)), ("delta", "<f8"), 
 EXPORTS = ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts", "dem_get_forces",
            "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_set_timing", "dem_get_timing",
            "dem_reset_timing", "dem_bench_sweeps", "dem_num_particles", "dem_num_local", "dem_nccl_unique_id",
-           "dem_loopback_create", "dem_loopback_destroy", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
+           "dem_loopback_create", "dem_loopback_destroy", "dem_generator_count", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
            "dem_contact_network_length", "dem_plan_iterations", "dem_plan_timestep"]
 
 _lib = None
@@ -152,6 +159,8 @@ def lib():
         L.dem_loopback_create.restype = vp
         L.dem_loopback_destroy.argtypes = [vp]
         L.dem_loopback_destroy.restype = None
+        L.dem_generator_count.argtypes = [C.POINTER(Generator), C.POINTER(Box), d, d, C.POINTER(C.c_int64)]
+        L.dem_generator_count.restype = C.c_int
         L.dem_stream.argtypes = [vp]
         L.dem_stream.restype = vp
         L.dem_destroy.argtypes = [vp]
@@ -221,6 +230,45 @@ def slab_bounds(x, world_size, lo, hi):
     return [lo] + [float(v) for v in q] + [hi]
 
 
+# ---------------------------------------------------------------- on-device generator (include/dem.h)
+def make_generator(kind="bands", bands=(), d_min=0.0, gamma=0.0, d_max=0.0, ratio_r=0.0, eta=0.0,
+                   spacing_factor=2.25, pos_jitter=0.01, size_jitter=0.10, seed=0):
+    """dem_generator: kind 'bands' with bands = [(depth_bottom, r_nom), ...] (top band first),
+    'profile' (Eq. 1: d_min, gamma, d_max) or 'layers' (Fig. 2: d_min, d_max, ratio_r, eta).
+    Returns (Generator, keep-alive arrays)."""
+    g = Generator()
+    g.kind = {"bands": 0, "profile": 1, "layers": 2}[kind]
+    keep = ()
+    if g.kind == 0:
+        bd = np.ascontiguousarray([b[0] for b in bands], dtype=np.float64)
+        br = np.ascontiguousarray([b[1] for b in bands], dtype=np.float64)
+        g.n_bands, g.band_bottom_depth, g.band_r_nom = len(bd), bd.ctypes.data, br.ctypes.data
+        keep = (bd, br)
+    g.d_min, g.gamma, g.d_max, g.ratio_r, g.eta = d_min, gamma, d_max, ratio_r, eta
+    g.spacing_factor, g.pos_jitter, g.size_jitter, g.seed = spacing_factor, pos_jitter, size_jitter, seed
+    return g, keep
+
+
+def _box(box):
+    bx = dict(lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), wall_mask=0x3F, wall_mu_t=0.0, wall_mu_r=0.0)
+    bx.update(box or {})
+    b = Box()
+    for j in range(3):
+        b.lo[j], b.hi[j] = bx["lo"][j], bx["hi"][j]
+    b.wall_mask, b.wall_mu_t, b.wall_mu_r = bx["wall_mask"], bx["wall_mu_t"], bx["wall_mu_r"]
+    return b
+
+
+def generator_count(gen, box, slab=(-np.inf, np.inf)):
+    """Particles the generator places with lattice x in slab (host-only, no GPU)."""
+    g, keep = make_generator(**gen)
+    n = C.c_int64()
+    st = lib().dem_generator_count(C.byref(g), C.byref(_box(box)), float(slab[0]), float(slab[1]), C.byref(n))
+    if st != DEM_OK:
+        raise DemError(st, "invalid generator")
+    return n.value
+
+
 # ---------------------------------------------------------------- bed
 def _ptr(a):
     return None if a is None else a.ctypes.data
@@ -236,8 +284,8 @@ def _f64(a, shape=None):
 class Bed:
     """One DEM context (one GPU).  Host arrays in, host arrays out, gid order."""
 
-    def __init__(self, pos, radius, vel=None, angvel=None, gid=None, *, material=None, solver=None, box=None,
-                 stream=None, torch_allocator=True, device=0, dist=None):
+    def __init__(self, pos=None, radius=None, vel=None, angvel=None, gid=None, *, material=None, solver=None, box=None,
+                 stream=None, torch_allocator=True, device=0, dist=None, generator=None):
         """dist (x-slab decomposition, include/dem.h): dict(rank, world_size, slab=(lo, hi),
         transport='nccl' with nccl_id=<128 bytes of rank 0> | 'loopback' with group=LoopbackGroup);
         pos... are then this rank's particles (inside its slab)."""
@@ -267,6 +315,10 @@ class Bed:
         for j in range(3):
             desc.box.lo[j], desc.box.hi[j] = bx["lo"][j], bx["hi"][j]
         desc.box.wall_mask, desc.box.wall_mu_t, desc.box.wall_mu_r = bx["wall_mask"], bx["wall_mu_t"], bx["wall_mu_r"]
+        if generator is not None:       # on-device generator (dem_generator): no particle arrays
+            desc.source = 1
+            desc.gen, self._gen_keep = make_generator(**generator)
+            pos, radius = np.zeros((0, 3)), np.zeros(0)
         pos = _f64(pos, (-1, 3))
         radius = _f64(radius)
         n = len(radius)
@@ -311,6 +363,8 @@ class Bed:
             raise DemError(st, lib().dem_last_error(None).decode())
         self._h = h
         self.last_report = None
+        if generator is not None:
+            self.n = self.n_owned
 
     # -- lifecycle
     def close(self):
