@@ -44,7 +44,7 @@ class Params(C.Structure):
         ("h", C.c_double), ("n_it", C.c_int32), ("n_imp", C.c_int32),
         ("e_H", C.c_double), ("k_lin", C.c_double), ("damp_steps", C.c_double),
         ("v_imp", C.c_double), ("g", C.c_double * 3),
-        ("rolling_dims", C.c_int32), ("pad", C.c_int32),
+        ("rolling_dims", C.c_int32), ("ordering", C.c_int32),
     ]
 
 
@@ -124,11 +124,31 @@ def lib():
         L.or_step.argtypes = [C.POINTER(World), C.POINTER(Params), C.c_void_p, i64, C.c_void_p, i64,
                               C.POINTER(i64), pd, pd, C.POINTER(Report)]
         L.or_step.restype = i32
+        L.or_color_contacts.argtypes = [i64, C.c_void_p, C.c_void_p, C.c_void_p, i64, C.c_void_p]
+        L.or_color_contacts.restype = i32
+        L.or_splitmix64.argtypes = [C.c_uint64]
+        L.or_splitmix64.restype = C.c_uint64
         _lib = L
     return _lib
 
 
 # ----------------------------------------------------------------------------- pure helpers
+
+def color_contacts(key, a, b, n_particles):
+    """Greedy colouring of the contact conflict graph in decreasing splitmix64(key) priority
+    (or_color_contacts).  Returns (colours array, number of colours)."""
+    key = np.ascontiguousarray(key, dtype=np.uint64)
+    a = np.ascontiguousarray(a, dtype=np.int64)
+    b = np.ascontiguousarray(b, dtype=np.int64)
+    col = np.empty(len(key), dtype=np.int32)
+    n = lib().or_color_contacts(len(key), key.ctypes.data, a.ctypes.data, b.ctypes.data, int(n_particles),
+                                col.ctypes.data)
+    return col, n
+
+
+def splitmix64(x):
+    return int(lib().or_splitmix64(int(x)))
+
 
 def mass_inertia(d: float, rho: float):
     m, I = C.c_double(), C.c_double()
@@ -181,6 +201,7 @@ def make_params(**kw) -> Params:
     for k in range(3):
         p.g[k] = g[k]
     p.rolling_dims = kw.get("rolling_dims", 3)
+    p.ordering = kw.get("ordering", 0)          # 0 Jacobi (R2), 1 coloured Gauss-Seidel (NEXT-1)
     return p
 
 
@@ -292,6 +313,8 @@ class OracleWorld:
                 T.ctypes.data_as(dp) if T is not None else None, C.byref(rep))
             if rc == -1:
                 raise RuntimeError("or_step: contact capacity exceeded")
+            if rc == -3:
+                raise RuntimeError("or_step: the Gauss-Seidel colouring needs more than 256 colours")
             self.time = W.time
             out = out[: n.value].copy()
             self.hist = out

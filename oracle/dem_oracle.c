@@ -434,6 +434,149 @@ static void sweep(const or_world *w, const or_params *p, row *R, int64_t nc,
     }
 }
 
+/* ---------------------------------------------------------------- coloured Gauss-Seidel (NEXT-1)
+ * The paper solves the MCP with projected Gauss-Seidel: contacts one after the other,
+ * each from the latest velocities, its impulse increment applied at once with the real masses.
+ * The order used here: by colour of a greedy colouring of the contact conflict graph (two
+ * contacts conflict if they share a particle), then by key.  Contacts of one colour touch
+ * disjoint particles, so within a colour the order does not matter. */
+uint64_t or_splitmix64(uint64_t x)
+{
+    x += 0x9E3779B97F4A7C15ULL;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+    return x ^ (x >> 31);
+}
+
+static const uint64_t *g_pri_key;      /* qsort context (single-threaded oracle) */
+static const uint64_t *g_pri;
+static int cmp_priority(const void *x, const void *y)
+{
+    const int64_t i = *(const int64_t *)x, j = *(const int64_t *)y;
+    if (g_pri[i] != g_pri[j]) return g_pri[i] > g_pri[j] ? -1 : 1;       /* decreasing priority */
+    return g_pri_key[i] < g_pri_key[j] ? -1 : (g_pri_key[i] > g_pri_key[j] ? 1 : 0);
+}
+
+int32_t or_color_contacts(int64_t nc, const uint64_t *key, const int64_t *a, const int64_t *b, int64_t n_particles,
+                          int32_t *color)
+{
+    uint64_t *pri = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(nc ? nc : 1));
+    int64_t *ord = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc ? nc : 1));
+    uint64_t *used = (uint64_t *)calloc((size_t)(n_particles ? n_particles : 1) * 4, sizeof(uint64_t));
+    int32_t ncol = 0;
+    for (int64_t c = 0; c < nc; c++) { pri[c] = or_splitmix64(key[c]); ord[c] = c; color[c] = -1; }
+    g_pri = pri;
+    g_pri_key = key;
+    qsort(ord, (size_t)nc, sizeof(int64_t), cmp_priority);
+    for (int64_t t = 0; t < nc; t++) {
+        const int64_t c = ord[t];
+        int32_t col = -1;
+        for (int q = 0; q < 256 && col < 0; q++) {
+            const uint64_t bit = 1ULL << (q & 63);
+            const int wa = (used[4 * a[c] + (q >> 6)] & bit) != 0;
+            const int wb = b[c] >= 0 ? (used[4 * b[c] + (q >> 6)] & bit) != 0 : 0;
+            if (!wa && !wb) col = q;
+        }
+        if (col < 0) { ncol = -1; break; }
+        color[c] = col;
+        used[4 * a[c] + (col >> 6)] |= 1ULL << (col & 63);
+        if (b[c] >= 0) used[4 * b[c] + (col >> 6)] |= 1ULL << (col & 63);
+        if (col + 1 > ncol) ncol = col + 1;
+    }
+    free(pri); free(ord); free(used);
+    return ncol;
+}
+
+/* One projected Gauss-Seidel sweep in the given contact order: the same contact-local update as
+ * the Jacobi sweep (normal -> friction -> rolling) with the real inverse masses, its increments
+ * applied to the bodies immediately. */
+static void sweep_gs(const or_world *w, const or_params *p, row *R, int64_t nc, const int64_t *order,
+                     const double *minv, const double *Iinv, double *v, double *om)
+{
+    for (int64_t t = 0; t < nc; t++) {
+        row *r = &R[order[t]];
+        const int64_t a = r->g.a;
+        const double *n = r->g.n;
+        double va[3], wa_[3], vb[3], wb_[3];
+        for (int k = 0; k < 3; k++) { va[k] = v[3 * a + k]; wa_[k] = om[3 * a + k]; }
+        body_b_vel(w, r, v, om, vb, wb_);
+        const double wA = minv[a], wtA = Iinv[a];
+        double wB = 0.0, wtB = 0.0;
+        if (r->g.kind == 0) { wB = minv[r->g.b]; wtB = Iinv[r->g.b]; }
+        const double Dn = wA + wB;
+        const double Dt = wA + wB + dot3(r->la, r->la) * wtA + dot3(r->lb, r->lb) * wtB;
+        const double Dr = wtA + wtB;
+        double dv[3];
+        for (int k = 0; k < 3; k++) dv[k] = vb[k] - va[k];
+        const double Pn0 = r->P[0];
+        double Pn = Pn0 - (dot3(n, dv) + r->S * Pn0 - r->bias) / (Dn + r->S);
+        if (Pn < 0.0) Pn = 0.0;
+        const double dPn = Pn - Pn0;
+        for (int k = 0; k < 3; k++) { va[k] -= wA * dPn * n[k]; vb[k] += wB * dPn * n[k]; }
+        double ca[3], cb[3], u[3], ut[3];
+        cross3(wa_, r->la, ca);
+        cross3(wb_, r->lb, cb);
+        for (int k = 0; k < 3; k++) u[k] = (vb[k] + cb[k]) - (va[k] + ca[k]);
+        const double uu = dot3(u, n);
+        for (int k = 0; k < 3; k++) ut[k] = u[k] - uu * n[k];
+        double Pt[3];
+        for (int k = 0; k < 3; k++) Pt[k] = r->P[1 + k] - ut[k] / Dt;
+        double lim = r->mu_t * Pn, mag = norm3(Pt);
+        if (mag > lim) { double s = mag > 0.0 ? lim / mag : 0.0; for (int k = 0; k < 3; k++) Pt[k] *= s; }
+        double dPt[3], ta[3], tb[3];
+        for (int k = 0; k < 3; k++) dPt[k] = Pt[k] - r->P[1 + k];
+        cross3(r->la, dPt, ta);
+        cross3(r->lb, dPt, tb);
+        for (int k = 0; k < 3; k++) {
+            va[k] -= wA * dPt[k];
+            wa_[k] -= wtA * ta[k];
+            vb[k] += wB * dPt[k];
+            wb_[k] += wtB * tb[k];
+        }
+        double ur[3];
+        for (int k = 0; k < 3; k++) ur[k] = wb_[k] - wa_[k];
+        if (p->rolling_dims == 2) { double q = dot3(ur, n); for (int k = 0; k < 3; k++) ur[k] -= q * n[k]; }
+        double Pr[3];
+        for (int k = 0; k < 3; k++) Pr[k] = r->P[4 + k] - ur[k] / Dr;
+        lim = r->mu_r * r->Rs * Pn;
+        mag = norm3(Pr);
+        if (mag > lim) { double s = mag > 0.0 ? lim / mag : 0.0; for (int k = 0; k < 3; k++) Pr[k] *= s; }
+        double dPr[3];
+        for (int k = 0; k < 3; k++) dPr[k] = Pr[k] - r->P[4 + k];
+        /* Gauss-Seidel: the increments go to the bodies now */
+        for (int k = 0; k < 3; k++) {
+            v[3 * a + k] -= minv[a] * (dPn * n[k] + dPt[k]);
+            om[3 * a + k] -= Iinv[a] * (ta[k] + dPr[k]);
+        }
+        if (r->g.kind == 0) {
+            const int64_t b = r->g.b;
+            for (int k = 0; k < 3; k++) {
+                v[3 * b + k] += minv[b] * (dPn * n[k] + dPt[k]);
+                om[3 * b + k] += Iinv[b] * (tb[k] + dPr[k]);
+            }
+        }
+        r->P[0] = Pn;
+        for (int k = 0; k < 3; k++) { r->P[1 + k] = Pt[k]; r->P[4 + k] = Pr[k]; }
+    }
+}
+
+/* contact order of the Gauss-Seidel sweeps: by colour, then by key (rows are in key order) */
+static int32_t gs_order(const row *R, int64_t nc, int64_t N, int64_t *order)
+{
+    uint64_t *key = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(nc ? nc : 1));
+    int64_t *a = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc ? nc : 1));
+    int64_t *b = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc ? nc : 1));
+    int32_t *col = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nc ? nc : 1));
+    for (int64_t c = 0; c < nc; c++) { key[c] = R[c].g.key; a[c] = R[c].g.a; b[c] = R[c].g.kind == 0 ? R[c].g.b : -1; }
+    const int32_t ncol = or_color_contacts(nc, key, a, b, N, col);
+    int64_t t = 0;
+    for (int32_t q = 0; q < ncol; q++)
+        for (int64_t c = 0; c < nc; c++)
+            if (col[c] == q) order[t++] = c;
+    free(key); free(a); free(b); free(col);
+    return ncol;
+}
+
 /* apply impulses P of every row to the bodies with real masses (warm start) */
 static void apply_impulses(const or_world *w, row *R, int64_t nc, const double *minv,
                            const double *Iinv, double *v, double *om)
@@ -539,6 +682,15 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
     }
     rep->n_contacts = nc;
     rep->n_degenerate = n_degen;
+    const int gs = p->ordering == 1;
+    int64_t *order = NULL;
+    if (gs) {
+        order = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc ? nc : 1));
+        if (gs_order(R, nc, N, order) < 0) {                    /* more than 256 colours */
+            free(L.v); free(minv); free(Iinv); free(cnt); free(accL); free(accA); free(R); free(order);
+            return -3;
+        }
+    }
 
     /* 3. impact trigger: u_n^- = n.(v_b^k - v_a^k) < -v_imp */
     int fired = 0;
@@ -561,7 +713,10 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
             r->S = 0.0;
             r->bias = r->impacting ? -p->e_rest * r->un_minus : 0.0;
         }
-        for (int32_t s = 0; s < n_imp; s++) sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA);
+        for (int32_t s = 0; s < n_imp; s++) {
+            if (gs) sweep_gs(w, p, R, nc, order, minv, Iinv, w->v, w->w);
+            else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA);
+        }
     }
 
     /* 4. main-stage rows (SPOOK; reading R4):
@@ -599,8 +754,11 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
         for (int k = 0; k < 3; k++) w->v[3 * i + k] += h * p->g[k];
     apply_impulses(w, R, nc, minv, Iinv, w->v, w->w);
 
-    /* 7. N_it Jacobi sweeps */
-    for (int32_t s = 0; s < p->n_it; s++) sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA);
+    /* 7. N_it sweeps: Jacobi, or coloured Gauss-Seidel */
+    for (int32_t s = 0; s < p->n_it; s++) {
+        if (gs) sweep_gs(w, p, R, nc, order, minv, Iinv, w->v, w->w);
+        else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA);
+    }
 
     /* 8. outputs: forces/torques (P/h sums), plate reactions, residuals (O6, O9) */
     if (F) memset(F, 0, sizeof(double) * 3 * (size_t)N);
@@ -681,6 +839,6 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
         for (int k = 0; k < 7; k++) if (!isfinite(R[c].P[k])) bad = 1;
     }
     if (bad) rc = -2;
-    free(L.v); free(minv); free(Iinv); free(cnt); free(accL); free(accA); free(R); free(H);
+    free(L.v); free(minv); free(Iinv); free(cnt); free(accL); free(accA); free(R); free(H); free(order);
     return rc;
 }

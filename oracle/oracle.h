@@ -34,7 +34,8 @@ typedef struct {
     double v_imp;             /* impact threshold; <0 -> 20|g|h; >=1e30 disables */
     double g[3];              /* gravity */
     int32_t rolling_dims;     /* 3 (default) or 2 (rolling row projected on tangent plane) */
-    int32_t pad;
+    int32_t ordering;         /* 0: Jacobi with mass splitting (reading R2); 1: coloured projected
+                                 Gauss-Seidel (P:134 PGS), see or_color_contacts */
 } or_params;
 
 /* Static or kinematic plane wall: contact iff (X-p).n < r (reading R17). */
@@ -113,6 +114,15 @@ int32_t or_detect(const or_world *w, const or_params *p, or_contact *out, int64_
  * deduplicated and sorted by key: sampled pair-set checks on full-size beds */
 int32_t or_contacts_of(const or_world *w, const int64_t *idx, int64_t nidx, or_contact *out, int64_t cap,
                        int64_t *n_out);
+
+/* Colouring of the contact graph for the Gauss-Seidel ordering: contacts that
+ * share a particle conflict.  Priority pi(c) = splitmix64(key(c)) (ties: smaller key first);
+ * contacts are coloured greedily in decreasing priority, each with the smallest colour not used
+ * by an already-coloured conflicting contact.  a[c], b[c]: particle indices (b < 0: wall or
+ * plate).  color[c] out; returns the number of colours, or -1 if more than 256 are needed. */
+int32_t or_color_contacts(int64_t nc, const uint64_t *key, const int64_t *a, const int64_t *b, int64_t n_particles,
+                          int32_t *color);
+uint64_t or_splitmix64(uint64_t x);
 
 /* one full time step: detection, impact stage, SPOOK rows, warm start,
  * n_it Jacobi sweeps, integration, plates/walls.  hist (any order) supplies the warm start.

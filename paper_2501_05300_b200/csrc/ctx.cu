@@ -1394,6 +1394,9 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
             } else if (var == 30) {
                 launch_sweep8(N, maxb, vi, wi, vo, wo, ca6, bs6, xs6, xl8, ctx->cij, bsl6, ctx->geo, ctx->row, pai, pbi, pao,
                               pbo, ctx->db, ctx->sp, s);
+            } else if (var == 22) {
+                launch_sweep7(N, maxb, vi, wi, vo, wo, ca6, bs6, xs6, xl6, ctx->cij, bsl6, ctx->geo, ctx->row, pai, pbi, pao,
+                              pbo, ctx->db, ctx->sp, s);
             } else if (var >= 20) {
                 launch_sweep6(tile6, false, N, maxb, ctx->pos_prev, vi, wi, vo, wo, ca6, bs6, xs6, xl6, ctx->cij, bsl6, cb,
                               pai, pbi, pao, pbo, ctx->db, ctx->sp, s);

@@ -115,3 +115,7 @@ void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin,
 bool generate_bed(const dem_generator &g, const dem_box &box, double slab_lo, double slab_hi,
                   void *(*alloc)(size_t, void *), void *actx, cudaStream_t s, double **x, double **r, uint32_t **gid,
                   int64_t *n, std::string &err);
+void launch_sweep7(int64_t N, unsigned max_b, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
+                   const uint32_t *ca, const uint32_t *bstart, const uint32_t *xstart, const uint2 *xlist,
+                   const uint2 *cij, const uint32_t *bslot, const G4 *geo, const R4 *row, const P4 *Pa_in,
+                   const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);

@@ -259,6 +259,177 @@ __global__ void __launch_bounds__(TILE, TILE == 256 ? 2 : SWEEP6_MINB)
     }
 }
 
+
+#ifndef SWEEP7_MINB
+#define SWEEP7_MINB 4
+#endif
+template <int TILE>
+__global__ void __launch_bounds__(TILE, SWEEP7_MINB)
+    k_sweep7(int64_t N, int cap, const double4 *__restrict__ pos, const double4 *__restrict__ vin,
+             const double4 *__restrict__ win, double4 *__restrict__ vout, double4 *__restrict__ wout,
+             const uint32_t *__restrict__ ca, const uint32_t *__restrict__ bstart, const uint32_t *__restrict__ xstart,
+             const uint2 *__restrict__ xlist, const uint2 *__restrict__ cij, const uint32_t *__restrict__ bslot,
+             const G4 *__restrict__ geo, const R4 *__restrict__ row, const P4 *__restrict__ Pa_in, const P4 *__restrict__ Pb_in,
+             P4 *__restrict__ Pa_out, P4 *__restrict__ Pb_out, const DevBoundary *__restrict__ bnd, SolveParams sp)
+{
+    extern __shared__ __align__(16) unsigned char smraw[];
+    Smem6<TILE> &sm = *reinterpret_cast<Smem6<TILE> *>(smraw);
+    double *slot = reinterpret_cast<double *>(smraw + sizeof(Smem6<TILE>));   // [6][cap]
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    const int64_t p0 = (int64_t)blockIdx.x * TILE;
+    const int np = (int)min((int64_t)TILE, N - p0);
+    if (t < np) {
+        sm.sV[t] = ld4g(&vin[p0 + t]);
+        sm.sW[t] = ld4g(&win[p0 + t]);
+    }
+    for (int q = t; q <= np; q += TILE) {
+        sm.sCa[q] = ca[p0 + q];
+        sm.sXs[q] = xstart[p0 + q];
+        sm.sBs[q] = bstart[p0 + q];
+    }
+#pragma unroll
+    for (int f = 0; f < 6; f++) sm.sAcc[w][f][lane] = 0.0;
+    __syncthreads();
+    const uint32_t base = sm.sBs[0];
+    const int lo_p = 32 * w, hi_p = min(32 * w + 32, np);
+    const int me = lo_p + lane;
+    const bool mine = me < hi_p;
+    if (lo_p < np) {
+        const uint32_t a0 = sm.sCa[lo_p], a1 = sm.sCa[hi_p], x0 = sm.sXs[lo_p], x1 = sm.sXs[hi_p];
+        const uint32_t nA = a1 - a0, nT = nA + (x1 - x0);
+        // this lane's particle: A-range and cross-B range, in the warp's item numbering
+        const uint32_t aS = mine ? sm.sCa[me] - a0 : 0u, aE = mine ? sm.sCa[me + 1] - a0 : 0u;
+        const uint32_t xS = mine ? nA + sm.sXs[me] - x0 : 0u, xE = mine ? nA + sm.sXs[me + 1] - x0 : 0u;
+        int carryA = 0, carryX = 0;
+        for (uint32_t kb = 0; kb < nT; kb += 32) {
+            const uint32_t k = kb + lane;
+            const bool valid = k < nT, isA = k < nA;
+            const bool stA = aE > aS && aS >= kb && aS < kb + 32;
+            const bool stX = xE > xS && xS >= kb && xS < kb + 32;
+            const unsigned mA = __reduce_or_sync(0xffffffffu, stA ? (1u << (aS - kb)) : 0u);
+            const unsigned mX = __reduce_or_sync(0xffffffffu, stX ? (1u << (xS - kb)) : 0u);
+            if (stA) sm.sOwnA[w][aS - kb] = (uint8_t)lane;
+            if (stX) sm.sOwnX[w][xS - kb] = (uint8_t)lane;
+            __syncwarp();
+            const unsigned upto = 0xffffffffu >> (31 - lane);
+            const unsigned leA = mA & upto, leX = mX & upto;
+            const int sA = leA ? 31 - __clz(leA) : 0;
+            const int ownerA = leA ? (int)sm.sOwnA[w][sA] : carryA;
+            const int ownerX = leX ? (int)sm.sOwnX[w][31 - __clz(leX)] : carryX;
+            double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
+            if (valid) {
+                uint32_t c, p;
+                int oself;
+                double4 VA, WA, VB, WB;
+                bool intra = false;
+                if (isA) {
+                    c = a0 + k;
+                    p = cij[c].y;
+                    oself = lo_p + ownerA;
+                    VA = sm.sV[oself]; WA = sm.sW[oself];
+                    if (!(p & PARTNER_EXT)) {
+                        const int64_t pl = (int64_t)p - p0;
+                        intra = pl >= 0 && pl < np;
+                        if (intra) { VB = sm.sV[pl]; WB = sm.sW[pl]; }
+                        else { VB = ld4g(&vin[p]); WB = ld4g(&win[p]); }
+                    }
+                } else {
+                    const uint2 e = xlist[x0 + (k - nA)];
+                    c = e.x;
+                    p = 0u;                       // body b is this tile's particle
+                    oself = lo_p + ownerX;
+                    VA = ld4g(&vin[e.y]); WA = ld4g(&win[e.y]);
+                    VB = sm.sV[oself]; WB = sm.sW[oself];
+                }
+                const G4 g = ld4g(&geo[c]);
+                const R4 rw = ld4g(&row[c]);
+                double mt = sp.mu_t;
+                if (p & PARTNER_EXT) {
+                    d3 bv;
+                    double mr;
+                    boundary_body(p, bnd, bv, mt, mr);
+                    VB = make_double4(bv.x, bv.y, bv.z, 0.0);
+                    WB = make_double4(0.0, 0.0, 0.0, 0.0);
+                }
+                const double la = rw.z, lb = rw.w;
+                const ContactOut r = contact_core(VA, WA, VB, WB, mt, mk(g.x, g.y, g.z), g.w, rw.x, rw.y, la, lb,
+                                                  Pa_in[c], Pb_in[c], sp.rolling_dims);
+                if (isA) {
+                    Pa_out[c] = r.Pa;
+                    Pb_out[c] = r.Pb;
+                    v0 = -r.L.x; v1 = -r.L.y; v2 = -r.L.z;
+                    v3 = -(la * r.nxdPt.x + r.dPr.x); v4 = -(la * r.nxdPt.y + r.dPr.y); v5 = -(la * r.nxdPt.z + r.dPr.z);
+                }
+                if (!isA || intra) {
+                    const uint32_t q = bslot[c] - base;
+                    slot[0 * cap + q] = r.L.x;
+                    slot[1 * cap + q] = r.L.y;
+                    slot[2 * cap + q] = r.L.z;
+                    slot[3 * cap + q] = -lb * r.nxdPt.x + r.dPr.x;
+                    slot[4 * cap + q] = -lb * r.nxdPt.y + r.dPr.y;
+                    slot[5 * cap + q] = -lb * r.nxdPt.z + r.dPr.z;
+                }
+            }
+            // segmented inclusive scan of the A-items, depth = longest A segment of the chunk
+            const int dist = (valid && isA) ? lane - sA : 0;
+            const int maxd = __reduce_max_sync(0xffffffffu, dist);
+            for (int d = 1; d <= maxd; d <<= 1) {
+                const double u0 = __shfl_up_sync(0xffffffffu, v0, d), u1 = __shfl_up_sync(0xffffffffu, v1, d);
+                const double u2 = __shfl_up_sync(0xffffffffu, v2, d), u3 = __shfl_up_sync(0xffffffffu, v3, d);
+                const double u4 = __shfl_up_sync(0xffffffffu, v4, d), u5 = __shfl_up_sync(0xffffffffu, v5, d);
+                if (lane - d >= sA) { v0 += u0; v1 += u1; v2 += u2; v3 += u3; v4 += u4; v5 += u5; }
+            }
+            const bool seg_end = valid && isA && (lane == 31 || ((mA >> (lane + 1)) & 1u) || k + 1 >= nA);
+            if (seg_end) {
+                sm.sAcc[w][0][ownerA] += v0; sm.sAcc[w][1][ownerA] += v1; sm.sAcc[w][2][ownerA] += v2;
+                sm.sAcc[w][3][ownerA] += v3; sm.sAcc[w][4][ownerA] += v4; sm.sAcc[w][5][ownerA] += v5;
+            }
+            carryA = __shfl_sync(0xffffffffu, ownerA, 31);
+            carryX = __shfl_sync(0xffffffffu, ownerX, 31);
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    if (t < np) {
+        // A-sum, then the B-slots in list order (by partner): fixed order -> bit-reproducible
+        double s0 = sm.sAcc[w][0][lane], s1 = sm.sAcc[w][1][lane], s2 = sm.sAcc[w][2][lane];
+        double s3 = sm.sAcc[w][3][lane], s4 = sm.sAcc[w][4][lane], s5 = sm.sAcc[w][5][lane];
+        const uint32_t q0 = sm.sBs[t] - base, q1 = sm.sBs[t + 1] - base;
+        for (uint32_t q = q0; q < q1; q++) {
+            s0 += slot[0 * cap + q]; s1 += slot[1 * cap + q]; s2 += slot[2 * cap + q];
+            s3 += slot[3 * cap + q]; s4 += slot[4 * cap + q]; s5 += slot[5 * cap + q];
+        }
+        double4 V = sm.sV[t], W = sm.sW[t];
+        const uint32_t cnt = (sm.sCa[t + 1] - sm.sCa[t]) + (q1 - q0);
+        if (cnt) {
+            // body update with the real masses (1/m = (c/m)/c): the mass-splitting average
+            const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
+            V.x += im * s0; V.y += im * s1; V.z += im * s2;
+            W.x += iI * s3; W.y += iI * s4; W.z += iI * s5;
+        }
+        st4g(&vout[p0 + t], V);
+        st4g(&wout[p0 + t], W);
+    }
+}
+
+
+void launch_sweep7(int64_t N, unsigned max_b, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
+                   const uint32_t *ca, const uint32_t *bstart, const uint32_t *xstart, const uint2 *xlist,
+                   const uint2 *cij, const uint32_t *bslot, const G4 *geo, const R4 *row, const P4 *Pa_in,
+                   const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s)
+{
+    if (!N) return;
+    if (max_b == 0) max_b = 1;
+    const size_t smem = sweep6_smem<128>(max_b);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(k_sweep7<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = smem;
+    }
+    k_sweep7<128><<<(unsigned)((N + 127) / 128), 128, smem, s>>>(N, (int)max_b, nullptr, vin, win, vout, wout, ca, bstart,
+                                                               xstart, xlist, cij, bslot, geo, row, Pa_in, Pb_in, Pa_out,
+                                                               Pb_out, bnd, sp);
+}
 // ------------------------------------------------------------------ launchers
 void launch_inc6(int64_t N, int tile, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start,
                  const uint2 *inc, uint32_t *ca, uint32_t *bstart, uint32_t *xcnt, uint32_t *xstart, uint32_t *bslot,

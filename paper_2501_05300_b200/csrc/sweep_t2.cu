@@ -156,7 +156,7 @@ __device__ __forceinline__ void stP8(P8 *p, const float4 a, const float4 b)
                  : "memory");
 }
 
-template <bool USE_P8, bool USE_VW>
+template <bool USE_P8, bool USE_VW, bool NOSEL = false>
 __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     k_sweep_t3(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win, double4 *__restrict__ vout,
                double4 *__restrict__ wout, const VW *__restrict__ vwin, VW *__restrict__ vwout,
@@ -229,8 +229,9 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                     WP = make_double4(0.0, 0.0, 0.0, 0.0);
                 }
                 const double4 VS = cat2(sVa[o], sVb[o]), WS = cat2(sWa[o], sWb[o]);
-                const HalfOut r = half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt, g, rw,
-                                               pa, pb, sp.rolling_dims);
+                const HalfOut r = NOSEL ? half_contact(VS, WS, VP, WP, isB, mt, g, rw, pa, pb, sp.rolling_dims)
+                                        : half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt,
+                                                       g, rw, pa, pb, sp.rolling_dims);
                 if (!isB) {
                     if (USE_P8) stP8(&P8out[c], r.Pa, r.Pb);
                     else { Pa_out[c] = r.Pa; Pb_out[c] = r.Pb; }
@@ -288,7 +289,7 @@ void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin,
                   P4 *Pa[2], P4 *Pb[2], void *scratch, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s,
                   double4 *vres, cudaEvent_t e0, cudaEvent_t e1)
 {
-    const bool p8 = variant & 1, vw = (variant >> 1) & 1;
+    const bool p8 = variant & 1, vw = (variant >> 1) & 1, nosel = (variant >> 2) & 1;
     P8 *q[2] = {(P8 *)scratch, (P8 *)scratch + nc};
     VW *u[2] = {(VW *)(q[1] + nc), (VW *)(q[1] + nc) + N};
     const unsigned gb = (unsigned)((N + TT - 1) / TT);
@@ -299,7 +300,8 @@ void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin,
     for (int it = 0; it < n; it++) {
         const int a = it & 1, b = a ^ 1;
 #define T3ARGS N, vi, wi, vbuf[a], wbuf[a], u[a], u[b], inc_start, inc, geo, row, Pa[a], Pb[a], Pa[b], Pb[b], q[a], q[b], bnd, sp
-        if (p8 && vw) k_sweep_t3<true, true><<<gb, TT, 0, s>>>(T3ARGS);
+        if (nosel) k_sweep_t3<true, false, true><<<gb, TT, 0, s>>>(T3ARGS);   // timing only: wrong orientation for B
+        else if (p8 && vw) k_sweep_t3<true, true><<<gb, TT, 0, s>>>(T3ARGS);
         else if (p8) k_sweep_t3<true, false><<<gb, TT, 0, s>>>(T3ARGS);
         else if (vw) k_sweep_t3<false, true><<<gb, TT, 0, s>>>(T3ARGS);
         else k_sweep_t3<false, false><<<gb, TT, 0, s>>>(T3ARGS);

@@ -432,6 +432,98 @@ def test_jacobi_fixed_point_equals_lcp_enumeration(oracle_mod):
     np.testing.assert_allclose(c2["P"][:, 0], c["P"][:, 0], rtol=1e-6)
 
 
+def test_gauss_seidel_fixed_point_equals_lcp_enumeration(oracle_mod):
+    """Coloured projected Gauss-Seidel (P:134 PGS) converges to the same LCP
+    solution of the SPOOK normal rows as the Jacobi iteration: enumeration on the
+    configuration of the Jacobi pin, and GS at 200 sweeps already as close as Jacobi at 20,000."""
+    r = 3e-3
+    h = 1e-5
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    x = np.array([[0, 0, r - 2e-5], [5.9e-3, 0, r - 1e-5], [2.9e-3, 1e-4, r + 5.1e-3]])
+    v = np.array([[0.001, 0, -0.002], [0, 0.001, 0], [0, 0, -0.003]])
+    n = len(x)
+    mk = lambda: oracle_mod.OracleWorld(x, v, np.zeros((n, 3)), [r] * n, np.arange(n), walls=floor)
+    cj, _, _ = mk().step(oracle_mod.make_params(h=h, n_it=20000, mu_t=0, mu_r=0, v_imp=1e30))
+    cg, _, _ = mk().step(oracle_mod.make_params(h=h, n_it=20000, mu_t=0, mu_r=0, v_imp=1e30, ordering=1))
+    np.testing.assert_allclose(cg["P"][:, 0], cj["P"][:, 0], rtol=1e-7)
+    c200, _, _ = mk().step(oracle_mod.make_params(h=h, n_it=200, mu_t=0, mu_r=0, v_imp=1e30, ordering=1))
+    np.testing.assert_allclose(c200["P"][:, 0], cj["P"][:, 0], rtol=1e-6)
+
+
+def test_gauss_seidel_single_row_is_exact_after_one_sweep(oracle_mod):
+    """one normal row, the LCP solution max(0, -q/(G M^-1 G^T + Sigma)) after ONE
+    Gauss-Seidel iteration (sphere resting on a floor, frictionless, no impact stage)."""
+    r, h = 3e-3, 1e-5
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    x, v = np.array([[0.0, 0.0, r - 1e-5]]), np.array([[0.0, 0.0, -0.01]])
+    W = oracle_mod.OracleWorld(x, v, np.zeros((1, 3)), [r], [0], walls=floor)
+    p = oracle_mod.make_params(h=h, n_it=1, mu_t=0, mu_r=0, v_imp=1e30, ordering=1)
+    c, _, _ = W.step(p)
+    m, _ = oracle_mod.mass_inertia(2 * r, p.rho)
+    Es = p.E / (2 * (1 - p.nu**2))
+    Ups = 1.0 / (1 + 4 * p.damp_steps)
+    dl = 1e-5
+    kn = Es * math.sqrt(2 * r) / 3
+    S = 4 * Ups / (h * h * 1.25 * kn * math.sqrt(dl))
+    # n = -z (particle -> wall): u_n = n.(v_wall - v) = v_z; the bias uses u_n at v^k, the row v* = v^k + h g
+    un_star = v[0, 2] + h * -9.81
+    b = 4 * Ups / h * dl / 1.25 + Ups * v[0, 2]
+    P = max(0.0, -(un_star - b) / (1.0 / m + S))
+    assert c["P"][0, 0] == pytest.approx(P, rel=1e-12)
+
+
+def test_splitmix64_published_values(oracle_mod):
+    """The colouring priority is SplitMix64 (Steele, Lea, Flood 2014): with seed 0 its first
+    two outputs are 0xE220A8397B1DCDAF and 0x6E789E6AA1B965F4."""
+    assert oracle_mod.splitmix64(0) == 0xE220A8397B1DCDAF
+    assert oracle_mod.splitmix64(0x9E3779B97F4A7C15) == 0x6E789E6AA1B965F4
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_colouring_is_proper_and_greedy_by_priority(oracle_mod, seed):
+    """Checked by properties, not by re-running the algorithm: (1) contacts sharing a particle
+    have different colours; (2) every colour below a contact's colour is taken by a conflicting
+    contact of higher priority (the defining property of greedy colouring in priority order)."""
+    rng = np.random.default_rng(seed)
+    n = 60
+    a = rng.integers(0, n, 400)
+    b = rng.integers(-1, n, 400)
+    b = np.where(b == a, -1, b)
+    key = np.array([(int(min(x, y)) << 32) | int(max(x, y)) if y >= 0 else (int(x) << 32) | 0xFFFFFFF0
+                    for x, y in zip(a, b)], dtype=np.uint64)
+    key, idx = np.unique(key, return_index=True)
+    a, b = a[idx], b[idx]
+    col, ncol = oracle_mod.color_contacts(key, a, b, n)
+    assert ncol == col.max() + 1 and ncol > 1
+    pri = np.array([oracle_mod.splitmix64(int(k)) for k in key], dtype=object)
+    touch = [set() for _ in range(n)]
+    for c in range(len(key)):
+        touch[a[c]].add(c)
+        if b[c] >= 0:
+            touch[b[c]].add(c)
+    for c in range(len(key)):
+        nb = (touch[a[c]] | (touch[b[c]] if b[c] >= 0 else set())) - {c}
+        assert all(col[o] != col[c] for o in nb)
+        higher = {col[o] for o in nb if (pri[o], -int(key[o])) > (pri[c], -int(key[c]))}
+        assert all(q in higher for q in range(col[c]))
+
+
+def test_gauss_seidel_converges_faster_than_jacobi(oracle_mod):
+    """The reason the paper uses PGS: on a 4-stack under gravity, Gauss-Seidel at N
+    sweeps is closer to the converged impulses than mass-splitting Jacobi at N sweeps."""
+    r, h = 3e-3, 1e-4
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    k = 4
+    x = np.array([[0, 0, r + i * (2 * r - 2e-6)] for i in range(k)])
+    mk = lambda: oracle_mod.OracleWorld(x, np.zeros((k, 3)), np.zeros((k, 3)), [r] * k, np.arange(k), walls=floor)
+    ref, _, _ = mk().step(oracle_mod.make_params(h=h, n_it=20000, v_imp=1e30, ordering=1))
+    err = {}
+    for o in (0, 1):
+        c, _, _ = mk().step(oracle_mod.make_params(h=h, n_it=8, v_imp=1e30, ordering=o))
+        err[o] = np.abs(c["P"][:, 0] - ref["P"][:, 0]).max()
+    assert err[1] < 0.5 * err[0]
+
+
 def test_kinematic_and_force_driven_plate(oracle_mod):
     """A velocity-driven axis advances exactly u h per step; a force-driven plate pressing
     a sphere onto the floor reaches the static balance F_p = -F_applied, floor = F + m g."""
