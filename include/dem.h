@@ -69,7 +69,10 @@ typedef struct {
     double v_impact;           /* impact threshold [m/s]; < 0 -> 20 |g| dt; >= 1e30 off */
     double gravity[3];
     int32_t rolling_dims;      /* 3: rolling row on the full relative spin (default); 2: tangential */
-    int32_t pad0;
+    int32_t ordering;          /* 0: Jacobi sweep with mass splitting (default, reading R2);
+                                  1: coloured projected Gauss-Seidel (P:134 PGS):
+                                  contacts coloured greedily in SplitMix64(key) priority, swept colour
+                                  by colour with the real masses (single undecomposed context only) */
     double skin;               /* Verlet skin [m] of the candidate list; <= 0 -> 0.1 r_min */
 } dem_solver;
 
@@ -167,6 +170,8 @@ typedef struct {
     double max_v;              /* max |v| after the step */
     double max_disp;           /* max displacement since the last rebuild [m] */
     int32_t n_iter, n_iter_impact;
+    int32_t n_colors;          /* Gauss-Seidel ordering: colours of the step's contact graph (else 0) */
+    int32_t pad0;
 } dem_step_report;
 
 /* State exchange, ascending gid order; n = capacity in, count out. */

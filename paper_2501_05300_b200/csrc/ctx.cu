@@ -104,6 +104,12 @@ struct dem_ctx {
     int64_t n_send[2] = {0, 0}, n_recv[2] = {0, 0}, cap_halo[2] = {0, 0};
     uint32_t *send_pre[2] = {nullptr, nullptr}, *send_idx[2] = {nullptr, nullptr}, *recv_idx[2] = {nullptr, nullptr};
     double4 *hs[2] = {nullptr, nullptr}, *hr[2] = {nullptr, nullptr};
+    // coloured Gauss-Seidel ordering (solver.ordering == 1; gs.cu)
+    uint64_t *gs_key = nullptr;
+    int *gs_col = nullptr;
+    uint32_t *gs_ord = nullptr;
+    unsigned int *gs_scr = nullptr;
+    std::vector<uint32_t> gs_cstart;
     // timing
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -324,6 +330,8 @@ static dem_status ensure_cand(dem_ctx *ctx, int64_t n)
     TRY(regrow(ctx, &ctx->row_imp, cap)); TRY(regrow(ctx, &ctx->Pwa, cap)); TRY(regrow(ctx, &ctx->Pwb, cap));
     for (int k = 0; k < 2; k++) { TRY(regrow(ctx, &ctx->Pa[k], cap)); TRY(regrow(ctx, &ctx->Pb[k], cap)); }
     TRY(regrow(ctx, &ctx->ccand, cap));
+    TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
+    if (!ctx->gs_scr) TRY(A(ctx, &ctx->gs_scr, 260));
     TRY(regrow(ctx, &ctx->inc, 2 * cap));
     ctx->cap_cand = cap;
     ctx->nc = 0;
@@ -732,7 +740,25 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     }
     tstart(ctx, 2);
     const int n_imp = ctx->sol.n_iter_impact > 0 ? ctx->sol.n_iter_impact : ctx->sol.n_iter;
-    if (impact) {
+    const bool gs = ctx->sol.ordering == 1;
+    if (gs) {
+        // colour the contact graph (priority SplitMix64(key): the oracle's greedy colouring)
+        const int ncol = gs_color(nc, ctx->cij, ctx->gid, ctx->inc_start, ctx->inc, ctx->gs_key, ctx->gs_col, ctx->keys,
+                                  ctx->vals, ctx->sort_tmp, ctx->gs_scr, ctx->gs_cstart, s, &ctx->launches);
+        if (ncol < 0) { ctx->err = "Gauss-Seidel colouring needs more than 256 colours"; return DEM_ERR_INVALID; }
+        if (nc) CK(cudaMemcpyAsync(ctx->gs_ord, ctx->vals[0], nc * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+    }
+    if (impact && gs) {
+        // Newton impact stage (reading R13) in Gauss-Seidel order, in place
+        CK(cudaMemsetAsync(ctx->Pa[0], 0, nc * sizeof(P4), s));
+        CK(cudaMemsetAsync(ctx->Pb[0], 0, nc * sizeof(P4), s));
+        for (int it = 0; it < n_imp; it++)
+            gs_sweep(ctx->gs_cstart, ctx->gs_ord, ctx->cij, ctx->geo, ctx->row_imp, ctx->Pa[0], ctx->Pb[0],
+                     ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->inc_start, ctx->db, sp, s, &ctx->launches);
+        ctx->tm.n_sweep_launches += n_imp;
+        ctx->tm.contact_sweeps += (int64_t)n_imp * nc;
+        ctx->tm.particle_sweeps += (int64_t)n_imp * N;
+    } else if (impact) {
         // Newton impact stage from P = 0 with Sigma = 0 (reading R13); impulses discarded
         CK(cudaMemsetAsync(ctx->Pa[0], 0, nc * sizeof(P4), s));
         CK(cudaMemsetAsync(ctx->Pb[0], 0, nc * sizeof(P4), s));
@@ -760,7 +786,19 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     tstart(ctx, 3);
     const int n_it = ctx->sol.n_iter;
     const P4 *pin_a = ctx->Pwa, *pin_b = ctx->Pwb;
-    for (int it = 0; it < n_it; it++) {
+    if (gs) {
+        // N_it coloured Gauss-Seidel sweeps, impulses and velocities updated in place
+        if (nc) {
+            CK(cudaMemcpyAsync(ctx->Pa[0], ctx->Pwa, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(ctx->Pb[0], ctx->Pwb, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
+        }
+        for (int it = 0; it < n_it; it++)
+            gs_sweep(ctx->gs_cstart, ctx->gs_ord, ctx->cij, ctx->geo, ctx->row, ctx->Pa[0], ctx->Pb[0], ctx->vel[ctx->cur],
+                     ctx->ang[ctx->cur], ctx->inc_start, ctx->db, sp, s, &ctx->launches);
+        pin_a = ctx->Pa[0];
+        pin_b = ctx->Pb[0];
+    }
+    for (int it = 0; it < (gs ? 0 : n_it); it++) {
         P4 *oa = ctx->Pa[it & 1], *ob = ctx->Pb[it & 1];
         launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                      ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
@@ -770,7 +808,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         pin_a = oa;
         pin_b = ob;
     }
-    ctx->launches += n_it;
+    if (!gs) ctx->launches += n_it;
     ctx->tm.n_sweep_launches += n_it;
     ctx->tm.contact_sweeps += (int64_t)n_it * nc;
     ctx->tm.particle_sweeps += (int64_t)n_it * N;
@@ -864,6 +902,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     rep->max_v = maxv;
     rep->max_disp = maxd;
     rep->n_iter = n_it;
+    rep->n_colors = gs ? (int32_t)ctx->gs_cstart.size() - 1 : 0;
     rep->n_iter_impact = impact ? n_imp : 0;
     const double skin = ctx->grid.skin;
     ctx->need_rebuild = (2.0 * maxd >= 0.9 * skin) || (maxd + sc.bnd_disp >= 0.9 * skin);
@@ -942,7 +981,7 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
     if (desc->struct_size != sizeof(dem_bed_desc)) { g_create_err = "dem_bed_desc struct_size mismatch"; return DEM_ERR_INVALID; }
     if (!valid_material(desc->mat)) { g_create_err = "invalid material"; return DEM_ERR_INVALID; }
     const dem_solver &so = desc->solver;
-    if (!(so.dt > 0) || so.n_iter < 1 || !(so.hertz_exp == 1.25 || so.hertz_exp == 1.0) ||
+    if (!(so.dt > 0) || so.n_iter < 1 || !(so.ordering == 0 || so.ordering == 1) || !(so.hertz_exp == 1.25 || so.hertz_exp == 1.0) ||
         (so.hertz_exp == 1.0 && !(so.k_lin > 0)) || so.damping_steps < 0) {
         g_create_err = "invalid solver settings (dt > 0, n_iter >= 1, hertz_exp 1.25 or 1 with k_lin > 0)";
         return DEM_ERR_INVALID;
@@ -1046,7 +1085,7 @@ dem_status dem_step(dem_ctx *ctx, int32_t n_steps, dem_step_report *last)
 
 static bool valid_solver(const dem_solver &so)
 {
-    return so.dt > 0 && so.n_iter >= 1 && (so.hertz_exp == 1.25 || so.hertz_exp == 1.0) &&
+    return (so.ordering == 0 || so.ordering == 1) && so.dt > 0 && so.n_iter >= 1 && (so.hertz_exp == 1.25 || so.hertz_exp == 1.0) &&
            !(so.hertz_exp == 1.0 && !(so.k_lin > 0)) && so.damping_steps >= 0;
 }
 
@@ -1054,6 +1093,7 @@ dem_status dem_set_solver(dem_ctx *ctx, const dem_solver *so)
 {
     if (!ctx || !so) return DEM_ERR_INVALID;
     if (!valid_solver(*so)) { ctx->err = "invalid solver settings"; return DEM_ERR_INVALID; }
+    if (ctx->tp && so->ordering == 1) { ctx->err = "Gauss-Seidel ordering needs a single undecomposed context"; return DEM_ERR_INVALID; }
     const double skin = ctx->grid.skin;
     ctx->sol = *so;
     setup_solve_params(ctx);

@@ -1,6 +1,7 @@
 // kernels.h -- host launchers of the device kernels (detect.cu, solve.cu); internal to libdem.so.
 #pragma once
 #include <string>
+#include <vector>
 
 #include "../../include/dem.h"
 #include "common.cuh"
@@ -119,3 +120,10 @@ void launch_sweep7(int64_t N, unsigned max_b, const double4 *vin, const double4 
                    const uint32_t *ca, const uint32_t *bstart, const uint32_t *xstart, const uint2 *xlist,
                    const uint2 *cij, const uint32_t *bslot, const G4 *geo, const R4 *row, const P4 *Pa_in,
                    const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+// gs.cu: coloured Gauss-Seidel ordering
+int gs_color(int64_t nc, const uint2 *cij, const uint32_t *gid, const uint32_t *inc_start, const uint2 *inc,
+             uint64_t *key, int *color, uint64_t *keys[2], uint32_t *vals[2], void *sort_tmp, unsigned int *dscr,
+             std::vector<uint32_t> &cstart, cudaStream_t s, long long *launches);
+void gs_sweep(const std::vector<uint32_t> &cstart, const uint32_t *ord, const uint2 *cij, const G4 *geo, const R4 *row,
+              P4 *Pa, P4 *Pb, double4 *vel, double4 *ang, const uint32_t *inc_start, const DevBoundary *bnd,
+              const SolveParams &sp, cudaStream_t s, long long *launches);

@@ -89,8 +89,10 @@ def compare_step(bed, n_it=30, dt=1e-5, with_walls=True, hist=None, material=Non
     """Run n_steps on both sides from the same state; compare the last step."""
     rho = (material or {}).get("density", 2600.0)
     Wo = oracle_world(bed, walls=with_walls)
-    po = oracle_params(n_it, dt, material, **{k: v for k, v in solver.items() if k in ("v_imp", "g", "n_imp")})
+    po = oracle_params(n_it, dt, material, **{k: v for k, v in solver.items() if k in ("v_imp", "g", "n_imp", "ordering")})
     gsol = dict(dt=dt, n_iter=n_it)
+    if "ordering" in solver:
+        gsol["ordering"] = solver["ordering"]
     if "v_imp" in solver:
         gsol["v_impact"] = solver["v_imp"]
     if "g" in solver:
@@ -118,6 +120,7 @@ def compare_step(bed, n_it=30, dt=1e-5, with_walls=True, hist=None, material=Non
         "force_err": float(eF.max()) if len(eF) else 0.0, "torque_err": float(eT.max()) if len(eT) else 0.0,
         "force_p99": float(np.percentile(eF, 99)) if len(eF) else 0.0,
         "impact_ref": int(Wo.last_report.impact_fired), "impact_gpu": int(rep["impact_fired"]),
+        "n_colors_gpu": int(rep.get("n_colors", 0)),
     }
     if pairs_equal and len(c_ref):
         res["normal_err"] = float(np.abs(c_gpu["n"] - c_ref["n"]).max())
