@@ -209,6 +209,9 @@ typedef struct {
 typedef struct {
     double pos[3], vel[3];
     double force[3];           /* contact reaction on the plate during the last step [N] */
+    double motor_force[3];     /* axis force of the last step [N]: the target of a force axis; for
+                                  velocity / locked axes the constraint (motor) force lambda_j that
+                                  the drive applied (the required pull force) */
     int64_t n_contacts;
 } dem_plate_state;
 
@@ -254,10 +257,20 @@ dem_status dem_get_contacts(dem_ctx *ctx, dem_contact_view *view);
  * step (O6).  on_device selects device or host buffers. */
 dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device);
 
-/* Plates: add (all axes locked), drive one axis, read state. */
+/* Plates: add (all axes locked), drive one axis, read state.
+ * dem_drive_plate: mode DEM_AXIS_VELOCITY is a motor G_j v = u_j(t) with u ramped linearly
+ * from 0 to target over ramp_time from the call; its constraint force is limited to
+ * [f_min, f_max] (Eq. 4; -INFINITY / INFINITY: unlimited).  Coupling is staggered (reading
+ * R18): after each step the motor force lambda = m (u(t+h) - v)/h - F_contact is clamped to the
+ * limits and the axis velocity for the next step is v + h (lambda + F_contact)/m (= u(t+h)
+ * exactly when no limit is active).  At the call an unlimited velocity axis takes u at once (0 if
+ * ramped), a limited one keeps its velocity.  Force axes (target in N) and locked axes ignore the
+ * limits.
+ * DEM_ERR_INVALID: bad plate/axis/mode, non-finite target, ramp_time < 0, NaN or f_min > f_max. */
 dem_status dem_add_plate(dem_ctx *ctx, const dem_plate_desc *desc, const double pos[3], int32_t *plate_id);
 dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mode,
-                           double target /* m/s or N */, double ramp_time /* s, velocity mode */);
+                           double target /* m/s or N */, double ramp_time /* s, velocity mode */,
+                           double f_min, double f_max /* N, velocity mode (Eq. 4) */);
 dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *out);
 
 /* Kinematic box wall: velocity along its inward normal (shear-box / servo walls). */

@@ -62,6 +62,8 @@ class Plate(C.Structure):
         ("mode", C.c_int32 * 3), ("pad2", C.c_int32),
         ("target", C.c_double * 3), ("ramp", C.c_double * 3), ("t0", C.c_double * 3),
         ("force", C.c_double * 3),
+        ("limit", C.c_int32 * 3), ("pad3", C.c_int32),
+        ("fmin", C.c_double * 3), ("fmax", C.c_double * 3), ("motor", C.c_double * 3),
     ]
 
 

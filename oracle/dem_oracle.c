@@ -815,15 +815,29 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
         or_plate *P = &w->plates[q];
         for (int k = 0; k < 3; k++) P->pos[k] += h * P->vel[k];
         for (int k = 0; k < 3; k++) {
-            if (P->mode[k] == 0) P->vel[k] = 0.0;
-            else if (P->mode[k] == 1) {
+            if (P->mode[k] == 2) {                                          /* staggered force axis */
+                P->vel[k] += h * (P->target[k] + P->force[k]) / P->mass;
+                P->motor[k] = P->target[k];
+                continue;
+            }
+            /* locked (u = 0) or motor G_j v = u_j(t) with u ramped over ramp[k] */
+            double u = 0.0;
+            if (P->mode[k] == 1) {
                 double s = P->ramp[k] > 0.0 ? (t1 - P->t0[k]) / P->ramp[k] : 1.0;
                 if (s > 1.0) s = 1.0;
                 if (s < 0.0) s = 0.0;
-                P->vel[k] = P->target[k] * s;
-            } else {
-                P->vel[k] += h * (P->target[k] + P->force[k]) / P->mass;   /* staggered force axis */
+                u = P->target[k] * s;
             }
+            /* staggered motor (R18): the force reaching u at t1 against this step's contact
+             * reaction; Eq. 4 limits lambda_min <= lambda <= lambda_max on velocity axes */
+            double lambda = P->mass * (u - P->vel[k]) / h - P->force[k];
+            if (P->mode[k] == 1 && P->limit[k] && (lambda < P->fmin[k] || lambda > P->fmax[k])) {
+                lambda = lambda < P->fmin[k] ? P->fmin[k] : P->fmax[k];
+                P->vel[k] += h * (lambda + P->force[k]) / P->mass;
+            } else {
+                P->vel[k] = u;
+            }
+            P->motor[k] = lambda;
         }
     }
     w->time = t1;

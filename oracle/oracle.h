@@ -60,6 +60,10 @@ typedef struct {
     double ramp[3];           /* linear ramp time of a velocity target */
     double t0[3];             /* time the drive started */
     double force[3];          /* out: contact reaction on the plate of the last step [N] */
+    int32_t limit[3];         /* velocity axis with motor force limits (Eq. 4) */
+    int32_t pad3;
+    double fmin[3], fmax[3];  /* lambda_min, lambda_max [N] (used when limit[k]) */
+    double motor[3];          /* out: the axis force of the last step [N] (target of a force axis) */
 } or_plate;
 
 /* A contact (output) or a history record (input; only key and P are read).

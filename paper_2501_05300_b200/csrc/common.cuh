@@ -148,6 +148,10 @@ struct DevBoundary {
     int mode[DEM_MAX_PLATES][3];
     double target[DEM_MAX_PLATES][3], ramp[DEM_MAX_PLATES][3], t0[DEM_MAX_PLATES][3];
     double pforce[DEM_MAX_PLATES][3];   // reaction of the last step [N]
+    // motor force limits of velocity axes (Eq. 4: lambda_min <= lambda_j <= lambda_max)
+    int plimit[DEM_MAX_PLATES][3];
+    double pfmin[DEM_MAX_PLATES][3], pfmax[DEM_MAX_PLATES][3];
+    double pmotor[DEM_MAX_PLATES][3];   // motor / constraint force of the last step [N]
     int64_t pcount[DEM_MAX_PLATES];
     double time;
     // references at the last rebuild (trigger)

@@ -1258,6 +1258,10 @@ dem_status dem_add_plate(dem_ctx *ctx, const dem_plate_desc *d, const double pos
         b.ramp[p][k] = 0;
         b.t0[p][k] = 0;
         b.pforce[p][k] = 0;
+        b.pmotor[p][k] = 0;
+        b.plimit[p][k] = 0;
+        b.pfmin[p][k] = -INFINITY;
+        b.pfmax[p][k] = INFINITY;
     }
     b.pmass[p] = d->mass;
     b.pmu_t[p] = d->mu_t;
@@ -1270,12 +1274,13 @@ dem_status dem_add_plate(dem_ctx *ctx, const dem_plate_desc *d, const double pos
     return DEM_OK;
 }
 
-dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mode, double target, double ramp_time)
+dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mode, double target, double ramp_time,
+                           double f_min, double f_max)
 {
     if (!ctx) return DEM_ERR_INVALID;
     DevBoundary &b = ctx->hb;
     if (plate < 0 || plate >= b.n_plates || axis < 0 || axis > 2 || mode < 0 || mode > 2 || !std::isfinite(target) ||
-        ramp_time < 0) {
+        !(ramp_time >= 0) || std::isnan(f_min) || std::isnan(f_max) || !(f_min <= f_max)) {
         ctx->err = "invalid plate drive";
         return DEM_ERR_INVALID;
     }
@@ -1283,8 +1288,13 @@ dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mo
     b.target[plate][axis] = target;
     b.ramp[plate][axis] = ramp_time;
     b.t0[plate][axis] = b.time;
+    b.plimit[plate][axis] = mode == DEM_AXIS_VELOCITY && (f_min > -INFINITY || f_max < INFINITY);
+    b.pfmin[plate][axis] = f_min;
+    b.pfmax[plate][axis] = f_max;
+    // an unlimited motor takes its speed at once (from rest if ramped); a force-limited one keeps
+    // the current velocity and is accelerated by its motor from the next step on
     if (mode == DEM_AXIS_LOCKED) b.pvel[plate][axis] = 0;
-    else if (mode == DEM_AXIS_VELOCITY) b.pvel[plate][axis] = ramp_time > 0 ? 0.0 : target;
+    else if (mode == DEM_AXIS_VELOCITY && !b.plimit[plate][axis]) b.pvel[plate][axis] = ramp_time > 0 ? 0.0 : target;
     return upload_boundary(ctx);
 }
 
@@ -1293,7 +1303,8 @@ dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *o)
     if (!ctx || !o) return DEM_ERR_INVALID;
     const DevBoundary &b = ctx->hb;
     if (plate < 0 || plate >= b.n_plates) { ctx->err = "no such plate"; return DEM_ERR_INVALID; }
-    for (int k = 0; k < 3; k++) { o->pos[k] = b.ppos[plate][k]; o->vel[k] = b.pvel[plate][k]; o->force[k] = b.pforce[plate][k]; }
+    for (int k = 0; k < 3; k++) { o->pos[k] = b.ppos[plate][k]; o->vel[k] = b.pvel[plate][k]; o->force[k] = b.pforce[plate][k];
+                                    o->motor_force[k] = b.pmotor[plate][k]; }
     o->n_contacts = b.pcount[plate];
     return DEM_OK;
 }

@@ -659,13 +659,28 @@ __global__ void k_boundary(DevBoundary *bnd, const unsigned long long *__restric
         bnd->pcount[q] = pcount[q];
         for (int k = 0; k < 3; k++) {
             const int md = bnd->mode[q][k];
-            if (md == 0) bnd->pvel[q][k] = 0.0;
-            else if (md == 1) {
+            const double v = bnd->pvel[q][k], fc = bnd->pforce[q][k], m = bnd->pmass[q];
+            if (md == 2) {
+                bnd->pvel[q][k] = v + h * (bnd->target[q][k] + fc) / m;
+                bnd->pmotor[q][k] = bnd->target[q][k];
+                continue;
+            }
+            double u1 = 0.0;   // locked axes: u = 0, never limited
+            if (md == 1) {
                 double s = bnd->ramp[q][k] > 0.0 ? (t1 - bnd->t0[q][k]) / bnd->ramp[q][k] : 1.0;
                 s = s > 1.0 ? 1.0 : (s < 0.0 ? 0.0 : s);
-                bnd->pvel[q][k] = bnd->target[q][k] * s;
+                u1 = bnd->target[q][k] * s;
+            }
+            // staggered motor (reading R18 + Eq. 4): the force that brings the axis to u(t1)
+            // against this step's contact reaction, clamped to [f_min, f_max]
+            const double lam = m * (u1 - v) / h - fc;
+            if (md == 1 && bnd->plimit[q][k] && (lam < bnd->pfmin[q][k] || lam > bnd->pfmax[q][k])) {
+                const double lc = lam < bnd->pfmin[q][k] ? bnd->pfmin[q][k] : bnd->pfmax[q][k];
+                bnd->pvel[q][k] = v + h * (lc + fc) / m;
+                bnd->pmotor[q][k] = lc;
             } else {
-                bnd->pvel[q][k] += h * (bnd->target[q][k] + bnd->pforce[q][k]) / bnd->pmass[q];
+                bnd->pvel[q][k] = u1;
+                bnd->pmotor[q][k] = lam;
             }
         }
         double d2 = 0.0;

@@ -102,7 +102,8 @@ class PlateDesc(C.Structure):
 
 
 class PlateState(C.Structure):
-    _fields_ = [("pos", C.c_double * 3), ("vel", C.c_double * 3), ("force", C.c_double * 3), ("n_contacts", C.c_int64)]
+    _fields_ = [("pos", C.c_double * 3), ("vel", C.c_double * 3), ("force", C.c_double * 3),
+                ("motor_force", C.c_double * 3), ("n_contacts", C.c_int64)]
 
 
 class Timing(C.Structure):
@@ -142,7 +143,7 @@ def lib():
         L.dem_get_contacts.argtypes = [vp, C.POINTER(ContactView)]
         L.dem_get_forces.argtypes = [vp, vp, vp, i32]
         L.dem_add_plate.argtypes = [vp, C.POINTER(PlateDesc), C.POINTER(C.c_double), C.POINTER(i32)]
-        L.dem_drive_plate.argtypes = [vp, i32, i32, i32, d, d]
+        L.dem_drive_plate.argtypes = [vp, i32, i32, i32, d, d, d, d]
         L.dem_get_plate.argtypes = [vp, i32, C.POINTER(PlateState)]
         L.dem_drive_wall.argtypes = [vp, i32, d]
         L.dem_set_timing.argtypes = [vp, i32]
@@ -479,13 +480,15 @@ class Bed:
         self._check(lib().dem_add_plate(self._h, C.byref(d), p, C.byref(pid)))
         return pid.value
 
-    def drive_plate(self, plate, axis, mode, target, ramp_time=0.0):
-        self._check(lib().dem_drive_plate(self._h, plate, axis, mode, target, ramp_time))
+    def drive_plate(self, plate, axis, mode, target, ramp_time=0.0, f_min=-np.inf, f_max=np.inf):
+        """Drive one plate axis (dem_drive_plate): f_min/f_max limit a velocity axis' motor force (Eq. 4)."""
+        self._check(lib().dem_drive_plate(self._h, plate, axis, mode, target, ramp_time, f_min, f_max))
 
     def get_plate(self, plate):
         s = PlateState()
         self._check(lib().dem_get_plate(self._h, plate, C.byref(s)))
-        return {"pos": list(s.pos), "vel": list(s.vel), "force": list(s.force), "n_contacts": s.n_contacts}
+        return {"pos": list(s.pos), "vel": list(s.vel), "force": list(s.force),
+                "motor_force": list(s.motor_force), "n_contacts": s.n_contacts}
 
     def drive_wall(self, wall, normal_velocity):
         self._check(lib().dem_drive_wall(self._h, wall, normal_velocity))

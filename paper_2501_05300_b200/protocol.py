@@ -9,7 +9,8 @@ axis is velocity-driven, its speed ramped from 0 to u over t_shear_ramp (P:254: 
 linearly from 0 to 100 mm/s over 0.1 s") then constant until t_end, the vertical axis still at
 F_N.  Recorded per step: t, sinkage (datum: the surface under the plate at t = 0), the applied
 load, the measured normal contact force, the pull force F_T (the horizontal motor's constraint
-force = minus the horizontal contact reaction) and the traction F_T / F_N.
+force lambda of Eq. 4, which at constant speed is minus the horizontal contact reaction) and
+the traction F_T / F_N.
 """
 from __future__ import annotations
 
@@ -32,6 +33,7 @@ class PlateProtocol:
     window: float = 0.1           # averaging window of the sinkage metrics [s]
     smooth: float = 0.025         # moving average before the peak-traction maximum [s]
     max_contact_loss: float = 0.2  # no plate contact for longer in phase II/III: fault
+    f_pull_max: float = float("inf")  # Eq. 4 limit |lambda| <= f_pull_max on the pull motor
 
 
 class ExperimentFault(RuntimeError):
@@ -57,7 +59,8 @@ def run_plate_test(bed: "D.Bed", plate: int, proto: PlateProtocol, dt: float, z_
             bed.drive_plate(plate, 2, D.AXIS_FORCE, -F)          # downward load on a force axis
         elif s == n_I:
             bed.drive_plate(plate, 2, D.AXIS_FORCE, -proto.F_N)
-            bed.drive_plate(plate, 0, D.AXIS_VELOCITY, proto.u_shear, proto.t_shear_ramp)
+            bed.drive_plate(plate, 0, D.AXIS_VELOCITY, proto.u_shear, proto.t_shear_ramp,
+                            -proto.f_pull_max, proto.f_pull_max)
         rep = bed.step(1)
         if s % record_every:
             continue
@@ -67,8 +70,9 @@ def run_plate_test(bed: "D.Bed", plate: int, proto: PlateProtocol, dt: float, z_
         cols["sinkage"].append(z_datum - g["pos"][2])
         cols["F_N_applied"].append(F_app)
         cols["F_N_measured"].append(g["force"][2])
-        cols["F_T"].append(-g["force"][0])
-        cols["traction"].append(-g["force"][0] / F_app if F_app > 0 else np.nan)
+        F_T = g["motor_force"][0]                                   # the pull motor's force
+        cols["F_T"].append(F_T)
+        cols["traction"].append(F_T / F_app if F_app > 0 else np.nan)
         cols["plate_x"].append(g["pos"][0])
         cols["n_contacts"].append(g["n_contacts"])
         if s >= n_I:                                               # SPEC S:474 experiment fault

@@ -300,3 +300,45 @@ def test_full_size_sampled_pair_set_and_invariants():
     mine = c[np.isin(ka, list(sg)) | np.isin(kb, list(sg))]
     np.testing.assert_array_equal(np.sort(mine["key"]), ref["key"])
     assert len(ref) > 1000
+
+
+def test_force_limited_motor_vs_oracle():
+    """Eq. 4 motor limits: a grouser plate pressed down by a velocity motor (-0.3 m/s)
+    limited to 0.2 N, and sheared along x by a motor limited to 0.05 N; 60 steps on both sides:
+    pair sets every step, plate positions, contact and motor forces."""
+    bed = _small_bed_for_plates(47)
+    lo = [(-0.006, -0.006, 0.0), (-0.006, -0.006, -0.003), (0.003, -0.006, -0.003)]
+    hi = [(0.006, 0.006, 0.002), (-0.004, 0.006, 0.0), (0.005, 0.006, 0.0)]
+    top = bed.x[:, 2].max() + 2.0e-3
+    P = O.make_plate(lo, hi, pos=(0.015, 0.015, top), mass=0.02)
+    P.mode[2], P.target[2], P.limit[2], P.fmin[2], P.fmax[2] = 1, -0.3, 1, -0.2, 0.2
+    P.mode[0], P.target[0], P.limit[0], P.fmin[0], P.fmax[0] = 1, 0.1, 1, -0.05, 0.05
+    Wo = oracle_world(bed, plates=[P])
+    po = oracle_params(30, 1e-5)
+    gb = gpu_bed(bed, dt=1e-5, n_iter=30)
+    pid = gb.add_plate(lo, hi, (0.015, 0.015, top), 0.02)
+    gb.drive_plate(pid, 2, 1, -0.3, 0.0, -0.2, 0.2)
+    gb.drive_plate(pid, 0, 1, 0.1, 0.0, -0.05, 0.05)
+    saturated = 0
+    try:
+        for s in range(60):
+            c_ref, _, _ = Wo.step(po)
+            gb.step(1)
+            c = gb.get_contacts()
+            assert np.array_equal(c["key"], c_ref["key"]), s
+            g = gb.get_plate(pid)
+            for k in (0, 2):
+                assert g["pos"][k] == pytest.approx(Wo.plates[0].pos[k], abs=1e-12), (s, k)
+                assert g["motor_force"][k] == pytest.approx(Wo.plates[0].motor[k], rel=1e-6, abs=1e-9), (s, k)
+            saturated += g["motor_force"][2] == -0.2
+    finally:
+        gb.close()
+    assert (c_ref["key"] & np.uint64(0xFFFFFFFF) >= np.uint64(O.PLATE_KEY_BASE)).sum() > 0
+    assert saturated > 10
+    with pytest.raises(Exception):
+        gb2 = gpu_bed(bed, dt=1e-5, n_iter=30)
+        try:
+            p2 = gb2.add_plate(lo, hi, (0.015, 0.015, top), 0.02)
+            gb2.drive_plate(p2, 0, 1, 0.1, 0.0, 1.0, -1.0)          # f_min > f_max: DEM_ERR_INVALID
+        finally:
+            gb2.close()

@@ -549,3 +549,45 @@ def test_kinematic_and_force_driven_plate(oracle_mod):
     assert W.plates[0].force[2] == pytest.approx(F0, rel=0.01)
     f = {int(k) & 0xFFFFFFFF: c["P"][i, 0] / h for i, k in enumerate(c["key"])}
     assert f[oracle_mod.WALL_KEY_BASE + 4] == pytest.approx(F0 + m * 9.81, rel=0.01)
+
+
+def test_motor_force_limits(oracle_mod):
+    """Eq. 4 on a plate motor, staggered reading R18: a force-limited velocity axis
+    accelerates a free plate at f_max/m (staggered: x_n = x_0 + a h^2 n(n-1)/2) until it reaches
+    u, then holds u with zero motor force; a locked plate under a resting sphere carries its weight;
+    a press whose motor saturates at f_min reduces to a force axis (static balance F_p = -f_min)."""
+    r, h = 4.25e-3, 1e-4
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    p = oracle_mod.make_params(h=h, n_it=20, E=1e9, nu=0.15, rho=2200.0)
+    for sgn in (1.0, -1.0):
+        u, F, m = 0.1 * sgn, 0.1, 0.05
+        a = F / m
+        P = oracle_mod.make_plate([(-0.01, -0.01, 0.0)], [(0.01, 0.01, 0.005)], pos=(0.5, 0.5, 0.5), mass=m)
+        P.mode[0], P.target[0], P.limit[0] = 1, u, 1
+        P.fmin[0], P.fmax[0] = (-math.inf, F) if sgn > 0 else (-F, math.inf)
+        W = oracle_mod.OracleWorld([[0, 0, r]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], walls=floor, plates=[P])
+        x0 = W.plates[0].pos[0]
+        for n in range(1, 401):
+            W.step(p)
+            assert W.plates[0].pos[0] - x0 == pytest.approx(sgn * a * h * h * n * (n - 1) / 2, rel=1e-12, abs=2.5e-16 * n)
+            assert W.plates[0].motor[0] == sgn * F
+        W.step(p, 200)
+        assert W.plates[0].vel[0] == u and W.plates[0].motor[0] == 0.0
+    # locked plate as the floor under a resting sphere: the motor carries m g (upward)
+    P = oracle_mod.make_plate([(-0.01, -0.01, -0.005)], [(0.01, 0.01, 0.0)], pos=(0, 0, 0), mass=0.05)
+    W = oracle_mod.OracleWorld([[0, 0, r]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], plates=[P])
+    W.step(p, 300)
+    mp, _ = oracle_mod.mass_inertia(2 * r, 2200.0)
+    assert W.plates[0].force[2] == pytest.approx(-mp * 9.81, rel=0.01)
+    assert W.plates[0].motor[2] == pytest.approx(mp * 9.81, rel=0.01)
+    # a press at -0.05 m/s limited to f_min = -F0 balances like a force axis of -F0
+    F0 = 2.0
+    P = oracle_mod.make_plate([(-0.01, -0.01, 0.0)], [(0.01, 0.01, 0.005)], pos=(0, 0, 2 * r - 1e-6), mass=0.05)
+    P.mode[2], P.target[2], P.limit[2], P.fmin[2], P.fmax[2] = 1, -0.05, 1, -F0, math.inf
+    W = oracle_mod.OracleWorld([[0, 0, r]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], walls=floor, plates=[P])
+    p = oracle_mod.make_params(h=h, n_it=50, E=1e9, nu=0.15, rho=2200.0)
+    c, _, _ = W.step(p, 1500)
+    assert W.plates[0].motor[2] == -F0
+    assert W.plates[0].force[2] == pytest.approx(F0, rel=0.01)
+    f = {int(k) & 0xFFFFFFFF: c["P"][i, 0] / h for i, k in enumerate(c["key"])}
+    assert f[oracle_mod.WALL_KEY_BASE + 4] == pytest.approx(F0 + mp * 9.81, rel=0.01)

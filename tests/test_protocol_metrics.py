@@ -109,7 +109,7 @@ class StandInBed:
         self.dt, self.t, self.cmds, self.contact = dt, 0.0, [], contact
         self.z, self.x, self.mode = 0.0, 0.0, {}
 
-    def drive_plate(self, plate, axis, mode, target, ramp_time=0.0):
+    def drive_plate(self, plate, axis, mode, target, ramp_time=0.0, f_min=-np.inf, f_max=np.inf):
         self.cmds.append((round(self.t / self.dt), axis, mode, target, ramp_time))
         self.mode[axis] = (mode, target, ramp_time, self.t)
 
@@ -124,7 +124,7 @@ class StandInBed:
     def get_plate(self, plate):
         F = -self.mode[2][1]
         return {"pos": [self.x, 0.0, self.z], "vel": [0, 0, 0], "force": [-0.3 * F, 0.0, F],
-                "n_contacts": self.contact(self.t)}
+                "motor_force": [0.3 * F, 0.0, -F], "n_contacts": self.contact(self.t)}
 
 
 def test_run_plate_test_phase_logic():
@@ -143,6 +143,7 @@ def test_run_plate_test_phase_logic():
     # the horizontal axis is locked in phase I and switched to the velocity ramp at t_I_end
     shear = [c for c in bed.cmds if c[1] == 0]
     assert shear[0][2] == AXIS_LOCKED and shear[-1] == (200, 0, AXIS_VELOCITY, 0.1, 0.005)
+    assert len(bed.cmds) == 1 + 200 + 1 + 1
     assert np.allclose(sr["traction"][150:], 0.3)
     m = PR.extract_metrics(sr, proto)
     assert m["avg_traction"] == pytest.approx(0.3)
