@@ -180,6 +180,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no baseline, no clocks")
+    ap.add_argument("--reduction", default="canonical", choices=["canonical", "contiguous"],
+                    help="per-particle sum of the Jacobi sweep: canonical (default; bit-identical for any number of "
+                         "GPUs) or contiguous (slightly faster; rounding depends on the decomposition)")
     ap.add_argument("--ordering", default="jacobi", choices=["jacobi", "gs"],
                     help="contact-solve ordering: Jacobi with mass splitting (default) or coloured Gauss-Seidel")
     ap.add_argument("--decompose", action="store_true",
@@ -217,7 +220,8 @@ def main():
     N_total = dem.generator_count(gen, box)
     if args.settle > 0:
         bed.step(args.settle)             # coarse relaxation of the jammed packing (not timed)
-    bed.set_solver(dt=w["dt"], n_iter=n_it, ordering=1 if args.ordering == "gs" else 0)
+    bed.set_solver(dt=w["dt"], n_iter=n_it, ordering=1 if args.ordering == "gs" else 0,
+                   reduction=0 if args.reduction == "canonical" else 1)
     for _ in range(args.warmup):
         bed.step(1)
     stream = bed.stream
@@ -274,7 +278,8 @@ def main():
                    if (world > 1 or args.decompose) else "single GPU",
                    "l2": "inputs larger than L2 (no flush needed)",
                    "precision": "fp64 state and row math; fp64 normals/rows, fp32 impulses",
-                   "ordering": "coloured Gauss-Seidel" if args.ordering == "gs" else "Jacobi (mass splitting)"},
+                   "ordering": "coloured Gauss-Seidel" if args.ordering == "gs" else "Jacobi (mass splitting)",
+                   "reduction": args.reduction},
         "contacts_per_s": contacts_per_s,
         "contact_sweeps_per_s": tm["contact_sweeps"] / (ms / 1e3) * world,   # rank-local contacts (incl. ghost copies)
         "roofline": {"bound": "hbm", "kernel": "k_gs_color (all colours of a sweep)" if args.ordering == "gs" else "k_sweep_t2", "achieved": achieved, "peak": hbm, "unit": "GB/s",

@@ -74,6 +74,13 @@ typedef struct {
                                   contacts coloured greedily in SplitMix64(key) priority, swept colour
                                   by colour with the real masses (single undecomposed context only) */
     double skin;               /* Verlet skin [m] of the candidate list; <= 0 -> 0.1 r_min */
+    int32_t reduction;         /* per-particle sum of the Jacobi sweep: 0 (default) canonical -- each
+                                  particle's contributions, ordered by partner gid, summed by a tree
+                                  that depends only on its own list, so trajectories are bit-identical
+                                  for any number of GPUs/slabs; 1 contiguous -- ~4 %
+                                  faster sweep (no packing holes), bit-reproducible run to run, but the
+                                  rounding of the sums depends on the decomposition */
+    int32_t pad1;
 } dem_solver;
 
 /* Container: axis-aligned box; wall w = 2*axis + side (0:-x 1:+x 2:-y 3:+y 4:-z 5:+z). */

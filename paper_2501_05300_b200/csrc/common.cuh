@@ -23,6 +23,20 @@
 #define PARTNER_EXT 0x80000000u          // partner is not a particle
 #define PARTNER_PLATE 0x00000100u        // ext code: plate box = EXT|PLATE|(p<<4)|b ; wall = EXT|w
 #define B_SIDE 0x80000000u               // incidence entry: this particle is body b of the contact
+#define INC_CMASK 0x7FFFFFFFu            // incidence entry: contact index bits
+#define CCAND_FLIP 0x80000000u           // ccand entry: the contact's (a, b) is its candidate (j, i)
+
+// Canonical orientation of a particle pair: body a = the smaller gid, so every
+// decomposition evaluates a contact with the same operands in the same order.
+__device__ __forceinline__ bool cand_flip(uint2 ij, const uint32_t *__restrict__ gid)
+{
+    return !(ij.y & PARTNER_EXT) && gid[ij.y] < gid[ij.x];
+}
+// sort key of an incidence partner: its gid; boundary bodies after all particles, by code
+__device__ __forceinline__ uint64_t partner_key(uint32_t p, const uint32_t *__restrict__ gid)
+{
+    return (p & PARTNER_EXT) ? (1ull << 32) + (p & ~PARTNER_EXT) : (uint64_t)gid[p];
+}
 #define WALL_KEY_BASE 0xFFFFFFF0u        // public key of wall w: 2^32-16+w
 #define PLATE_KEY_BASE 0xFFFFF000u       // public key of plate p box b: 2^32-4096+16p+b
 #define FIXED_SCALE 1099511627776.0      // 2^40: int64 fixed point for plate impulse sums

@@ -77,6 +77,11 @@ struct dem_ctx {
     uint32_t *ccand = nullptr;
     // incidence
     uint32_t *inc_cnt = nullptr, *inc_start = nullptr, *order = nullptr;
+    // packed incidence of the canonical reduction (solver.reduction == 0; sweep_t2.cu)
+    uint32_t *pk_off = nullptr, *pk_start = nullptr, *pk_wsize = nullptr, *pk_wbase = nullptr;
+    uint2 *pk_inc = nullptr;
+    int64_t pk_cap = 0, pk_n = 0;
+    PackedInc pkv{};
     uint2 *inc = nullptr;
     // history
     int64_t nh = 0, cap_h = 0;
@@ -118,6 +123,7 @@ struct dem_ctx {
 };
 
 // ------------------------------------------------------------------ helpers
+#define PKV(ctx) ((ctx)->sol.reduction == 0 && (ctx)->pk_n ? &(ctx)->pkv : nullptr)
 #define OWN(ctx) ((ctx)->tp ? (const uint8_t *)(ctx)->own : (const uint8_t *)nullptr)
 #define CK(call)                                                                      \
     do {                                                                              \
@@ -252,6 +258,16 @@ static dem_status setup_levels(dem_ctx *ctx, const std::vector<double> &r)
     // ghost band: any partner of an owned particle within r_a + r_b + skin, plus one skin of margin
     // so that pairs about to meet carry their history across the faces
     ctx->band_w = 2.0 * rmax + 2.0 * ctx->grid.skin;
+    if (ctx->tp) {
+        // ghosts come from the two neighbouring slabs only: an interior slab must be at least one
+        // band wide (decided collectively, so every rank fails the create together)
+        double thin = (ctx->rank > 0 && ctx->rank < ctx->G - 1 && ctx->slab_hi - ctx->slab_lo < ctx->band_w) ? 1.0 : 0.0;
+        if (!ctx->tp->allreduce_f64(&thin, 1, 1, ctx->s, ctx->err)) return DEM_ERR_NCCL;
+        if (thin > 0.0) {
+            ctx->err = "an interior slab is thinner than the ghost band 2 r_max + 2 skin";
+            return DEM_ERR_INVALID;
+        }
+    }
     return DEM_OK;
 }
 
@@ -283,7 +299,8 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
     double4 **d4[] = {&ctx->pos, &ctx->pos2, &ctx->vel[0], &ctx->vel[1], &ctx->ang[0], &ctx->ang[1], &ctx->vel2,
                       &ctx->ang2, &ctx->xref, &ctx->pos_prev, &ctx->vel_prev, &ctx->ang_prev};
     uint32_t **u4[] = {&ctx->gid, &ctx->gid2, &ctx->gid_sorted, &ctx->co_start, &ctx->ct_cnt, &ctx->ct_start,
-                       &ctx->ct_cursor, &ctx->inc_cnt, &ctx->inc_start, &ctx->order};
+                       &ctx->ct_cursor, &ctx->inc_cnt, &ctx->inc_start, &ctx->order, &ctx->pk_off, &ctx->pk_start,
+                       &ctx->pk_wsize, &ctx->pk_wbase};
     const size_t N = (size_t)cap + 1;
     for (auto q : d4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N)); }
     for (auto q : u4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N + 1)); }
@@ -669,6 +686,7 @@ static dem_status rebuild(dem_ctx *ctx)
     uint32_t ncand = 0;
     CK(cudaMemcpyAsync(&ncand, ctx->co_start + N, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (ncand >= CCAND_FLIP) { ctx->err = "more than 2^31 contact candidates on one rank"; return DEM_ERR_OOM; }
     TRY(ensure_cand(ctx, std::max<int64_t>(ncand, 1)));
     ctx->ncand = ncand;
     if (N) {
@@ -691,6 +709,26 @@ static dem_status rebuild(dem_ctx *ctx)
 }
 
 // ------------------------------------------------------------------ one step
+// canonical reduction: pack each warp's half-contact lists into 32-lane chunks (sweep_t2.cu)
+static dem_status pack_incidence(dem_ctx *ctx, int64_t N)
+{
+    cudaStream_t s = ctx->s;
+    const int64_t nw = (N + 31) / 32;
+    pack_plan(N, ctx->inc_start, ctx->pk_off, ctx->pk_wsize, ctx->pk_wbase, ctx->scan_tmp, s, &ctx->launches);
+    uint32_t np = 0;
+    CK(cudaMemcpyAsync(&np, ctx->pk_wbase + nw, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if ((int64_t)np > ctx->pk_cap) {
+        const int64_t cap = std::max<int64_t>((int64_t)np + np / 4, 1024);
+        TRY(regrow(ctx, &ctx->pk_inc, cap));
+        ctx->pk_cap = cap;
+    }
+    ctx->pk_n = np;
+    pack_fill(N, ctx->inc_start, ctx->inc, ctx->pk_off, ctx->pk_wbase, ctx->pk_start, ctx->pk_inc, np, s, &ctx->launches);
+    ctx->pkv = PackedInc{ctx->pk_inc, ctx->pk_start, ctx->pk_wbase};
+    return DEM_OK;
+}
+
 static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
 {
     cudaStream_t s = ctx->s;
@@ -718,12 +756,14 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     CK(cudaMemcpyAsync(ctx->hnc, ctx->cscan + ncand, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     nc = *ctx->hnc;
+    if (nc > INC_CMASK) { ctx->err = "more than 2^31 contacts on one rank"; return DEM_ERR_OOM; }
     ctx->nc = nc;
     launch_compact(ncand, ctx->cand, ctx->cflag, ctx->cscan, ctx->pos, ctx->db, sp, ctx->Pca, ctx->Pcb, ctx->cij,
-                   ctx->geo, ctx->row, ctx->cdel, ctx->Pwa, ctx->Pwb, ctx->ccand, ctx->dsc, s);
+                   ctx->geo, ctx->row, ctx->cdel, ctx->Pwa, ctx->Pwb, ctx->ccand, ctx->gid, ctx->dsc, s);
     launch_count_kinds(nc, OWN(ctx), ctx->cij, ctx->gid, ctx->dsc, s);
-    launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->inc_cnt,
+    launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->gid, ctx->inc_cnt,
                ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
+    if (ctx->sol.reduction == 0 && ctx->sol.ordering == 0) TRY(pack_incidence(ctx, N));
     launch_prepare(N, ctx->inc_start, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], sp.rho, s);
     TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));      // ghosts' weights c/m, c/I from their owners
     if (sweep_uses_order()) launch_tile_order(N, ctx->inc_start, ctx->order, s);
@@ -765,7 +805,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         for (int it = 0; it < n_imp; it++) {
             const int pi = it & 1;
             launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
-                         ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row_imp, ctx->Pa[pi],
+                         ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row_imp, ctx->Pa[pi],
                          ctx->Pb[pi], ctx->Pa[pi ^ 1], ctx->Pb[pi ^ 1], ctx->db, sp, s);
             ctx->cur ^= 1;
             TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
@@ -778,7 +818,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     // main stage: SPOOK rows, gravity + warm start, N_it Jacobi sweeps
     launch_rows(nc, 1, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
     launch_sweep(SWEEP_MODE_APPLY, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
-                 ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, nullptr,
+                 ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, nullptr,
                  nullptr, ctx->db, sp, s);
     ctx->cur ^= 1;
     ctx->launches += 2;
@@ -801,7 +841,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     for (int it = 0; it < (gs ? 0 : n_it); it++) {
         P4 *oa = ctx->Pa[it & 1], *ob = ctx->Pb[it & 1];
         launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
-                     ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
+                     ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
                      ctx->db, sp, s);
         ctx->cur ^= 1;
         TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
@@ -981,7 +1021,8 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
     if (desc->struct_size != sizeof(dem_bed_desc)) { g_create_err = "dem_bed_desc struct_size mismatch"; return DEM_ERR_INVALID; }
     if (!valid_material(desc->mat)) { g_create_err = "invalid material"; return DEM_ERR_INVALID; }
     const dem_solver &so = desc->solver;
-    if (!(so.dt > 0) || so.n_iter < 1 || !(so.ordering == 0 || so.ordering == 1) || !(so.hertz_exp == 1.25 || so.hertz_exp == 1.0) ||
+    if (!(so.dt > 0) || so.n_iter < 1 || !(so.ordering == 0 || so.ordering == 1) || !(so.reduction == 0 || so.reduction == 1) ||
+        !(so.hertz_exp == 1.25 || so.hertz_exp == 1.0) ||
         (so.hertz_exp == 1.0 && !(so.k_lin > 0)) || so.damping_steps < 0) {
         g_create_err = "invalid solver settings (dt > 0, n_iter >= 1, hertz_exp 1.25 or 1 with k_lin > 0)";
         return DEM_ERR_INVALID;
@@ -1085,7 +1126,8 @@ dem_status dem_step(dem_ctx *ctx, int32_t n_steps, dem_step_report *last)
 
 static bool valid_solver(const dem_solver &so)
 {
-    return (so.ordering == 0 || so.ordering == 1) && so.dt > 0 && so.n_iter >= 1 && (so.hertz_exp == 1.25 || so.hertz_exp == 1.0) &&
+    return (so.ordering == 0 || so.ordering == 1) && (so.reduction == 0 || so.reduction == 1) && so.dt > 0 &&
+           so.n_iter >= 1 && (so.hertz_exp == 1.25 || so.hertz_exp == 1.0) &&
            !(so.hertz_exp == 1.0 && !(so.k_lin > 0)) && so.damping_steps >= 0;
 }
 
@@ -1219,7 +1261,7 @@ dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device)
     if (!N) return DEM_OK;
     cudaStream_t s = ctx->s;
     launch_sweep(SWEEP_MODE_FORCES, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
-                 ctx->inc, ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, nullptr, nullptr, ctx->db, ctx->sp, s);
+                 ctx->inc, PKV(ctx), ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, nullptr, nullptr, ctx->db, ctx->sp, s);
     double *d = nullptr;
     TRY(A(ctx, &d, 6 * N));
     launch_to_gid_order(N, Nown, OWN(ctx), ctx->gid, ctx->gid_sorted, ctx->vel2, ctx->ang2, nullptr, d, d + 3 * Nown, nullptr, nullptr,
@@ -1437,7 +1479,7 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
             double4 *vo = vbuf[it & 1], *wo = wbuf[it & 1];
             if (var < 10 || (var >= 40 && var < 50)) {
                 set_sweep_variant(var);
-                launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, vi, wi, vo, wo, ctx->inc_start, ctx->inc, ctx->geo, ctx->row,
+                launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, vi, wi, vo, wo, ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row,
                              pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
             } else if (var == 50) {
                 launch_sweep9(N, caps9[0], caps9[1], caps9[2], vi, wi, vo, wo, ca6, xs6, xl9, ctx->inc_start, ctx->inc, ctx->cij,

@@ -306,12 +306,14 @@ __global__ void k_compact(int64_t nc, const uint2 *__restrict__ cand, const uint
                           const DevBoundary *__restrict__ bnd, SolveParams sp, const P4 *__restrict__ Pca,
                           const P4 *__restrict__ Pcb, uint2 *__restrict__ cij, G4 *__restrict__ geo,
                           R4 *__restrict__ row, double *__restrict__ cdel, P4 *__restrict__ Pa, P4 *__restrict__ Pb,
-                          uint32_t *__restrict__ ccand, StepScalars *sc)
+                          uint32_t *__restrict__ ccand, const uint32_t *__restrict__ gid, StepScalars *sc)
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= nc || !flag[k]) return;
     const uint32_t c = scan[k];
-    const uint2 ij = cand[k];
+    // canonical orientation: a = smaller gid (the candidate may hold the pair either way)
+    const bool flip = cand_flip(cand[k], gid);
+    const uint2 ij = flip ? make_uint2(cand[k].y, cand[k].x) : cand[k];
     d3 n;
     double delta;
     contact_geom(ij, pos, bnd, n, delta);
@@ -326,9 +328,11 @@ __global__ void k_compact(int64_t nc, const uint2 *__restrict__ cand, const uint
     geo[c] = gf;
     row[c] = mkR4(0, 0, ra - 0.5 * delta, ext ? 0.0 : rb - 0.5 * delta);
     cdel[c] = delta;
-    ccand[c] = (uint32_t)k;
+    ccand[c] = (uint32_t)k | (flip ? CCAND_FLIP : 0u);
     // warm start (reading R12): re-project P_t onto the new tangent plane, clamp cones
-    const P4 A = Pca[k], B = Pcb[k];
+    // (candidate-slot impulses are kept in candidate orientation: flip to canonical)
+    P4 A = Pca[k], B = Pcb[k];
+    if (flip) { A.y = -A.y; A.z = -A.z; A.w = -A.w; B.x = -B.x; B.y = -B.y; B.z = -B.z; }
     const d3 nf = mk(gf.x, gf.y, gf.z);
     double Pn = A.x > 0 ? (double)A.x : 0.0;
     d3 Pt = mk(A.y, A.z, A.w), Pr = mk(B.x, B.y, B.z);
@@ -378,20 +382,31 @@ __global__ void k_inc_count(int64_t N, const uint32_t *__restrict__ co_start, co
     cnt[i] = c;
 }
 
+// A particle's half-contacts in the order of their partners' gids (boundary bodies last): the
+// per-particle reduction order is then the same in every decomposition.
 __global__ void k_inc_fill(int64_t N, const uint32_t *__restrict__ co_start, const uint2 *__restrict__ cand,
                            const uint32_t *__restrict__ scan, const uint32_t *__restrict__ ct_start,
                            const uint32_t *__restrict__ ct_list, const uint32_t *__restrict__ flag,
-                           const uint32_t *__restrict__ inc_start, uint2 *__restrict__ inc)
+                           const uint32_t *__restrict__ gid, const uint32_t *__restrict__ inc_start,
+                           uint2 *__restrict__ inc)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    uint32_t o = inc_start[i];
-    for (uint32_t t = ct_start[i]; t < ct_start[i + 1]; t++) {
+    const uint32_t s = inc_start[i];
+    uint32_t o = s;
+    for (uint32_t t = ct_start[i]; t < ct_start[i + 1]; t++) {       // i is the candidate's j
         const uint32_t k = ct_list[t];
-        if (flag[k]) inc[o++] = make_uint2(scan[k] | B_SIDE, cand[k].x);
+        if (flag[k]) inc[o++] = make_uint2(scan[k] | (cand_flip(cand[k], gid) ? 0u : B_SIDE), cand[k].x);
     }
-    for (uint32_t k = co_start[i]; k < co_start[i + 1]; k++)
-        if (flag[k]) inc[o++] = make_uint2(scan[k], cand[k].y);
+    for (uint32_t k = co_start[i]; k < co_start[i + 1]; k++)        // i is the candidate's i
+        if (flag[k]) inc[o++] = make_uint2(scan[k] | (cand_flip(cand[k], gid) ? B_SIDE : 0u), cand[k].y);
+    for (uint32_t a = s + 1; a < o; a++) {                           // insertion sort by partner
+        const uint2 v = inc[a];
+        const uint64_t kv = partner_key(v.y, gid);
+        uint32_t b = a;
+        while (b > s && partner_key(inc[b - 1].y, gid) > kv) { inc[b] = inc[b - 1]; b--; }
+        inc[b] = v;
+    }
 }
 
 // ------------------------------------------------------------------ output helpers
@@ -478,17 +493,18 @@ void launch_narrow(int64_t nc, const uint2 *cand, const double4 *pos, const DevB
 { if (nc) k_narrow<<<GRID(nc)>>>(nc, cand, pos, bnd, flag, Pa, Pb, sc); }
 void launch_compact(int64_t nc, const uint2 *cand, const uint32_t *flag, const uint32_t *scan, const double4 *pos,
                     const DevBoundary *bnd, const SolveParams &sp, const P4 *Pca, const P4 *Pcb, uint2 *cij,
-                    G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, StepScalars *sc, cudaStream_t s)
-{ if (nc) k_compact<<<GRID(nc)>>>(nc, cand, flag, scan, pos, bnd, sp, Pca, Pcb, cij, geo, row, cdel, Pa, Pb, ccand, sc); }
+                    G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, const uint32_t *gid, StepScalars *sc,
+                    cudaStream_t s)
+{ if (nc) k_compact<<<GRID(nc)>>>(nc, cand, flag, scan, pos, bnd, sp, Pca, Pcb, cij, geo, row, cdel, Pa, Pb, ccand, gid, sc); }
 void launch_count_kinds(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, StepScalars *sc, cudaStream_t s)
 { if (nc) k_count_kinds<<<GRID(nc)>>>(nc, own, cij, gid, sc); }
 void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const uint32_t *scan, const uint32_t *ct_start,
-                const uint32_t *ct_list, const uint32_t *flag, uint32_t *cnt, uint32_t *inc_start, uint2 *inc,
-                void *scan_tmp, cudaStream_t s, long long *launches)
+                const uint32_t *ct_list, const uint32_t *flag, const uint32_t *gid, uint32_t *cnt, uint32_t *inc_start,
+                uint2 *inc, void *scan_tmp, cudaStream_t s, long long *launches)
 {
     if (N) k_inc_count<<<GRID(N)>>>(N, co_start, scan, ct_start, ct_list, flag, cnt);
     scan_u32(cnt, inc_start, N, scan_tmp, s, launches);
-    if (N) k_inc_fill<<<GRID(N)>>>(N, co_start, cand, scan, ct_start, ct_list, flag, inc_start, inc);
+    if (N) k_inc_fill<<<GRID(N)>>>(N, co_start, cand, scan, ct_start, ct_list, flag, gid, inc_start, inc);
     *launches += 2;
 }
 void launch_contact_keys(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, uint64_t *keys, uint32_t *vals,

@@ -69,7 +69,7 @@ __global__ void k_gs_round(int64_t nc, const uint2 *__restrict__ cij, const uint
     for (int q = 0; q < nb; q++) {
         const uint32_t s = inc_start[body[q]], e = inc_start[body[q] + 1];
         for (uint32_t k = s; k < e; k++) {
-            const uint32_t o = inc[k].x & ~B_SIDE;
+            const uint32_t o = inc[k].x & INC_CMASK;
             if (o == (uint32_t)c) continue;
             const int co = vcol[o];
             if (co < 0) {

@@ -26,11 +26,12 @@ void launch_narrow(int64_t nc, const uint2 *cand, const double4 *pos, const DevB
                    P4 *Pa, P4 *Pb, StepScalars *sc, cudaStream_t s);
 void launch_compact(int64_t nc, const uint2 *cand, const uint32_t *flag, const uint32_t *scan, const double4 *pos,
                     const DevBoundary *bnd, const SolveParams &sp, const P4 *Pca, const P4 *Pcb, uint2 *cij,
-                    G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, StepScalars *sc, cudaStream_t s);
+                    G4 *geo, R4 *row, double *cdel, P4 *Pa, P4 *Pb, uint32_t *ccand, const uint32_t *gid, StepScalars *sc,
+                    cudaStream_t s);
 void launch_count_kinds(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, StepScalars *sc, cudaStream_t s);
 void launch_inc(int64_t N, const uint32_t *co_start, const uint2 *cand, const uint32_t *scan, const uint32_t *ct_start,
-                const uint32_t *ct_list, const uint32_t *flag, uint32_t *cnt, uint32_t *inc_start, uint2 *inc,
-                void *scan_tmp, cudaStream_t s, long long *launches);
+                const uint32_t *ct_list, const uint32_t *flag, const uint32_t *gid, uint32_t *cnt, uint32_t *inc_start,
+                uint2 *inc, void *scan_tmp, cudaStream_t s, long long *launches);
 void launch_contact_keys(int64_t nc, const uint8_t *own, const uint2 *cij, const uint32_t *gid, uint64_t *keys, uint32_t *vals,
                          unsigned int *cnt, cudaStream_t s);
 void launch_contact_out(int64_t nc, const uint32_t *vals, const uint2 *cij, const uint32_t *gid, const G4 *geo,
@@ -43,8 +44,20 @@ void launch_prepare(int64_t N, const uint32_t *inc_start, const double4 *pos, do
 void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const double *cdel, R4 *row, R4 *row_imp,
                  const double4 *vel, const double4 *pos, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
                  cudaStream_t s);
+// packed incidence of the canonical reduction (sweep_t2.cu): entries in 32-lane chunks, start[i]
+// = packed position of particle i's list, wbase[g] = first packed entry of warp g's particles
+struct PackedInc {
+    const uint2 *inc;
+    const uint32_t *start;
+    const uint32_t *wbase;
+};
+void pack_plan(int64_t N, const uint32_t *inc_start, uint32_t *off_local, uint32_t *wsize, uint32_t *wbase,
+               void *scan_tmp, cudaStream_t s, long long *launches);
+void pack_fill(int64_t N, const uint32_t *inc_start, const uint2 *inc, const uint32_t *off_local, const uint32_t *wbase,
+               uint32_t *pstart, uint2 *pinc, int64_t npacked, cudaStream_t s, long long *launches);
 void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin, const double4 *win, double4 *vout,
-                  double4 *wout, const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
+                  double4 *wout, const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo,
+                  const R4 *row,
                   const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
 bool sweep_uses_order();
@@ -94,9 +107,9 @@ void launch_sweep8(int64_t N, unsigned max_slots, const double4 *vin, const doub
                    const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
 // sweep_t2.cu: tile sweep with 256-bit records and conflict-free shared staging
 void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
-                     const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row, const P4 *Pa_in,
-                     const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp,
-                     cudaStream_t s);
+                     const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo, const R4 *row,
+                     const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd,
+                     const SolveParams &sp, cudaStream_t s);
 // sweep9.cu: staged tile sweep (each contact once per tile, cp.async staging, reduction from increments)
 void launch_inc9(int64_t N, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start, const uint2 *inc,
                  uint32_t *ca, uint32_t *xcnt, uint32_t *xstart, uint4 *xlist, unsigned int *caps, void *scan_tmp,

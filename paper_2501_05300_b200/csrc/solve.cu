@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(TP, SWEEP_MINB) k_sweep_tile(int64_t N, const 
                 // chunk computes; incidence two chunks ahead in registers
                 ent_next = ent_nn;
                 if (kb + 32 + lane < k1) {
-                    const uint32_t c2 = ent_next.x & ~B_SIDE, p2 = ent_next.y;
+                    const uint32_t c2 = ent_next.x & INC_CMASK, p2 = ent_next.y;
                     pf_l1(&geo[c2]); pf_l1(&row[c2]); pf_l1(&Pa_in[c2]); pf_l1(&Pb_in[c2]);
                     if (!(p2 & PARTNER_EXT)) {
                         const int64_t pl = (int64_t)p2 - p0;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(TP, SWEEP_MINB) k_sweep_tile(int64_t N, const 
             double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
             if (valid) {
                 const int o = lo_p + owner;
-                const uint32_t c = ent.x & ~B_SIDE;
+                const uint32_t c = ent.x & INC_CMASK;
                 const bool isB = (ent.x & B_SIDE) != 0;
                 const uint32_t p = ent.y;
                 const double4 *pPV, *pPW;
@@ -292,7 +292,7 @@ __device__ __forceinline__ void issue_stage(Stage &S, int lane, bool valid, uint
                                             const double4 *__restrict__ win)
 {
     if (!valid) return;
-    const uint32_t c = ent.x & ~B_SIDE, p = ent.y;
+    const uint32_t c = ent.x & INC_CMASK, p = ent.y;
     cpT(&S.geo[lane], &geo[c]);
     cpT(&S.row[lane], &row[c]);
     cpT(&S.pa[lane], &Pa[c]);
@@ -376,7 +376,7 @@ __global__ void __launch_bounds__(TPP, SWEEP_MINB_PIPE) k_sweep_pipe(int64_t N, 
                 const HalfOut r = half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt,
                                                S.geo[lane], S.row[lane], S.pa[lane], S.pb[lane], sp.rolling_dims);
                 if (!isB) {
-                    const uint32_t c = entA.x & ~B_SIDE;
+                    const uint32_t c = entA.x & INC_CMASK;
                     Pa_out[c] = r.Pa;
                     Pb_out[c] = r.Pb;
                 }
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(TPT, SWEEP_MINB_PPT) k_sweep_ppt(int64_t N, co
     for (uint32_t k = s; k < e; k++) {
         const uint2 ent = ent_next;
         if (k + 1 < e) ent_next = inc[k + 1];
-        const uint32_t c = ent.x & ~B_SIDE;
+        const uint32_t c = ent.x & INC_CMASK;
         const bool isB = (ent.x & B_SIDE) != 0;
         const uint32_t p = ent.y;
         double4 VP, WP;
@@ -516,7 +516,7 @@ __global__ void k_apply(int64_t N, const double4 *__restrict__ vin, const double
     d3 aL = mk(0, 0, 0), aA = mk(0, 0, 0);
     for (uint32_t k = s; k < e; k++) {
         const uint2 ent = inc[k];
-        const uint32_t c = ent.x & ~B_SIDE;
+        const uint32_t c = ent.x & INC_CMASK;
         const bool isB = (ent.x & B_SIDE) != 0;
         const G4 g = geo[c];
         const R4 rw = row[c];
@@ -696,9 +696,12 @@ __global__ void k_scatter_P(int64_t nc, const uint32_t *__restrict__ ccand, cons
 {
     const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= nc) return;
-    const uint32_t k = ccand[c];
-    Pca[k] = Pa[c];
-    Pcb[k] = Pb[c];
+    // back to candidate orientation (k_compact flipped the pair to canonical)
+    const uint32_t kf = ccand[c], k = kf & ~CCAND_FLIP;
+    P4 a = Pa[c], b = Pb[c];
+    if (kf & CCAND_FLIP) { a.y = -a.y; a.z = -a.z; a.w = -a.w; b.x = -b.x; b.y = -b.y; b.z = -b.z; }
+    Pca[k] = a;
+    Pcb[k] = b;
 }
 
 // sorted order -> ascending-gid order (rank of gid in the sorted gid list)
@@ -748,7 +751,8 @@ void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const do
                  cudaStream_t s)
 { if (nc) k_rows<<<GRID(nc)>>>(nc, mode, cij, geo, cdel, row, row_imp, vel, pos, bnd, sp, sc); }
 void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin, const double4 *win, double4 *vout,
-                  double4 *wout, const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
+                  double4 *wout, const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo,
+                  const R4 *row,
                   const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s)
 {
@@ -764,8 +768,10 @@ void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin
         }
         k_sweep_pipe<<<(unsigned)((N + TPP - 1) / TPP), TPP, sizeof(PipeSmem), s>>>(
             N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
-    } else if (mode == SWEEP_MODE_SWEEP && g_sweep_variant == 0)
-        launch_sweep_t2(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp, s);
+    } else if (mode == SWEEP_MODE_SWEEP && (g_sweep_variant == 0 || g_sweep_variant == 7))
+        // 0: the context's reduction (packed canonical if pk, else contiguous); 7: contiguous
+        launch_sweep_t2(N, vin, win, vout, wout, inc_start, inc, g_sweep_variant == 7 ? nullptr : pk, geo, row, Pa_in,
+                        Pb_in, Pa_out, Pb_out, bnd, sp, s);
     else if (mode == SWEEP_MODE_SWEEP)
         (g_sweep_variant == 3 ? k_sweep_tile<true> : g_sweep_variant == 41 ? k_sweep_tile<false, 1> :
          g_sweep_variant == 42 ? k_sweep_tile<false, 2> : g_sweep_variant == 43 ? k_sweep_tile<false, 3> : k_sweep_tile<false>)<<<(unsigned)((N + TP - 1) / TP), TP, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, geo, row,

@@ -71,7 +71,7 @@ __device__ __forceinline__ void ld5(Ld5 &L, uint2 ent, const double4 *__restrict
                                     const double4 *__restrict__ win, const double *__restrict__ cb,
                                     const P4 *__restrict__ Pa, const P4 *__restrict__ Pb)
 {
-    const uint32_t c = ent.x & ~B_SIDE, p = ent.y;
+    const uint32_t c = ent.x & INC_CMASK, p = ent.y;
     L.b = cb[c];
     L.pa = Pa[c];
     L.pb = Pb[c];
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(T5, PF ? 3 : SWEEP5_MINB)
             uint2 ent_nn = make_uint2(0, 0);
             if (k + 1 < e) ld5(nxt, ent_n, pos, vin, win, cb, Pa_in, Pb_in);
             if (k + 2 < e) ent_nn = inc[k + 2];
-            const uint32_t c = ent.x & ~B_SIDE;
+            const uint32_t c = ent.x & INC_CMASK;
             const bool isB = (ent.x & B_SIDE) != 0;
             const HalfOut r = eval5<IMPACT>(X, V, W, cur.XP, cur.VP, cur.WP, isB, ent.y, cur.b, cur.pa, cur.pb, bnd, sp);
             if (!isB) {
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(T5, PF ? 3 : SWEEP5_MINB)
             const uint2 ent = inc[k];
             Ld5 L;
             ld5(L, ent, pos, vin, win, cb, Pa_in, Pb_in);
-            const uint32_t c = ent.x & ~B_SIDE;
+            const uint32_t c = ent.x & INC_CMASK;
             const bool isB = (ent.x & B_SIDE) != 0;
             const HalfOut r = eval5<IMPACT>(X, V, W, L.XP, L.VP, L.WP, isB, ent.y, L.b, L.pa, L.pb, bnd, sp);
             if (!isB) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(T5, SWEEP5T_MINB)
             double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
             if (valid) {
                 const int o = lo_p + owner;
-                const uint32_t c = ent.x & ~B_SIDE;
+                const uint32_t c = ent.x & INC_CMASK;
                 const bool isB = (ent.x & B_SIDE) != 0;
                 const uint32_t p = ent.y;
                 double4 XP, VP, WP;

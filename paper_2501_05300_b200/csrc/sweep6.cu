@@ -60,7 +60,7 @@ __global__ void k_inc6_fill(int64_t N, int tile, const uint32_t *__restrict__ in
     uint32_t o = xstart[i];
     for (uint32_t t = 0; t < nb; t++) {
         const uint2 e = inc[s + t];
-        const uint32_t c = e.x & ~B_SIDE;
+        const uint32_t c = e.x & INC_CMASK;
         bslot[c] = b0 + t;
         if ((int64_t)e.y / tile != ti) xlist[o++] = make_uint2(c, e.y);
     }
@@ -504,7 +504,7 @@ __global__ void k_inc8_fill(int64_t N, int tile, const uint32_t *__restrict__ in
     uint32_t o = xstart[i];
     for (uint32_t t = 0; t < nb; t++) {
         const uint2 e = inc[s + t];
-        const uint32_t c = e.x & ~B_SIDE;
+        const uint32_t c = e.x & INC_CMASK;
         bslot[c] = b0 + t;
         if ((int64_t)e.y / tile != ti) xlist[o++] = make_uint4(c, e.y, b0 + t, (uint32_t)(i - ti * tile));
     }

@@ -67,7 +67,7 @@ __global__ void k_inc9_fill(int64_t N, const uint32_t *__restrict__ inc_start, c
     uint32_t o = xstart[i];
     for (uint32_t t = 0; t < nb; t++) {
         const uint2 e = inc[s + t];
-        if ((int64_t)e.y / T9 != ti) xlist[o++] = make_uint4(e.x & ~B_SIDE, e.y, 0u, (uint32_t)(i - ti * T9));
+        if ((int64_t)e.y / T9 != ti) xlist[o++] = make_uint4(e.x & INC_CMASK, e.y, 0u, (uint32_t)(i - ti * T9));
     }
 }
 
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(NT9, SWEEP9_MINB)
         const uint32_t ib = sI[t] - sI[0];
         for (uint32_t j = 0; j < nb; j++) {
             const uint2 e = sInc[ib + j];
-            const uint32_t c = e.x & ~B_SIDE;
+            const uint32_t c = e.x & INC_CMASK;
             G4 g;
             double lb;
             P4 o, nw, ob, nb2;

@@ -19,9 +19,101 @@ constexpr int NWT = TT / 32;
 
 __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { return make_double4(a.x, a.y, b.x, b.y); }
 
+// ------------------------------------------------------------------ packed incidence
+// Canonical reduction (trajectories bit-identical for any number of slabs).  The
+// warp's segmented scan sums a particle's contributions with a tree that depends only on the
+// particle's own list -- as long as the list does not straddle a 32-entry chunk boundary.  Once
+// per step each warp's 32 particles are packed first-fit into 32-lane chunks so that no list of
+// <= 32 half-contacts straddles a boundary and a longer list starts on one (its pieces are then
+// cut at fixed offsets 32, 64, ... of its own list); unused lanes are holes (0xFFFFFFFF).  The
+// packing depends only on list lengths, the sums only on the lists (ordered by partner gid), so
+// every decomposition and warp grouping produces the same bits.
+constexpr uint32_t PK_HOLE = 0xFFFFFFFFu;
+
+// one warp per 32 consecutive particles (the sweep's warp grouping): first-fit packing
+__global__ void k_pack_plan(int64_t N, const uint32_t *__restrict__ inc_start, uint32_t *__restrict__ off_local,
+                            uint32_t *__restrict__ wsize)
+{
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (32 * g >= N) return;                               // whole warp
+    const int64_t i = 32 * g + lane;
+    const uint32_t L = i < N ? inc_start[i + 1] - inc_start[i] : 0u;
+    uint32_t my_off = 0, cap = 0, binno = 0;               // lane s: open slot s (capacity, bin)
+    uint32_t nb = 0, nslots = 0;
+    unsigned longs = __ballot_sync(0xffffffffu, L > 32u);
+    while (longs) {                                        // lists > 32 start on a chunk boundary
+        const int p = __ffs(longs) - 1;
+        const uint32_t Lp = __shfl_sync(0xffffffffu, L, p);
+        if (lane == p) my_off = 32u * nb;
+        nb += Lp / 32u;
+        if (Lp % 32u) {
+            if (lane == (int)nslots) { cap = 32u - Lp % 32u; binno = nb; }
+            nslots++;
+            nb++;
+        }
+        longs &= longs - 1;
+    }
+    unsigned shorts = __ballot_sync(0xffffffffu, L > 0u && L <= 32u);
+    while (shorts) {                                       // first fit, in particle order
+        const int p = __ffs(shorts) - 1;
+        const uint32_t Lp = __shfl_sync(0xffffffffu, L, p);
+        const unsigned fit = __ballot_sync(0xffffffffu, lane < (int)nslots && cap >= Lp);
+        uint32_t off;
+        if (fit) {
+            const int sl = __ffs(fit) - 1;
+            const uint32_t c = __shfl_sync(0xffffffffu, cap, sl), b = __shfl_sync(0xffffffffu, binno, sl);
+            off = 32u * b + (32u - c);
+            if (lane == sl) cap -= Lp;
+        } else {
+            off = 32u * nb;
+            if (lane == (int)nslots) { cap = 32u - Lp; binno = nb; }
+            nslots++;
+            nb++;
+        }
+        if (lane == p) my_off = off;
+        shorts &= shorts - 1;
+    }
+    if (i < N) off_local[i] = my_off;
+    if (lane == 0) wsize[g] = 32u * nb;
+}
+
+__global__ void k_pack_fill(int64_t N, const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
+                            const uint32_t *__restrict__ off_local, const uint32_t *__restrict__ wbase,
+                            uint32_t *__restrict__ pstart, uint2 *__restrict__ pinc)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const uint32_t ps = wbase[i >> 5] + off_local[i], s = inc_start[i], e = inc_start[i + 1];
+    pstart[i] = ps;
+    for (uint32_t k = s; k < e; k++) pinc[ps + (k - s)] = inc[k];
+}
+
+// packed size of the whole bed (host reads it to size pinc), then the fill
+void pack_plan(int64_t N, const uint32_t *inc_start, uint32_t *off_local, uint32_t *wsize, uint32_t *wbase,
+               void *scan_tmp, cudaStream_t s, long long *launches)
+{
+    const int64_t nw = (N + 31) / 32;
+    if (nw) k_pack_plan<<<(unsigned)((nw + 3) / 4), 128, 0, s>>>(N, inc_start, off_local, wsize);
+    scan_u32(wsize, wbase, nw, scan_tmp, s, launches);
+    *launches += 1;
+}
+void pack_fill(int64_t N, const uint32_t *inc_start, const uint2 *inc, const uint32_t *off_local, const uint32_t *wbase,
+               uint32_t *pstart, uint2 *pinc, int64_t npacked, cudaStream_t s, long long *launches)
+{
+    if (npacked) cudaMemsetAsync(pinc, 0xFF, npacked * sizeof(uint2), s);
+    if (N) k_pack_fill<<<(unsigned)((N + 255) / 256), 256, 0, s>>>(N, inc_start, inc, off_local, wbase, pstart, pinc);
+    *launches += 1;
+}
+
+// PACKED: the canonical reduction above (default); false: the contiguous CSR chunks (fastest
+// layout-independent of packing; bit-reproducible run to run but rounding depends on the warp
+// grouping, i.e. on the decomposition)
+template <bool PACKED>
 __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     k_sweep_t2(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win, double4 *__restrict__ vout,
                double4 *__restrict__ wout, const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
+               const uint32_t *__restrict__ pstart, const uint32_t *__restrict__ wbase,
                const G4 *__restrict__ geo, const R4 *__restrict__ row, const P4 *__restrict__ Pa_in,
                const P4 *__restrict__ Pb_in, P4 *__restrict__ Pa_out, P4 *__restrict__ Pb_out,
                const DevBoundary *__restrict__ bnd, SolveParams sp)
@@ -30,6 +122,7 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     __shared__ double sAcc[NWT][6][32];
     __shared__ uint8_t sOwn[NWT][32];
     __shared__ uint32_t sI[TT + 1];
+    __shared__ uint32_t sPS[PACKED ? TT : 1];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t p0 = (int64_t)blockIdx.x * TT;
     const int np = (int)min((int64_t)TT, N - p0);
@@ -39,21 +132,24 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
         sWa[t] = make_double2(o.x, o.y); sWb[t] = make_double2(o.z, o.w);
     }
     for (int q = t; q <= np; q += TT) sI[q] = inc_start[p0 + q];
+    if (PACKED && t < np) sPS[t] = pstart[p0 + t];
 #pragma unroll
     for (int f = 0; f < 6; f++) sAcc[w][f][lane] = 0.0;
     __syncthreads();
     const int lo_p = 32 * w, hi_p = min(32 * w + 32, np);
     const int me = lo_p + lane;
-    const uint32_t s_me = me < hi_p ? sI[me] : 0u, e_me = me < hi_p ? sI[me + 1] : 0u;
+    const uint32_t cnt_me = me < hi_p ? sI[me + 1] - sI[me] : 0u;
+    const uint32_t s_me = me < hi_p ? (PACKED ? sPS[me] : sI[me]) : 0u, e_me = s_me + cnt_me;
     if (lo_p < np) {
-        const uint32_t k0 = sI[lo_p], k1 = sI[hi_p];
+        const uint32_t k0 = PACKED ? wbase[(p0 >> 5) + w] : sI[lo_p];
+        const uint32_t k1 = PACKED ? wbase[(p0 >> 5) + w + 1] : sI[hi_p];
         uint2 ent_next = make_uint2(0, 0);
         if (k0 + lane < k1) ent_next = inc[k0 + lane];
         int carry = 0;
         for (uint32_t kb = k0; kb < k1; kb += 32) {
             const uint32_t k = kb + lane;
-            const bool valid = k < k1;
             const uint2 ent = ent_next;
+            const bool valid = k < k1 && (!PACKED || ent.x != PK_HOLE);
             if (kb + 32 + lane < k1) ent_next = inc[kb + 32 + lane];
             const bool starts = e_me > s_me && s_me >= kb && s_me < kb + 32;
             const unsigned smask = __reduce_or_sync(0xffffffffu, starts ? (1u << (s_me - kb)) : 0u);
@@ -65,7 +161,7 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
             double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
             if (valid) {
                 const int o = lo_p + owner;
-                const uint32_t c = ent.x & ~B_SIDE;
+                const uint32_t c = ent.x & INC_CMASK;
                 const bool isB = (ent.x & B_SIDE) != 0;
                 const uint32_t p = ent.y;
                 const G4 g = ld4g(&geo[c]);
@@ -87,7 +183,7 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                 const double4 VS = cat2(sVa[o], sVb[o]), WS = cat2(sWa[o], sWb[o]);
                 const HalfOut r = half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt, g, rw,
                                                pa, pb, sp.rolling_dims);
-                if (!isB) {
+                if (!isB) {   // both halves compute the same impulses; body a stores them
                     Pa_out[c] = r.Pa;
                     Pb_out[c] = r.Pb;
                 }
@@ -101,7 +197,10 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                 const double u4 = __shfl_up_sync(0xffffffffu, v4, d), u5 = __shfl_up_sync(0xffffffffu, v5, d);
                 if (lane - d >= sstart) { v0 += u0; v1 += u1; v2 += u2; v3 += u3; v4 += u4; v5 += u5; }
             }
-            const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1);
+            // holes only trail a chunk: a segment also ends before the first hole
+            const unsigned vmask = PACKED ? __ballot_sync(0xffffffffu, valid) : 0xffffffffu;
+            const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1 ||
+                                           (PACKED && !((vmask >> (lane + 1)) & 1u)));
             if (seg_end) {
                 sAcc[w][0][owner] += v0; sAcc[w][1][owner] += v1; sAcc[w][2][owner] += v2;
                 sAcc[w][3][owner] += v3; sAcc[w][4][owner] += v4; sAcc[w][5][owner] += v5;
@@ -112,7 +211,7 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     }
     if (me < hi_p) {
         double4 V = cat2(sVa[me], sVb[me]), W = cat2(sWa[me], sWb[me]);
-        const uint32_t cnt = e_me - s_me;
+        const uint32_t cnt = cnt_me;
         if (cnt) {
             // body update with the real masses (1/m = (c/m)/c): the mass-splitting average
             const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
@@ -125,12 +224,18 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
 }
 
 void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
-                     const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row, const P4 *Pa_in,
-                     const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp,
-                     cudaStream_t s)
+                     const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo, const R4 *row,
+                     const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd,
+                     const SolveParams &sp, cudaStream_t s)
 {
-    if (N) k_sweep_t2<<<(unsigned)((N + TT - 1) / TT), TT, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, geo, row,
-                                                                   Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
+    if (!N) return;
+    const unsigned gb = (unsigned)((N + TT - 1) / TT);
+    if (pk)
+        k_sweep_t2<true><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase, geo, row,
+                                           Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
+    else
+        k_sweep_t2<false><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, nullptr, nullptr, geo, row, Pa_in,
+                                            Pb_in, Pa_out, Pb_out, bnd, sp);
 }
 
 // ==================================================================== layout experiment (t3)
@@ -206,7 +311,7 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
             double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
             if (valid) {
                 const int o = lo_p + owner;
-                const uint32_t c = ent.x & ~B_SIDE;
+                const uint32_t c = ent.x & INC_CMASK;
                 const bool isB = (ent.x & B_SIDE) != 0;
                 const uint32_t p = ent.y;
                 const G4 g = ld4g(&geo[c]);

@@ -39,7 +39,7 @@ class Solver(C.Structure):
     _fields_ = [("dt", C.c_double), ("n_iter", C.c_int32), ("n_iter_impact", C.c_int32),
                 ("hertz_exp", C.c_double), ("k_lin", C.c_double), ("damping_steps", C.c_double),
                 ("v_impact", C.c_double), ("gravity", C.c_double * 3), ("rolling_dims", C.c_int32),
-                ("ordering", C.c_int32), ("skin", C.c_double)]
+                ("ordering", C.c_int32), ("skin", C.c_double), ("reduction", C.c_int32), ("pad1", C.c_int32)]
 
 
 class Box(C.Structure):
@@ -215,11 +215,17 @@ class LoopbackGroup:
     device copies: the decomposition on a single GPU (include/dem.h)."""
 
     def __init__(self, world_size):
+        import weakref
         self.world_size = world_size
         self.handle = lib().dem_loopback_create(world_size)
+        self._beds = weakref.WeakSet()
 
     def close(self):
+        """Destroys the group; beds still open on it are closed first (their transports point
+        into the group)."""
         if self.handle:
+            for b in list(self._beds):
+                b.close()
             lib().dem_loopback_destroy(self.handle)
             self.handle = None
 
@@ -299,7 +305,8 @@ class Bed:
         mat.update(material or {})
         material = mat
         sol = dict(dt=1e-5, n_iter=92, n_iter_impact=0, hertz_exp=1.25, k_lin=0.0, damping_steps=4.5,
-                   v_impact=-1.0, gravity=(0.0, 0.0, -9.81), rolling_dims=3, ordering=0, skin=0.0)
+                   v_impact=-1.0, gravity=(0.0, 0.0, -9.81), rolling_dims=3, ordering=0, skin=0.0,
+                   reduction=0)
         sol.update(solver or {})
         bx = dict(lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), wall_mask=0x3F, wall_mu_t=0.0, wall_mu_r=0.0)
         bx.update(box or {})
@@ -338,6 +345,7 @@ class Bed:
             dist.slab_lo, dist.slab_hi = float(dcfg["slab"][0]), float(dcfg["slab"][1])
             if dcfg.get("transport", "nccl") == "loopback":
                 dist.transport, dist.loopback = 1, dcfg["group"].handle
+                self._group = dcfg["group"]
             else:
                 self._nccl_id = (C.c_ubyte * 128).from_buffer_copy(dcfg["nccl_id"])
                 dist.transport, dist.nccl_unique_id = 0, C.cast(self._nccl_id, C.c_void_p)
@@ -363,6 +371,8 @@ class Bed:
         if st != DEM_OK:
             raise DemError(st, lib().dem_last_error(None).decode())
         self._h = h
+        if getattr(self, "_group", None) is not None:
+            self._group._beds.add(self)
         self.last_report = None
         if generator is not None:
             self.n = self.n_owned

@@ -93,6 +93,8 @@ def compare_step(bed, n_it=30, dt=1e-5, with_walls=True, hist=None, material=Non
     gsol = dict(dt=dt, n_iter=n_it)
     if "ordering" in solver:
         gsol["ordering"] = solver["ordering"]
+    if "reduction" in solver:
+        gsol["reduction"] = solver["reduction"]
     if "v_imp" in solver:
         gsol["v_impact"] = solver["v_imp"]
     if "g" in solver:
@@ -148,6 +150,7 @@ def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bo
     err = [None] * G
 
     def rank_main(r):
+        b = None
         try:
             m = (bed.x[:, 0] >= bounds[r]) & (bed.x[:, 0] < bounds[r + 1])
             b = dem.Bed(bed.x[m], bed.r[m], bed.v[m], bed.w[m], bed.gid[m], solver=solver, box=box, material=material,
@@ -157,9 +160,11 @@ def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bo
             reps = [b.step(1) for _ in range(n_steps)]
             res[r] = dict(state=b.get_state(), contacts=b.get_contacts(), forces=b.get_forces(), reports=reps,
                           plates=[b.get_plate(p) for p in pids], n_local=b.n_local, n_owned=b.n_owned)
-            b.close()
         except Exception as e:   # noqa: BLE001 -- surfaced by the caller
             err[r] = e
+        finally:
+            if b is not None:
+                b.close()
 
     th = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
     for t in th:

@@ -55,10 +55,12 @@ def test_config0_first_steps():
     assert res["force_err"] <= TOL_F and res["torque_err"] <= TOL_F, res
 
 
-def test_config0s_one_step_with_history():
-    """Settled config 0 with its contact history as warm start: ~10k contacts."""
+@pytest.mark.parametrize("reduction", [0, 1])
+def test_config0s_one_step_with_history(reduction):
+    """Settled config 0 (SURVEY C25) with its contact history as warm start: ~10k contacts;
+    both per-particle reductions of the sweep (canonical packed chunks, contiguous chunks)."""
     bed, hist = config0s()
-    res = compare_step(bed, n_it=92, dt=1e-5, hist=hist, v_imp=1e30)
+    res = compare_step(bed, n_it=92, dt=1e-5, hist=hist, v_imp=1e30, reduction=reduction)
     assert res["n_contacts_ref"] > 5000
     assert res["pairs_equal"], res
     assert res["force_err"] <= TOL_F and res["torque_err"] <= TOL_F, res
