@@ -283,6 +283,19 @@ dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *out);
 /* Kinematic box wall: velocity along its inward normal (shear-box / servo walls). */
 dem_status dem_drive_wall(dem_ctx *ctx, int32_t wall, double normal_velocity);
 
+/* Box wall state (walls: P:252; servo-controlled triaxial walls: P:166-202).
+ * Wall w = 2 axis + side (0 -x, 1 +x, 2 -y, 3 +y, 4 -z, 5 +z); its plane passes through `point`
+ * with inward unit `normal`.  force = contact reaction on the wall during the last step,
+ * (1/h) sum over its contacts of (P_n n + P_t), an exact int64 sum over contacts and ranks (the
+ * stress a wall carries is -force . normal / area).  DEM_ERR_INVALID: no such wall. */
+typedef struct {
+    double point[3], normal[3];
+    double velocity;           /* along the inward normal [m/s] */
+    double force[3];           /* [N] */
+    int64_t n_contacts;
+} dem_wall_state;
+dem_status dem_get_wall(dem_ctx *ctx, int32_t wall, dem_wall_state *out);
+
 /* Device-time accounting of the library's own kernels (CUDA events on the ctx stream). */
 dem_status dem_set_timing(dem_ctx *ctx, int32_t enable);
 dem_status dem_get_timing(dem_ctx *ctx, dem_timing *out);

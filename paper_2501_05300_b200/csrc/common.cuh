@@ -40,6 +40,7 @@ __device__ __forceinline__ uint64_t partner_key(uint32_t p, const uint32_t *__re
 #define WALL_KEY_BASE 0xFFFFFFF0u        // public key of wall w: 2^32-16+w
 #define PLATE_KEY_BASE 0xFFFFF000u       // public key of plate p box b: 2^32-4096+16p+b
 #define FIXED_SCALE 1099511627776.0      // 2^40: int64 fixed point for plate impulse sums
+#define NB_SLOTS (DEM_MAX_PLATES + 6)    // boundary-body sums: plates 0..7, walls 8..13
 
 // Storage precision of the contact arrays: -DDEM_P64 / -DDEM_G64 / -DDEM_R64
 // store impulses / normals / row constants as fp64 instead of fp32 (all row arithmetic is fp64).
@@ -166,6 +167,8 @@ struct DevBoundary {
     int plimit[DEM_MAX_PLATES][3];
     double pfmin[DEM_MAX_PLATES][3], pfmax[DEM_MAX_PLATES][3];
     double pmotor[DEM_MAX_PLATES][3];   // motor / constraint force of the last step [N]
+    double wforce[6][3];                // wall reactions of the last step [N]
+    int64_t wcount[6];
     int64_t pcount[DEM_MAX_PLATES];
     double time;
     // references at the last rebuild (trigger)

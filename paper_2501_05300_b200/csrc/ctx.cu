@@ -281,6 +281,8 @@ static void setup_walls(dem_ctx *ctx)
         b.wn[w][ax] = side == 0 ? 1.0 : -1.0;
         b.wvel[w] = 0;
         b.wpresent[w] = (ctx->box.wall_mask >> w) & 1;
+        for (int k = 0; k < 3; k++) b.wforce[w][k] = 0;
+        b.wcount[w] = 0;
         for (int k = 0; k < 3; k++) b.wp_ref[w][k] = b.wp[w][k];
     }
     b.wall_mu_t = ctx->box.wall_mu_t;
@@ -314,7 +316,7 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
         TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
         TRY(A(ctx, &ctx->db, 1));
         TRY(A(ctx, &ctx->pacc, 3 * DEM_MAX_PLATES));
-        TRY(A(ctx, &ctx->pcount, DEM_MAX_PLATES));
+        TRY(A(ctx, &ctx->pcount, NB_SLOTS));
         TRY(A(ctx, &ctx->dsc, 1));
     }
     ctx->capN = cap;
@@ -859,19 +861,19 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     launch_integrate(N, OWN(ctx), ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->xref, sp.h, sp.rho, ctx->ke_part,
                      ctx->dsc, s);
     launch_plate_sum(nc, OWN(ctx), ctx->cij, ctx->geo, ctx->Pfa, ctx->pacc, ctx->pcount, s);
-    if (ctx->tp && ctx->hb.n_plates > 0) {
-        // plate reactions: exact int64 sums over the ranks (each contact counted by its owner)
-        unsigned long long acc[3 * DEM_MAX_PLATES];
-        unsigned int pc[DEM_MAX_PLATES];
+    if (ctx->tp) {
+        // plate and wall reactions: exact int64 sums over the ranks (each contact counted by its owner)
+        unsigned long long acc[3 * NB_SLOTS];
+        unsigned int pc[NB_SLOTS];
         CK(cudaMemcpyAsync(acc, ctx->pacc, sizeof(acc), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(pc, ctx->pcount, sizeof(pc), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
-        long long v[4 * DEM_MAX_PLATES];
-        for (int q = 0; q < 3 * DEM_MAX_PLATES; q++) v[q] = (long long)acc[q];
-        for (int q = 0; q < DEM_MAX_PLATES; q++) v[3 * DEM_MAX_PLATES + q] = pc[q];
-        if (!ctx->tp->allreduce_i64(v, 4 * DEM_MAX_PLATES, 0, s, ctx->err)) return DEM_ERR_NCCL;
-        for (int q = 0; q < 3 * DEM_MAX_PLATES; q++) acc[q] = (unsigned long long)v[q];
-        for (int q = 0; q < DEM_MAX_PLATES; q++) pc[q] = (unsigned int)v[3 * DEM_MAX_PLATES + q];
+        long long v[4 * NB_SLOTS];
+        for (int q = 0; q < 3 * NB_SLOTS; q++) v[q] = (long long)acc[q];
+        for (int q = 0; q < NB_SLOTS; q++) v[3 * NB_SLOTS + q] = pc[q];
+        if (!ctx->tp->allreduce_i64(v, 4 * NB_SLOTS, 0, s, ctx->err)) return DEM_ERR_NCCL;
+        for (int q = 0; q < 3 * NB_SLOTS; q++) acc[q] = (unsigned long long)v[q];
+        for (int q = 0; q < NB_SLOTS; q++) pc[q] = (unsigned int)v[3 * NB_SLOTS + q];
         CK(cudaMemcpyAsync(ctx->pacc, acc, sizeof(acc), cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(ctx->pcount, pc, sizeof(pc), cudaMemcpyHostToDevice, s));
     }
@@ -1348,6 +1350,17 @@ dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *o)
     for (int k = 0; k < 3; k++) { o->pos[k] = b.ppos[plate][k]; o->vel[k] = b.pvel[plate][k]; o->force[k] = b.pforce[plate][k];
                                     o->motor_force[k] = b.pmotor[plate][k]; }
     o->n_contacts = b.pcount[plate];
+    return DEM_OK;
+}
+
+dem_status dem_get_wall(dem_ctx *ctx, int32_t wall, dem_wall_state *o)
+{
+    if (!ctx || !o) return DEM_ERR_INVALID;
+    const DevBoundary &b = ctx->hb;
+    if (wall < 0 || wall > 5 || !b.wpresent[wall]) { ctx->err = "no such wall"; return DEM_ERR_INVALID; }
+    for (int k = 0; k < 3; k++) { o->point[k] = b.wp[wall][k]; o->normal[k] = b.wn[wall][k]; o->force[k] = b.wforce[wall][k]; }
+    o->velocity = b.wvel[wall];
+    o->n_contacts = b.wcount[wall];
     return DEM_OK;
 }
 

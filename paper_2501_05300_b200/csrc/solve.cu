@@ -618,7 +618,8 @@ __global__ void k_reduce_ke(const double *__restrict__ part, int64_t nb, StepSca
     if (threadIdx.x == 0) sc->ke = sk[0];
 }
 
-// plate reaction: F_p = (1/h) sum_{c in p} (P_n n + P_t), int64 fixed point (order-free, exact)
+// plate and wall reactions: F = (1/h) sum_{c on the body} (P_n n + P_t), int64 fixed point
+// (order-free, exact; slots: plates 0..7, walls 8..13)
 __global__ void k_plate_sum(int64_t nc, const uint8_t *__restrict__ own, const uint2 *__restrict__ cij, const G4 *__restrict__ geo,
                             const P4 *__restrict__ Pa, unsigned long long *__restrict__ acc,
                             unsigned int *__restrict__ pcount)
@@ -627,8 +628,8 @@ __global__ void k_plate_sum(int64_t nc, const uint8_t *__restrict__ own, const u
     if (c >= nc) return;
     if (own && !own[cij[c].x]) return;                   // a ghost's plate contact: its owner adds it
     const uint32_t j = cij[c].y;
-    if ((j & (PARTNER_EXT | PARTNER_PLATE)) != (PARTNER_EXT | PARTNER_PLATE)) return;
-    const int q = (j >> 4) & 0xF;
+    if (!(j & PARTNER_EXT)) return;
+    const int q = (j & PARTNER_PLATE) ? (int)((j >> 4) & 0xF) : DEM_MAX_PLATES + (int)(j & ~PARTNER_EXT);
     const G4 g = geo[c];
     const P4 a = Pa[c];
     const double L[3] = {(double)a.x * g.x + a.y, (double)a.x * g.y + a.z, (double)a.x * g.z + a.w};
@@ -651,6 +652,11 @@ __global__ void k_boundary(DevBoundary *bnd, const unsigned long long *__restric
         disp = fmax(disp, sqrt(d2));
     }
     const double t1 = __dadd_rn(bnd->time, h);
+    for (int w = 0; w < 6; w++) {
+        for (int k = 0; k < 3; k++)
+            bnd->wforce[w][k] = (double)(long long)acc[3 * (DEM_MAX_PLATES + w) + k] / FIXED_SCALE / h;
+        bnd->wcount[w] = pcount[DEM_MAX_PLATES + w];
+    }
     for (int q = 0; q < bnd->n_plates; q++) {
         for (int k = 0; k < 3; k++) {
             bnd->pforce[q][k] = (double)(long long)acc[3 * q + k] / FIXED_SCALE / h;
@@ -792,8 +798,8 @@ void launch_integrate(int64_t N, const uint8_t *own, double4 *pos, const double4
 void launch_plate_sum(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
                       unsigned int *pcount, cudaStream_t s)
 {
-    cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 3 * DEM_MAX_PLATES, s);
-    cudaMemsetAsync(pcount, 0, sizeof(unsigned int) * DEM_MAX_PLATES, s);
+    cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * 3 * NB_SLOTS, s);
+    cudaMemsetAsync(pcount, 0, sizeof(unsigned int) * NB_SLOTS, s);
     if (nc) k_plate_sum<<<GRID(nc)>>>(nc, own, cij, geo, Pa, acc, pcount);
 }
 void launch_boundary(DevBoundary *bnd, const unsigned long long *acc, const unsigned int *pcount, double h, StepScalars *sc,

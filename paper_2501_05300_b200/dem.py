@@ -106,6 +106,11 @@ class PlateState(C.Structure):
                 ("motor_force", C.c_double * 3), ("n_contacts", C.c_int64)]
 
 
+class WallState(C.Structure):
+    _fields_ = [("point", C.c_double * 3), ("normal", C.c_double * 3), ("velocity", C.c_double),
+                ("force", C.c_double * 3), ("n_contacts", C.c_int64)]
+
+
 class Timing(C.Structure):
     _fields_ = [("ms_total", C.c_double), ("ms_detect", C.c_double), ("ms_rebuild", C.c_double),
                 ("ms_sweeps", C.c_double), ("ms_integrate", C.c_double), ("n_sweep_launches", C.c_int64),
@@ -119,7 +124,8 @@ CONTACT_DTYPE = np.dtype([("key", "<u8"), ("n", "<f8", (3,)), ("delta", "<f8"), 
 
 # every symbol include/dem.h declares (checked by tests/test_boundary.py)
 EXPORTS = ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts", "dem_get_forces",
-           "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_set_timing", "dem_get_timing",
+           "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_get_wall", "dem_set_timing",
+           "dem_get_timing",
            "dem_reset_timing", "dem_bench_sweeps", "dem_num_particles", "dem_num_local", "dem_nccl_unique_id",
            "dem_loopback_create", "dem_loopback_destroy", "dem_generator_count", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
            "dem_contact_network_length", "dem_plan_iterations", "dem_plan_timestep"]
@@ -146,6 +152,7 @@ def lib():
         L.dem_drive_plate.argtypes = [vp, i32, i32, i32, d, d, d, d]
         L.dem_get_plate.argtypes = [vp, i32, C.POINTER(PlateState)]
         L.dem_drive_wall.argtypes = [vp, i32, d]
+        L.dem_get_wall.argtypes = [vp, i32, C.POINTER(WallState)]
         L.dem_set_timing.argtypes = [vp, i32]
         L.dem_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.dem_reset_timing.argtypes = [vp]
@@ -177,7 +184,7 @@ def lib():
         L.dem_plan_timestep.restype = d
         for f in ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts",
                   "dem_get_forces", "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall",
-                  "dem_set_timing", "dem_get_timing", "dem_reset_timing", "dem_bench_sweeps", "dem_destroy"]:
+                  "dem_get_wall", "dem_set_timing", "dem_get_timing", "dem_reset_timing", "dem_bench_sweeps", "dem_destroy"]:
             getattr(L, f).restype = C.c_int
         _lib = L
     return _lib
@@ -499,6 +506,13 @@ class Bed:
         self._check(lib().dem_get_plate(self._h, plate, C.byref(s)))
         return {"pos": list(s.pos), "vel": list(s.vel), "force": list(s.force),
                 "motor_force": list(s.motor_force), "n_contacts": s.n_contacts}
+
+    def get_wall(self, wall):
+        """dem_get_wall: plane point, inward normal, normal velocity, contact reaction [N]."""
+        s = WallState()
+        self._check(lib().dem_get_wall(self._h, wall, C.byref(s)))
+        return {"point": list(s.point), "normal": list(s.normal), "velocity": s.velocity, "force": list(s.force),
+                "n_contacts": s.n_contacts}
 
     def drive_wall(self, wall, normal_velocity):
         self._check(lib().dem_drive_wall(self._h, wall, normal_velocity))

@@ -38,6 +38,7 @@ def test_struct_sizes_match_header(demlib, tmp_path):
     structs = {"dem_bed_desc": demlib.BedDesc, "dem_dist_desc": demlib.DistDesc, "dem_step_report": demlib.StepReport,
                "dem_state_view": demlib.StateView, "dem_contact_view": demlib.ContactView,
                "dem_plate_desc": demlib.PlateDesc, "dem_plate_state": demlib.PlateState, "dem_timing": demlib.Timing,
+               "dem_wall_state": demlib.WallState,
                "dem_solver": demlib.Solver, "dem_material": demlib.Material, "dem_box": demlib.Box,
                "dem_particles": demlib.Particles, "dem_generator": demlib.Generator}
     src = tmp_path / "sz.c"
