@@ -80,6 +80,9 @@ struct dem_ctx {
     // packed incidence of the canonical reduction (solver.reduction == 0; sweep_t2.cu)
     uint32_t *pk_off = nullptr, *pk_start = nullptr, *pk_wsize = nullptr, *pk_wbase = nullptr;
     uint2 *pk_inc = nullptr;
+    G4 *pk_geo = nullptr;
+    R4 *pk_row = nullptr, *pk_rowi = nullptr;
+    P8 *p8[2] = {nullptr, nullptr};
     int64_t pk_cap = 0, pk_n = 0;
     PackedInc pkv{};
     uint2 *inc = nullptr;
@@ -349,6 +352,7 @@ static dem_status ensure_cand(dem_ctx *ctx, int64_t n)
     TRY(regrow(ctx, &ctx->row_imp, cap)); TRY(regrow(ctx, &ctx->Pwa, cap)); TRY(regrow(ctx, &ctx->Pwb, cap));
     for (int k = 0; k < 2; k++) { TRY(regrow(ctx, &ctx->Pa[k], cap)); TRY(regrow(ctx, &ctx->Pb[k], cap)); }
     TRY(regrow(ctx, &ctx->ccand, cap));
+    TRY(regrow(ctx, &ctx->p8[0], cap)); TRY(regrow(ctx, &ctx->p8[1], cap));
     TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
     if (!ctx->gs_scr) TRY(A(ctx, &ctx->gs_scr, 260));
     TRY(regrow(ctx, &ctx->inc, 2 * cap));
@@ -723,11 +727,12 @@ static dem_status pack_incidence(dem_ctx *ctx, int64_t N)
     if ((int64_t)np > ctx->pk_cap) {
         const int64_t cap = std::max<int64_t>((int64_t)np + np / 4, 1024);
         TRY(regrow(ctx, &ctx->pk_inc, cap));
+        TRY(regrow(ctx, &ctx->pk_geo, cap)); TRY(regrow(ctx, &ctx->pk_row, cap)); TRY(regrow(ctx, &ctx->pk_rowi, cap));
         ctx->pk_cap = cap;
     }
     ctx->pk_n = np;
     pack_fill(N, ctx->inc_start, ctx->inc, ctx->pk_off, ctx->pk_wbase, ctx->pk_start, ctx->pk_inc, np, s, &ctx->launches);
-    ctx->pkv = PackedInc{ctx->pk_inc, ctx->pk_start, ctx->pk_wbase};
+    ctx->pkv = PackedInc{ctx->pk_inc, ctx->pk_start, ctx->pk_wbase, ctx->pk_geo, ctx->pk_row, ctx->p8[0], ctx->p8[1]};
     return DEM_OK;
 }
 
@@ -804,8 +809,16 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         // Newton impact stage from P = 0 with Sigma = 0 (reading R13); impulses discarded
         CK(cudaMemsetAsync(ctx->Pa[0], 0, nc * sizeof(P4), s));
         CK(cudaMemsetAsync(ctx->Pb[0], 0, nc * sizeof(P4), s));
+        if (PKV(ctx)) {   // canonical reduction: packed rows, impulses in 32-byte slots
+            pack_rows(ctx->pk_n, ctx->pk_inc, ctx->geo, ctx->row_imp, ctx->pk_geo, ctx->pk_rowi, s);
+            CK(cudaMemsetAsync(ctx->p8[0], 0, nc * sizeof(P8), s));
+            ctx->pkv.row = ctx->pk_rowi;
+            ctx->launches += 1;
+        }
         for (int it = 0; it < n_imp; it++) {
             const int pi = it & 1;
+            ctx->pkv.p8in = ctx->p8[pi];
+            ctx->pkv.p8out = ctx->p8[pi ^ 1];
             launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                          ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row_imp, ctx->Pa[pi],
                          ctx->Pb[pi], ctx->Pa[pi ^ 1], ctx->Pb[pi ^ 1], ctx->db, sp, s);
@@ -828,6 +841,13 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     tstart(ctx, 3);
     const int n_it = ctx->sol.n_iter;
     const P4 *pin_a = ctx->Pwa, *pin_b = ctx->Pwb;
+    const bool pk = !gs && PKV(ctx) != nullptr;
+    if (pk) {
+        pack_rows(ctx->pk_n, ctx->pk_inc, ctx->geo, ctx->row, ctx->pk_geo, ctx->pk_row, s);
+        p8_pack(nc, ctx->Pwa, ctx->Pwb, ctx->p8[0], s);
+        ctx->pkv.row = ctx->pk_row;
+        ctx->launches += 2;
+    }
     if (gs) {
         // N_it coloured Gauss-Seidel sweeps, impulses and velocities updated in place
         if (nc) {
@@ -842,6 +862,8 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     }
     for (int it = 0; it < (gs ? 0 : n_it); it++) {
         P4 *oa = ctx->Pa[it & 1], *ob = ctx->Pb[it & 1];
+        ctx->pkv.p8in = ctx->p8[it & 1];
+        ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
         launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                      ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
                      ctx->db, sp, s);
@@ -849,6 +871,13 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
         pin_a = oa;
         pin_b = ob;
+    }
+    if (pk && n_it > 0) {
+        // the final impulses back into the per-array layout the rest of the step reads
+        p8_unpack(nc, ctx->p8[n_it & 1], ctx->Pa[0], ctx->Pb[0], s);
+        pin_a = ctx->Pa[0];
+        pin_b = ctx->Pb[0];
+        ctx->launches += 1;
     }
     if (!gs) ctx->launches += n_it;
     ctx->tm.n_sweep_launches += n_it;
@@ -1487,9 +1516,15 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
         }
         const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
         P4 *pai = ctx->Pwa, *pbi = ctx->Pwb, *pao = spa, *pbo = spb;
+        if (var == 0 && PKV(ctx)) {
+            p8_pack(nc, ctx->Pwa, ctx->Pwb, ctx->p8[0], s);
+            ctx->pkv.row = ctx->pk_row;
+        }
         cudaEventRecord(ctx->ev[6], s);
         for (int it = 0; it < n; it++) {
             double4 *vo = vbuf[it & 1], *wo = wbuf[it & 1];
+            ctx->pkv.p8in = ctx->p8[it & 1];
+            ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
             if (var < 10 || (var >= 40 && var < 50)) {
                 set_sweep_variant(var);
                 launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, vi, wi, vo, wo, ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row,

@@ -50,7 +50,14 @@ struct PackedInc {
     const uint2 *inc;
     const uint32_t *start;
     const uint32_t *wbase;
+    const G4 *geo;        // normals, rows of the stage: one copy per half-contact, packed order
+    const R4 *row;
+    const P8 *p8in;       // impulses of the sweep, one 32-byte slot per contact
+    P8 *p8out;
 };
+void pack_rows(int64_t np, const uint2 *pinc, const G4 *geo, const R4 *row, G4 *gpk, R4 *rpk, cudaStream_t s);
+void p8_pack(int64_t nc, const P4 *a, const P4 *b, P8 *o, cudaStream_t s);
+void p8_unpack(int64_t nc, const P8 *q, P4 *a, P4 *b, cudaStream_t s);
 void pack_plan(int64_t N, const uint32_t *inc_start, uint32_t *off_local, uint32_t *wsize, uint32_t *wbase,
                void *scan_tmp, cudaStream_t s, long long *launches);
 void pack_fill(int64_t N, const uint32_t *inc_start, const uint2 *inc, const uint32_t *off_local, const uint32_t *wbase,

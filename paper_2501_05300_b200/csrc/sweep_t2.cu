@@ -106,6 +106,38 @@ void pack_fill(int64_t N, const uint32_t *inc_start, const uint2 *inc, const uin
     *launches += 1;
 }
 
+// per step (and per stage): normals and rows gathered into packed order, both halves a copy
+__global__ void k_pack_rows(int64_t np, const uint2 *__restrict__ pinc, const G4 *__restrict__ geo,
+                            const R4 *__restrict__ row, G4 *__restrict__ gpk, R4 *__restrict__ rpk)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= np) return;
+    const uint32_t e = pinc[k].x;
+    if (e == PK_HOLE) return;
+    const uint32_t c = e & INC_CMASK;
+    if (gpk) st4g(&gpk[k], ld4g(&geo[c]));
+    st4g(&rpk[k], ld4g(&row[c]));
+}
+__global__ void k_p8_pack(int64_t nc, const P4 *__restrict__ a, const P4 *__restrict__ b, P8 *__restrict__ o)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c < nc) stP8(&o[c], a[c], b[c]);
+}
+__global__ void k_p8_unpack(int64_t nc, const P8 *__restrict__ q, P4 *__restrict__ a, P4 *__restrict__ b)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const P8 v = ldP8(&q[c]);
+    a[c] = v.a;
+    b[c] = v.b;
+}
+void pack_rows(int64_t np, const uint2 *pinc, const G4 *geo, const R4 *row, G4 *gpk, R4 *rpk, cudaStream_t s)
+{ if (np) k_pack_rows<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(np, pinc, geo, row, gpk, rpk); }
+void p8_pack(int64_t nc, const P4 *a, const P4 *b, P8 *o, cudaStream_t s)
+{ if (nc) k_p8_pack<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(nc, a, b, o); }
+void p8_unpack(int64_t nc, const P8 *q, P4 *a, P4 *b, cudaStream_t s)
+{ if (nc) k_p8_unpack<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(nc, q, a, b); }
+
 // PACKED: the canonical reduction above (default); false: the contiguous CSR chunks (fastest
 // layout-independent of packing; bit-reproducible run to run but rounding depends on the warp
 // grouping, i.e. on the decomposition)
@@ -116,7 +148,8 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                const uint32_t *__restrict__ pstart, const uint32_t *__restrict__ wbase,
                const G4 *__restrict__ geo, const R4 *__restrict__ row, const P4 *__restrict__ Pa_in,
                const P4 *__restrict__ Pb_in, P4 *__restrict__ Pa_out, P4 *__restrict__ Pb_out,
-               const DevBoundary *__restrict__ bnd, SolveParams sp)
+               const P8 *__restrict__ P8_in, P8 *__restrict__ P8_out, const DevBoundary *__restrict__ bnd,
+               SolveParams sp)
 {
     __shared__ double2 sVa[TT], sVb[TT], sWa[TT], sWb[TT];
     __shared__ double sAcc[NWT][6][32];
@@ -164,9 +197,13 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                 const uint32_t c = ent.x & INC_CMASK;
                 const bool isB = (ent.x & B_SIDE) != 0;
                 const uint32_t p = ent.y;
-                const G4 g = ld4g(&geo[c]);
-                const R4 rw = ld4g(&row[c]);
-                const P4 pa = Pa_in[c], pb = Pb_in[c];
+                // PACKED: normals and rows duplicated per half-contact in packed order (coalesced),
+                // both impulse records of the contact in one 32-byte slot
+                const G4 g = ld4g(PACKED ? &geo[k] : &geo[c]);
+                const R4 rw = ld4g(PACKED ? &row[k] : &row[c]);
+                P4 pa, pb;
+                if (PACKED) { const P8 q = ldP8(&P8_in[c]); pa = q.a; pb = q.b; }
+                else { pa = Pa_in[c]; pb = Pb_in[c]; }
                 double4 VP, WP;
                 double mt = sp.mu_t;
                 if (!(p & PARTNER_EXT)) {
@@ -184,8 +221,8 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                 const HalfOut r = half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt, g, rw,
                                                pa, pb, sp.rolling_dims);
                 if (!isB) {   // both halves compute the same impulses; body a stores them
-                    Pa_out[c] = r.Pa;
-                    Pb_out[c] = r.Pb;
+                    if (PACKED) stP8(&P8_out[c], r.Pa, r.Pb);
+                    else { Pa_out[c] = r.Pa; Pb_out[c] = r.Pb; }
                 }
                 v0 = r.dL.x; v1 = r.dL.y; v2 = r.dL.z; v3 = r.dA.x; v4 = r.dA.y; v5 = r.dA.z;
             }
@@ -231,11 +268,11 @@ void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 
     if (!N) return;
     const unsigned gb = (unsigned)((N + TT - 1) / TT);
     if (pk)
-        k_sweep_t2<true><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase, geo, row,
-                                           Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
+        k_sweep_t2<true><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase, pk->geo,
+                                           pk->row, nullptr, nullptr, nullptr, nullptr, pk->p8in, pk->p8out, bnd, sp);
     else
         k_sweep_t2<false><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, nullptr, nullptr, geo, row, Pa_in,
-                                            Pb_in, Pa_out, Pb_out, bnd, sp);
+                                            Pb_in, Pa_out, Pb_out, nullptr, nullptr, bnd, sp);
 }
 
 // ==================================================================== layout experiment (t3)
@@ -243,23 +280,7 @@ void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 
 // (one 256-bit load and store instead of two 128-bit ones) and (VW) a particle's v and w
 // interleaved in one 64-byte record (both gathers hit one cache line).  Diagnostic only: the
 // bench converts the layouts before timing (dem_bench_sweeps variants 60-63).
-struct __align__(32) P8 { float4 a, b; };
 struct __align__(32) VW { double4 v, w; };
-
-__device__ __forceinline__ P8 ldP8(const P8 *p)
-{
-    P8 r;
-    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y), "=f"(r.b.z), "=f"(r.b.w)
-        : "l"(p));
-    return r;
-}
-__device__ __forceinline__ void stP8(P8 *p, const float4 a, const float4 b)
-{
-    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(a.z),
-                 "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
-                 : "memory");
-}
 
 template <bool USE_P8, bool USE_VW, bool NOSEL = false>
 __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
