@@ -1516,9 +1516,10 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
         }
         const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
         P4 *pai = ctx->Pwa, *pbi = ctx->Pwb, *pao = spa, *pbo = spb;
-        if (var == 0 && PKV(ctx)) {
+        if ((var == 0 || var == 8) && PKV(ctx)) {
             p8_pack(nc, ctx->Pwa, ctx->Pwb, ctx->p8[0], s);
-            ctx->pkv.row = ctx->pk_row;
+            ctx->pkv.geo = var == 8 ? ctx->geo : ctx->pk_geo;
+            ctx->pkv.row = var == 8 ? ctx->row : ctx->pk_row;
         }
         cudaEventRecord(ctx->ev[6], s);
         for (int it = 0; it < n; it++) {
@@ -1553,6 +1554,8 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
         }
         cudaEventRecord(ctx->ev[7], s);
         set_sweep_variant(0);
+        ctx->pkv.geo = ctx->pk_geo;
+        ctx->pkv.row = ctx->pk_row;
         CK(cudaGetLastError());
         if (pass == 0) CK(cudaMemcpyAsync(ref, vres, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
         CK(cudaStreamSynchronize(s));

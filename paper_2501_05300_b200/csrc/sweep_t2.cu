@@ -29,6 +29,7 @@ __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { retu
 // packing depends only on list lengths, the sums only on the lists (ordered by partner gid), so
 // every decomposition and warp grouping produces the same bits.
 constexpr uint32_t PK_HOLE = 0xFFFFFFFFu;
+bool g_t2_rows_by_contact = false;
 
 // one warp per 32 consecutive particles (the sweep's warp grouping): first-fit packing
 __global__ void k_pack_plan(int64_t N, const uint32_t *__restrict__ inc_start, uint32_t *__restrict__ off_local,
@@ -141,7 +142,7 @@ void p8_unpack(int64_t nc, const P8 *q, P4 *a, P4 *b, cudaStream_t s)
 // PACKED: the canonical reduction above (default); false: the contiguous CSR chunks (fastest
 // layout-independent of packing; bit-reproducible run to run but rounding depends on the warp
 // grouping, i.e. on the decomposition)
-template <bool PACKED>
+template <bool PACKED, bool ROWS_PK = true>
 __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     k_sweep_t2(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win, double4 *__restrict__ vout,
                double4 *__restrict__ wout, const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
@@ -199,8 +200,8 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                 const uint32_t p = ent.y;
                 // PACKED: normals and rows duplicated per half-contact in packed order (coalesced),
                 // both impulse records of the contact in one 32-byte slot
-                const G4 g = ld4g(PACKED ? &geo[k] : &geo[c]);
-                const R4 rw = ld4g(PACKED ? &row[k] : &row[c]);
+                const G4 g = ld4g(PACKED && ROWS_PK ? &geo[k] : &geo[c]);
+                const R4 rw = ld4g(PACKED && ROWS_PK ? &row[k] : &row[c]);
                 P4 pa, pb;
                 if (PACKED) { const P8 q = ldP8(&P8_in[c]); pa = q.a; pb = q.b; }
                 else { pa = Pa_in[c]; pb = Pb_in[c]; }
@@ -267,7 +268,11 @@ void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 
 {
     if (!N) return;
     const unsigned gb = (unsigned)((N + TT - 1) / TT);
-    if (pk)
+    if (pk && g_t2_rows_by_contact)   // diagnostic (dem_bench_sweeps 8): contact-indexed rows
+        k_sweep_t2<true, false><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase,
+                                                  pk->geo, pk->row, nullptr, nullptr, nullptr, nullptr, pk->p8in,
+                                                  pk->p8out, bnd, sp);
+    else if (pk)
         k_sweep_t2<true><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase, pk->geo,
                                            pk->row, nullptr, nullptr, nullptr, nullptr, pk->p8in, pk->p8out, bnd, sp);
     else

@@ -159,7 +159,8 @@ def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bo
             pids = [b.add_plate(**p) for p in plates]
             reps = [b.step(1) for _ in range(n_steps)]
             res[r] = dict(state=b.get_state(), contacts=b.get_contacts(), forces=b.get_forces(), reports=reps,
-                          plates=[b.get_plate(p) for p in pids], n_local=b.n_local, n_owned=b.n_owned)
+                          plates=[b.get_plate(p) for p in pids], n_local=b.n_local, n_owned=b.n_owned,
+                          walls=[b.get_wall(w) for w in range(6) if (box.get("wall_mask", 0x3F) >> w) & 1])
         except Exception as e:   # noqa: BLE001 -- surfaced by the caller
             err[r] = e
         finally:

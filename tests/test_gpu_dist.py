@@ -27,7 +27,8 @@ def single(bed, n_steps, solver, box, plates=()):
     pids = [b.add_plate(**p) for p in plates]
     reps = [b.step(1) for _ in range(n_steps)]
     out = dict(state=b.get_state(), contacts=b.get_contacts(), forces=b.get_forces(), reports=reps,
-               plates=[b.get_plate(p) for p in pids])
+               plates=[b.get_plate(p) for p in pids],
+               walls=[b.get_wall(w) for w in range(6) if (box.get("wall_mask", 0x3F) >> w) & 1])
     b.close()
     return out
 
@@ -140,6 +141,7 @@ def test_chaotic_bed_bit_identical_across_slab_counts(G):
     for r in out["ranks"]:
         assert r["plates"][0]["pos"] == ref["plates"][0]["pos"]
         assert r["plates"][0]["force"] == ref["plates"][0]["force"]
+        assert r["walls"] == ref["walls"]                              # wall reactions: int64 sums
     assert any(rep["impact_fired"] for rep in ref["reports"])
     assert any(rep["rebuilt"] for rep in ref["reports"][1:])
 
