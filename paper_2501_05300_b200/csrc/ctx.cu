@@ -731,6 +731,9 @@ static dem_status pack_incidence(dem_ctx *ctx, int64_t N)
         ctx->pk_cap = cap;
     }
     ctx->pk_n = np;
+    if (getenv("DEM_DEBUG"))
+        fprintf(stderr, "[dem] packed incidence: %u lanes for %llu half-contacts (%.2f %% holes)\n", np,
+                (unsigned long long)(2 * ctx->nc), np ? 100.0 * (np - 2.0 * ctx->nc) / np : 0.0);
     pack_fill(N, ctx->inc_start, ctx->inc, ctx->pk_off, ctx->pk_wbase, ctx->pk_start, ctx->pk_inc, np, s, &ctx->launches);
     ctx->pkv = PackedInc{ctx->pk_inc, ctx->pk_start, ctx->pk_wbase, ctx->pk_geo, ctx->pk_row, ctx->p8[0], ctx->p8[1]};
     return DEM_OK;
@@ -1431,6 +1434,12 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     if (!ctx || n < 1) return DEM_ERR_INVALID;
     if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
     if (ctx->tp) { ctx->err = "dem_bench_sweeps needs world_size 1"; return DEM_ERR_INVALID; }
+    if (variant >= 20 && variant < 60) {
+        // tile-paired / slot / staged experiments assume contacts oriented as their candidates
+        // (body a = the scanning particle); retired with the gid-canonical orientation
+        ctx->err = "sweep variants 20-59 were retired (they need candidate-oriented contacts)";
+        return DEM_ERR_INVALID;
+    }
     const int64_t N = ctx->N, nc = ctx->nc;
     cudaStream_t s = ctx->s;
     double *cb = nullptr;

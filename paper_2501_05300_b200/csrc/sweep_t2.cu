@@ -23,7 +23,7 @@ __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { retu
 // Canonical reduction (trajectories bit-identical for any number of slabs).  The
 // warp's segmented scan sums a particle's contributions with a tree that depends only on the
 // particle's own list -- as long as the list does not straddle a 32-entry chunk boundary.  Once
-// per step each warp's 32 particles are packed first-fit into 32-lane chunks so that no list of
+// per step each warp's 32 particles are packed (first fit decreasing) into 32-lane chunks so that no list of
 // <= 32 half-contacts straddles a boundary and a longer list starts on one (its pieces are then
 // cut at fixed offsets 32, 64, ... of its own list); unused lanes are holes (0xFFFFFFFF).  The
 // packing depends only on list lengths, the sums only on the lists (ordered by partner gid), so
@@ -55,8 +55,11 @@ __global__ void k_pack_plan(int64_t N, const uint32_t *__restrict__ inc_start, u
         }
         longs &= longs - 1;
     }
-    unsigned shorts = __ballot_sync(0xffffffffu, L > 0u && L <= 32u);
-    while (shorts) {                                       // first fit, in particle order
+    // first fit decreasing: lists by decreasing length (ties: particle order) into the first
+    // open chunk with room -- close to the fewest chunks, so few holes
+    for (uint32_t Lc = 32u; Lc >= 1u; Lc--) {
+    unsigned shorts = __ballot_sync(0xffffffffu, L == Lc);
+    while (shorts) {
         const int p = __ffs(shorts) - 1;
         const uint32_t Lp = __shfl_sync(0xffffffffu, L, p);
         const unsigned fit = __ballot_sync(0xffffffffu, lane < (int)nslots && cap >= Lp);
@@ -74,6 +77,7 @@ __global__ void k_pack_plan(int64_t N, const uint32_t *__restrict__ inc_start, u
         }
         if (lane == p) my_off = off;
         shorts &= shorts - 1;
+    }
     }
     if (i < N) off_local[i] = my_off;
     if (lane == 0) wsize[g] = 32u * nb;
