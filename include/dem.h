@@ -179,6 +179,9 @@ typedef struct {
     int32_t n_iter, n_iter_impact;
     int32_t n_colors;          /* Gauss-Seidel ordering: colours of the step's contact graph (else 0) */
     int32_t pad0;
+    double max_normal_residual; /* max over contacts of |min(P_n, u_n + Sigma P_n - b)| at the final
+                                   velocities [N s or m/s mix, as the row] (S:365 convergence report) */
+    double max_cone_excess;    /* max(0, |P_t| - mu_t P_n, |P_r| - mu_r R* P_n) [N s] */
 } dem_step_report;
 
 /* State exchange, ascending gid order; n = capacity in, count out. */

@@ -217,6 +217,8 @@ struct StepScalars {
     unsigned int pad;
     unsigned long long max_disp_bits;   // max |x - x_ref| (double bits; non-negative -> ordered)
     unsigned long long max_v_bits;
+    unsigned long long max_res_bits;    // max normal complementarity residual (report)
+    unsigned long long max_cone_bits;   // max cone excess (report)
     double ke;
     double bnd_disp;
 };

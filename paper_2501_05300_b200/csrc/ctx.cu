@@ -889,6 +889,8 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     tstart(ctx, 4);
     ctx->Pfa = (P4 *)pin_a;
     ctx->Pfb = (P4 *)pin_b;
+    launch_residuals(nc, OWN(ctx), ctx->cij, ctx->geo, ctx->row, ctx->vel[ctx->cur], ctx->Pfa, ctx->Pfb, ctx->db, sp,
+                     ctx->dsc, s);
     // integrate, plates and walls
     launch_integrate(N, OWN(ctx), ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->xref, sp.h, sp.rho, ctx->ke_part,
                      ctx->dsc, s);
@@ -919,15 +921,19 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     StepScalars sc = *ctx->hsc;
     if (ctx->tp) {
         // global report and decisions: every rank takes the same rollback / rebuild branch
-        double mx[3], sm[5];
+        double mx[5], sm[5];
         std::memcpy(&mx[0], &sc.max_disp_bits, 8);
         std::memcpy(&mx[1], &sc.max_v_bits, 8);
         mx[2] = sc.nan_flag ? 1.0 : 0.0;
+        std::memcpy(&mx[3], &sc.max_res_bits, 8);
+        std::memcpy(&mx[4], &sc.max_cone_bits, 8);
         sm[0] = sc.ke; sm[1] = sc.n_pp; sm[2] = sc.n_wall; sm[3] = sc.n_plate; sm[4] = sc.n_degenerate;
-        if (!ctx->tp->allreduce_f64(mx, 3, 1, s, ctx->err) || !ctx->tp->allreduce_f64(sm, 5, 0, s, ctx->err))
+        if (!ctx->tp->allreduce_f64(mx, 5, 1, s, ctx->err) || !ctx->tp->allreduce_f64(sm, 5, 0, s, ctx->err))
             return DEM_ERR_NCCL;
         std::memcpy(&sc.max_disp_bits, &mx[0], 8);
         std::memcpy(&sc.max_v_bits, &mx[1], 8);
+        std::memcpy(&sc.max_res_bits, &mx[3], 8);
+        std::memcpy(&sc.max_cone_bits, &mx[4], 8);
         sc.nan_flag = mx[2] > 0.0 ? 1u : 0u;
         sc.ke = sm[0];
         sc.n_pp = (unsigned)sm[1]; sc.n_wall = (unsigned)sm[2]; sc.n_plate = (unsigned)sm[3]; sc.n_degenerate = (unsigned)sm[4];
@@ -975,6 +981,8 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     rep->ke = sc.ke;
     rep->max_v = maxv;
     rep->max_disp = maxd;
+    std::memcpy(&rep->max_normal_residual, &sc.max_res_bits, 8);
+    std::memcpy(&rep->max_cone_excess, &sc.max_cone_bits, 8);
     rep->n_iter = n_it;
     rep->n_colors = gs ? (int32_t)ctx->gs_cstart.size() - 1 : 0;
     rep->n_iter_impact = impact ? n_imp : 0;

@@ -697,6 +697,44 @@ __global__ void k_boundary(DevBoundary *bnd, const unsigned long long *__restric
     sc->bnd_disp = disp;
 }
 
+// step report: at the final velocities, per owned contact
+// the normal complementarity residual |min(P_n, u_n + Sigma P_n - b)| and the cone excesses
+// |P_t| - mu_t P_n, |P_r| - mu_r R* P_n (non-negative maxima as ordered double bits)
+__global__ void k_residuals(int64_t nc, const uint8_t *__restrict__ own, const uint2 *__restrict__ cij,
+                            const G4 *__restrict__ geo, const R4 *__restrict__ row, const double4 *__restrict__ vel,
+                            const P4 *__restrict__ Pa, const P4 *__restrict__ Pb, const DevBoundary *__restrict__ bnd,
+                            SolveParams sp, StepScalars *sc)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double res = 0.0, cone = 0.0;
+    if (c < nc && (!own || own[cij[c].x])) {
+        const uint2 ij = cij[c];
+        const G4 g = geo[c];
+        const R4 rw = row[c];
+        const P4 a = Pa[c], b = Pb[c];
+        const d3 n = mk(g.x, g.y, g.z);
+        d3 vb;
+        double mt = sp.mu_t;
+        if (!(ij.y & PARTNER_EXT)) vb = xyz(vel[ij.y]);
+        else boundary_vel(ij.y, bnd, vb, mt);
+        const double Pn = a.x;
+        const double un = dot(n, vb - xyz(vel[ij.x]));
+        const double wn = un + rw.x * Pn - rw.y;
+        res = fabs(Pn < wn ? Pn : wn);
+        const double e1 = sqrt((double)a.y * a.y + (double)a.z * a.z + (double)a.w * a.w) - mt * Pn;
+        const double e2 = sqrt((double)b.x * b.x + (double)b.y * b.y + (double)b.z * b.z) - g.w * Pn;
+        cone = fmax(0.0, fmax(e1, e2));
+    }
+    for (int o = 16; o; o >>= 1) {
+        res = fmax(res, __shfl_xor_sync(0xffffffffu, res, o));
+        cone = fmax(cone, __shfl_xor_sync(0xffffffffu, cone, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (res > 0.0) atomicMax(&sc->max_res_bits, (unsigned long long)__double_as_longlong(res));
+        if (cone > 0.0) atomicMax(&sc->max_cone_bits, (unsigned long long)__double_as_longlong(cone));
+    }
+}
+
 __global__ void k_scatter_P(int64_t nc, const uint32_t *__restrict__ ccand, const P4 *__restrict__ Pa,
                             const P4 *__restrict__ Pb, P4 *__restrict__ Pca, P4 *__restrict__ Pcb)
 {
@@ -809,6 +847,10 @@ void launch_plate_sum(int64_t nc, const uint8_t *own, const uint2 *cij, const G4
 void launch_boundary(DevBoundary *bnd, const unsigned long long *acc, const unsigned int *pcount, double h, StepScalars *sc,
                      cudaStream_t s)
 { k_boundary<<<1, 32, 0, s>>>(bnd, acc, pcount, h, sc); }
+void launch_residuals(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const R4 *row, const double4 *vel,
+                      const P4 *Pa, const P4 *Pb, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
+                      cudaStream_t s)
+{ if (nc) k_residuals<<<GRID(nc)>>>(nc, own, cij, geo, row, vel, Pa, Pb, bnd, sp, sc); }
 void launch_scatter_P(int64_t nc, const uint32_t *ccand, const P4 *Pa, const P4 *Pb, P4 *Pca, P4 *Pcb, cudaStream_t s)
 { if (nc) k_scatter_P<<<GRID(nc)>>>(nc, ccand, Pa, Pb, Pca, Pcb); }
 void launch_to_gid_order(int64_t N, int64_t n_sorted, const uint8_t *own, const uint32_t *gid, const uint32_t *gid_sorted, const double4 *a,

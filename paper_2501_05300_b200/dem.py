@@ -80,7 +80,8 @@ class StepReport(C.Structure):
                 ("n_wall", C.c_int64), ("n_plate", C.c_int64), ("n_degenerate", C.c_int64),
                 ("n_candidates", C.c_int64), ("impact_fired", C.c_int32), ("rebuilt", C.c_int32),
                 ("ke", C.c_double), ("max_v", C.c_double), ("max_disp", C.c_double),
-                ("n_iter", C.c_int32), ("n_iter_impact", C.c_int32), ("n_colors", C.c_int32), ("pad0", C.c_int32)]
+                ("n_iter", C.c_int32), ("n_iter_impact", C.c_int32), ("n_colors", C.c_int32), ("pad0", C.c_int32),
+                ("max_normal_residual", C.c_double), ("max_cone_excess", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
