@@ -96,6 +96,7 @@ struct dem_ctx {
     DevBoundary *db = nullptr;
     unsigned long long *pacc = nullptr;
     unsigned int *pcount = nullptr;
+    unsigned long long *dscr_bad = nullptr;
     StepScalars *dsc = nullptr, *hsc = nullptr;
     uint32_t *hnc = nullptr;
     // status
@@ -939,6 +940,31 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         sc.n_pp = (unsigned)sm[1]; sc.n_wall = (unsigned)sm[2]; sc.n_plate = (unsigned)sm[3]; sc.n_degenerate = (unsigned)sm[4];
     }
     if (sc.nan_flag) {
+        // name the first offending contact (smallest key) or particle, over all ranks
+        unsigned long long bad[2] = {~0ull, ~0ull};
+        if (!ctx->dscr_bad) TRY(A(ctx, &ctx->dscr_bad, 2));
+        launch_first_bad(nc, N, OWN(ctx), ctx->cij, ctx->gid, ctx->Pfa, ctx->Pfb, ctx->pos, ctx->vel[ctx->cur],
+                         ctx->ang[ctx->cur], ctx->dscr_bad, s);
+        CK(cudaMemcpyAsync(bad, ctx->dscr_bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (ctx->tp) {
+            // global minimum of each 64-bit key: high words first, then the low words of the ranks
+            // holding the minimal high word (max of negatives, exact in int64)
+            for (int q = 0; q < 2; q++) {
+                long long hi = -(long long)(bad[q] >> 32);
+                if (!ctx->tp->allreduce_i64(&hi, 1, 1, s, ctx->err)) return DEM_ERR_NCCL;
+                const unsigned long long ghi = (unsigned long long)(-hi);
+                long long lo = (bad[q] >> 32) == ghi ? -(long long)(bad[q] & 0xFFFFFFFFull) : -(1ll << 32);
+                if (!ctx->tp->allreduce_i64(&lo, 1, 1, s, ctx->err)) return DEM_ERR_NCCL;
+                bad[q] = (ghi << 32) | (unsigned long long)(-lo);
+            }
+        }
+        std::string where = "";
+        if (bad[0] != ~0ull)
+            where = " at contact key " + std::to_string(bad[0]) + " (gid " + std::to_string(bad[0] >> 32) + ", partner " +
+                    std::to_string(bad[0] & 0xFFFFFFFFull) + ")";
+        else if (bad[1] != ~0ull)
+            where = " at particle gid " + std::to_string(bad[1] >> 32);
         // atomic step: restore the state of the step start
         if (N) {
             CK(cudaMemcpyAsync(ctx->pos, ctx->pos_prev, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
@@ -949,7 +975,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         TRY(upload_boundary(ctx));
         CK(cudaStreamSynchronize(s));
         ctx->have_step = false;
-        ctx->err = "step " + std::to_string(ctx->step) + " diverged (NaN/Inf); state rolled back";
+        ctx->err = "step " + std::to_string(ctx->step + 1) + " diverged (NaN/Inf)" + where + "; state rolled back";
         return DEM_ERR_DIVERGED;
     }
     launch_scatter_P(nc, ctx->ccand, ctx->Pfa, ctx->Pfb, ctx->Pca, ctx->Pcb, s);

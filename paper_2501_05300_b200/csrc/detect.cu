@@ -409,6 +409,38 @@ __global__ void k_inc_fill(int64_t N, const uint32_t *__restrict__ co_start, con
     }
 }
 
+// divergence diagnostics: the smallest public key among contacts with a non-finite
+// impulse, else the smallest gid among particles with a non-finite state (key = gid << 32 | ~0)
+__global__ void k_first_bad(int64_t nc, int64_t N, const uint8_t *__restrict__ own, const uint2 *__restrict__ cij,
+                            const uint32_t *__restrict__ gid, const P4 *__restrict__ Pa, const P4 *__restrict__ Pb,
+                            const double4 *__restrict__ pos, const double4 *__restrict__ vel,
+                            const double4 *__restrict__ ang, unsigned long long *out)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nc) {
+        const P4 a = Pa[t], b = Pb[t];
+        const bool bad = !isfinite(a.x) || !isfinite(a.y) || !isfinite(a.z) || !isfinite(a.w) || !isfinite(b.x) ||
+                         !isfinite(b.y) || !isfinite(b.z);
+        if (bad && (!own || own[cij[t].x])) {
+            bool flip;
+            atomicMin(&out[0], (unsigned long long)cand_key(cij[t], gid, flip));
+        }
+    }
+    if (t < N && (!own || own[t])) {
+        const double4 x = pos[t], v = vel[t], w = ang[t];
+        if (!isfinite(x.x + x.y + x.z) || !isfinite(v.x + v.y + v.z) || !isfinite(w.x + w.y + w.z))
+            atomicMin(&out[1], ((unsigned long long)gid[t] << 32) | 0xFFFFFFFFull);
+    }
+}
+void launch_first_bad(int64_t nc, int64_t N, const uint8_t *own, const uint2 *cij, const uint32_t *gid, const P4 *Pa,
+                      const P4 *Pb, const double4 *pos, const double4 *vel, const double4 *ang,
+                      unsigned long long *out, cudaStream_t s)
+{
+    cudaMemsetAsync(out, 0xFF, 2 * sizeof(unsigned long long), s);
+    const int64_t n = nc > N ? nc : N;
+    if (n) k_first_bad<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(nc, N, own, cij, gid, Pa, Pb, pos, vel, ang, out);
+}
+
 // ------------------------------------------------------------------ output helpers
 // contacts -> public keys (canonical orientation), values = contact index
 // contacts reported by this rank (owner of the smaller gid; boundary contacts: the particle's

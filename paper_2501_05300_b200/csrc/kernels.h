@@ -76,6 +76,9 @@ void launch_plate_sum(int64_t nc, const uint8_t *own, const uint2 *cij, const G4
                       unsigned int *pcount, cudaStream_t s);
 void launch_boundary(DevBoundary *bnd, const unsigned long long *acc, const unsigned int *pcount, double h, StepScalars *sc,
                      cudaStream_t s);
+void launch_first_bad(int64_t nc, int64_t N, const uint8_t *own, const uint2 *cij, const uint32_t *gid, const P4 *Pa,
+                      const P4 *Pb, const double4 *pos, const double4 *vel, const double4 *ang,
+                      unsigned long long *out, cudaStream_t s);
 void launch_residuals(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const R4 *row, const double4 *vel,
                       const P4 *Pa, const P4 *Pb, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
                       cudaStream_t s);

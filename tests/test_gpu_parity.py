@@ -368,3 +368,31 @@ def test_step_report_residuals_vs_oracle():
     assert ro.max_normal_residual > 0
     assert rep["max_normal_residual"] == pytest.approx(ro.max_normal_residual, rel=0.02)
     assert 0.0 <= rep["max_cone_excess"] <= ro.max_cone_excess + 1e-6 * Pmax
+
+
+def test_divergence_names_first_offending_contact_and_rolls_back():
+    """S:365 / S:385: a NaN in the state makes the step fail atomically; the error names the
+    step and the first offending contact (smallest key among contacts with non-finite impulses).
+    One sweep, no impact stage: exactly the contacts of the poisoned particle go non-finite."""
+    D = dem()
+    bed = synth.random_cloud(300, (0, 0, 0), (0.04, 0.04, 0.04), 1.5e-3, 3e-3, 23, v_scale=0.01)
+    c_ref, _ = oracle_world(bed).detect(oracle_params(1, 1e-5))
+    ka = (c_ref["key"] >> np.uint64(32)).astype(np.int64)
+    kb = (c_ref["key"] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    victim = int(np.bincount(ka, minlength=300)[:300].argmax())          # a particle with contacts
+    mine = (ka == victim) | (kb == victim)
+    expect = int(c_ref["key"][mine].min())
+    v = bed.v.copy()
+    v[np.flatnonzero(bed.gid == victim)[0], 0] = np.nan
+    b = D.Bed(bed.x, bed.r, v, bed.w, bed.gid, box=dict(lo=(0, 0, 0), hi=(0.04, 0.04, 0.04)),
+              solver=dict(dt=1e-5, n_iter=1, v_impact=1e30))
+    try:
+        st0 = b.get_state()
+        with pytest.raises(D.DivergedError) as ei:
+            b.step(1)
+        st1 = b.get_state()
+    finally:
+        b.close()
+    msg = str(ei.value)
+    assert "step 1 diverged" in msg and f"contact key {expect} " in msg, (msg, expect)
+    assert np.array_equal(st0["pos"], st1["pos"])                       # rolled back
