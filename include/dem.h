@@ -283,6 +283,15 @@ dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mo
                            double f_min, double f_max /* N, velocity mode (Eq. 4) */);
 dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *out);
 
+/* Load balance of the x-slab decomposition; collective, a no-op without a
+ * decomposition.  The owned particles' x are histogrammed over the box in n_bins >= 2 bins and
+ * summed over the ranks; each interior face moves toward its particle-count quantile by at most
+ * one Verlet skin (a particle that changes owner and all its last-step contacts, with their
+ * impulse history, are then already held by its new owner: the trajectory stays bit-identical),
+ * interior slabs stay at least one band wide.  Ownership moves at the next step's rebuild.
+ * faces_out (may be NULL): the world_size - 1 new faces.  Call every M steps to converge. */
+dem_status dem_rebalance(dem_ctx *ctx, int32_t n_bins, double *faces_out);
+
 /* Kinematic box wall: velocity along its inward normal (shear-box / servo walls). */
 dem_status dem_drive_wall(dem_ctx *ctx, int32_t wall, double normal_velocity);
 

@@ -90,6 +90,7 @@ struct dem_ctx {
     int64_t nh = 0, cap_h = 0;
     uint64_t *hkey = nullptr;
     P4 *hPa = nullptr, *hPb = nullptr;
+    uint8_t *hauth = nullptr;       // decomposed: this rank owned a body of the history entry
     bool hist_pending = false;
     // boundary
     DevBoundary hb{};
@@ -488,6 +489,7 @@ static dem_status export_history(dem_ctx *ctx)
     if (nh > ctx->cap_h) {
         int64_t cap = nh + nh / 4 + 1024;
         TRY(regrow(ctx, &ctx->hkey, cap)); TRY(regrow(ctx, &ctx->hPa, cap)); TRY(regrow(ctx, &ctx->hPb, cap));
+        TRY(regrow(ctx, &ctx->hauth, cap));
         ctx->cap_h = cap;
     }
     if (nh) {
@@ -495,7 +497,8 @@ static dem_status export_history(dem_ctx *ctx)
         radix_sort_u64(ctx->keys, ctx->vals, nh, 64, ctx->sort_tmp, s, &ctx->launches);
         CK(cudaMemcpyAsync(ctx->hkey, ctx->keys[0], nh * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
         launch_hist_gather(nh, ctx->vals[0], ctx->cand, ctx->gid, ctx->Pca, ctx->Pcb, ctx->hPa, ctx->hPb, s);
-        ctx->launches += 2;
+        if (ctx->tp) launch_hist_auth(nh, ctx->vals[0], ctx->cand, ctx->own, ctx->hauth, s);
+        ctx->launches += ctx->tp ? 3 : 2;
     }
     ctx->nh = nh;
     if (getenv("DEM_DEBUG")) fprintf(stderr, "[dem r%d] export history: ncand %lld nh %u\n", ctx->rank, (long long)nc, nh);
@@ -538,6 +541,108 @@ static dem_status halo(dem_ctx *ctx, double4 *vel, double4 *ang)
 // crossed into a neighbour's slab was a ghost there with a bit-identical state (ghosts move with
 // their owners' velocities), so it is simply owned there from now on: no particle is shipped
 // except as a band copy.  Owned particles come first, ghosts after (left band, right band).
+// History hand-over at a rebuild (dist.cu k_hist_*): after the new local sets are formed, send
+// each neighbour the authoritative history entries (this rank owned a body before the rebuild)
+// whose bodies the neighbour now holds -- its band from us and our band from it -- and merge the
+// received entries over ours (they win for equal keys).
+static dem_status exchange_history(dem_ctx *ctx, int64_t n_own, const uint32_t *tg, const uint32_t nsend[2],
+                                   const unsigned long long rc[2], const int has[2])
+{
+    cudaStream_t s = ctx->s;
+    const int64_t nh = ctx->nh;
+    void *sbuf[2] = {nullptr, nullptr}, *rbuf[2] = {nullptr, nullptr};
+    unsigned long long ns[2] = {0, 0}, nr[2] = {0, 0};
+    uint64_t *B = nullptr;
+    uint32_t *flag = nullptr, *scan = nullptr, *idx = nullptr;
+    const int64_t nBmax = std::max<int64_t>((int64_t)nsend[0] + (int64_t)rc[0], (int64_t)nsend[1] + (int64_t)rc[1]);
+    TRY(ensure_keys(ctx, std::max<int64_t>(nBmax, 1)));
+    TRY(A(ctx, &B, nBmax + 1));
+    TRY(A(ctx, &flag, nh + 2)); TRY(A(ctx, &scan, nh + 2)); TRY(A(ctx, &idx, nh + 2));
+    const int64_t goff[2] = {n_own, n_own + (int64_t)rc[0]};
+    for (int k = 0; k < 2; k++) {
+        if (has[k] && nh) {
+            const int64_t nB = (int64_t)nsend[k] + (int64_t)rc[k];
+            launch_gid_list(nsend[k], ctx->send_pre[k], tg, ctx->keys[0], s);
+            launch_gid_list((int64_t)rc[k], nullptr, ctx->gid + goff[k], ctx->keys[0] + nsend[k], s);
+            if (nB) radix_sort_u64(ctx->keys, ctx->vals, nB, 32, ctx->sort_tmp, s, &ctx->launches);
+            CK(cudaMemcpyAsync(B, ctx->keys[0], nB * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+            launch_hist_select(nh, ctx->hkey, ctx->hauth, B, nB, flag, s);
+            scan_u32(flag, scan, nh, ctx->scan_tmp, s, &ctx->launches);
+            uint32_t cnt = 0;
+            CK(cudaMemcpyAsync(&cnt, scan + nh, 4, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            ns[k] = cnt;
+            TRY(dalloc(ctx, &sbuf[k], std::max<size_t>(cnt, 1) * HIST_REC_BYTES));
+            launch_compact_idx(nh, flag, scan, idx, s);
+            launch_hist_pack(cnt, idx, ctx->hkey, ctx->hPa, ctx->hPb, sbuf[k], s);
+            ctx->launches += 4;
+        } else {
+            TRY(dalloc(ctx, &sbuf[k], HIST_REC_BYTES));
+        }
+    }
+    {   // counts, then the records
+        unsigned long long *cnt = nullptr;
+        TRY(A(ctx, &cnt, 4));
+        CK(cudaMemcpyAsync(cnt, ns, 16, cudaMemcpyHostToDevice, s));
+        CK(cudaMemsetAsync(cnt + 2, 0, 16, s));
+        const void *snd[2] = {cnt, cnt + 1};
+        void *rcv[2] = {cnt + 2, cnt + 3};
+        const size_t sb[2] = {has[0] ? 8u : 0u, has[1] ? 8u : 0u};
+        TRY(xchg(ctx, snd, sb, rcv, sb));
+        CK(cudaMemcpyAsync(nr, cnt + 2, 16, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        dfree(ctx, cnt);
+    }
+    for (int k = 0; k < 2; k++) TRY(dalloc(ctx, &rbuf[k], std::max<size_t>(nr[k], 1) * HIST_REC_BYTES));
+    {
+        const void *snd[2] = {sbuf[0], sbuf[1]};
+        const size_t sb[2] = {(size_t)ns[0] * HIST_REC_BYTES, (size_t)ns[1] * HIST_REC_BYTES};
+        const size_t rb[2] = {(size_t)nr[0] * HIST_REC_BYTES, (size_t)nr[1] * HIST_REC_BYTES};
+        TRY(xchg(ctx, snd, sb, rbuf, rb));
+    }
+    const int64_t total = nh + (int64_t)nr[0] + (int64_t)nr[1];
+    if (total > nh) {
+        // own entries then the received ones, stable-sorted by key; the last of each key is kept
+        TRY(ensure_keys(ctx, total));
+        P4 *ca = nullptr, *cb = nullptr;
+        uint32_t *f2 = nullptr, *s2 = nullptr;
+        TRY(A(ctx, &ca, total)); TRY(A(ctx, &cb, total)); TRY(A(ctx, &f2, total + 1)); TRY(A(ctx, &s2, total + 1));
+        launch_iota_keys(nh, ctx->hkey, ctx->keys[0], ctx->vals[0], s);
+        if (nh) {
+            CK(cudaMemcpyAsync(ca, ctx->hPa, nh * sizeof(P4), cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(cb, ctx->hPb, nh * sizeof(P4), cudaMemcpyDeviceToDevice, s));
+        }
+        int64_t o = nh;
+        for (int k = 0; k < 2; k++) {
+            launch_hist_unpack((int64_t)nr[k], rbuf[k], ctx->keys[0] + o, ctx->vals[0] + o, (uint32_t)o, ca + o, cb + o, s);
+            o += (int64_t)nr[k];
+        }
+        radix_sort_u64(ctx->keys, ctx->vals, total, 64, ctx->sort_tmp, s, &ctx->launches);
+        launch_hist_last(total, ctx->keys[0], f2, s);
+        scan_u32(f2, s2, total, ctx->scan_tmp, s, &ctx->launches);
+        uint32_t nn = 0;
+        CK(cudaMemcpyAsync(&nn, s2 + total, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if ((int64_t)nn > ctx->cap_h) {
+            const int64_t cap = nn + nn / 4 + 1024;
+            TRY(regrow(ctx, &ctx->hkey, cap)); TRY(regrow(ctx, &ctx->hPa, cap)); TRY(regrow(ctx, &ctx->hPb, cap));
+            TRY(regrow(ctx, &ctx->hauth, cap));
+            ctx->cap_h = cap;
+        }
+        launch_hist_emit(total, f2, s2, ctx->keys[0], ctx->vals[0], ca, cb, ctx->hkey, ctx->hPa, ctx->hPb, s);
+        CK(cudaStreamSynchronize(s));
+        ctx->nh = nn;
+        for (void *q : {(void *)ca, (void *)cb, (void *)f2, (void *)s2}) dfree(ctx, q);
+        ctx->launches += 4;
+    }
+    for (int k = 0; k < 2; k++) { dfree(ctx, sbuf[k]); dfree(ctx, rbuf[k]); }
+    for (void *q : {(void *)B, (void *)flag, (void *)scan, (void *)idx}) dfree(ctx, q);
+    if (getenv("DEM_DEBUG"))
+        fprintf(stderr, "[dem r%d] history hand-over: sent %llu/%llu received %llu/%llu -> %lld entries\n", ctx->rank,
+                ns[0], ns[1], nr[0], nr[1], (long long)ctx->nh);
+    return DEM_OK;
+}
+
 static dem_status redistribute(dem_ctx *ctx)
 {
     cudaStream_t s = ctx->s;
@@ -618,6 +723,7 @@ static dem_status redistribute(dem_ctx *ctx)
         off += rc[k];
     }
     CK(cudaStreamSynchronize(s));
+    TRY(exchange_history(ctx, n_own, tg, nsend, rc, has));
     for (void *q : {(void *)flag, (void *)scan, (void *)idx, (void *)tg, (void *)tp, (void *)tv, (void *)tw}) dfree(ctx, q);
     ctx->N = Nn;
     ctx->N_own = n_own;
@@ -1275,6 +1381,7 @@ dem_status dem_set_state(dem_ctx *ctx, const dem_state_view *st, const dem_conta
     if (nh > ctx->cap_h) {
         int64_t cap = nh + 1024;
         TRY(regrow(ctx, &ctx->hkey, cap)); TRY(regrow(ctx, &ctx->hPa, cap)); TRY(regrow(ctx, &ctx->hPb, cap));
+        TRY(regrow(ctx, &ctx->hauth, cap));
         ctx->cap_h = cap;
     }
     if (nh) {
@@ -1284,6 +1391,8 @@ dem_status dem_set_state(dem_ctx *ctx, const dem_state_view *st, const dem_conta
     }
     ctx->nh = nh;
     ctx->hist_pending = true;
+    // the caller's history is global (every rank gets all of it): nothing to hand over
+    if (nh && ctx->hauth) CK(cudaMemsetAsync(ctx->hauth, 0, nh, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     return rebuild(ctx);
 }
@@ -1625,6 +1734,54 @@ void *dem_stream(dem_ctx *ctx) { return ctx ? (void *)ctx->s : nullptr; }
 int64_t dem_num_particles(const dem_ctx *ctx) { return ctx ? ctx->N_own : -1; }
 
 int64_t dem_num_local(const dem_ctx *ctx) { return ctx ? ctx->N : -1; }
+
+dem_status dem_rebalance(dem_ctx *ctx, int32_t n_bins, double *faces_out)
+{
+    if (!ctx || n_bins < 2) return DEM_ERR_INVALID;
+    if (!ctx->tp || ctx->G < 2) return DEM_OK;
+    cudaStream_t s = ctx->s;
+    const int G = ctx->G;
+    const double lo = ctx->box.lo[0], hi = ctx->box.hi[0];
+    // 1. global histogram of the owned particles' x (each particle counted by its owner)
+    unsigned long long *dh = nullptr;
+    TRY(A(ctx, &dh, n_bins));
+    launch_hist_x(ctx->N, OWN(ctx), ctx->pos, lo, hi, n_bins, dh, s);
+    std::vector<long long> h(n_bins);
+    CK(cudaMemcpyAsync(h.data(), dh, n_bins * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    dfree(ctx, dh);
+    for (int o = 0; o < n_bins; o += 64)       // the transports reduce at most 64 values per call
+        if (!ctx->tp->allreduce_i64(h.data() + o, std::min(64, n_bins - o), 0, s, ctx->err)) return DEM_ERR_NCCL;
+    // 2. current faces (face k = slab_lo of rank k), assembled by a sum over ranks
+    std::vector<double> f(G - 1, 0.0);
+    if (ctx->rank > 0) f[ctx->rank - 1] = ctx->slab_lo;
+    for (int o = 0; o < G - 1; o += 64)
+        if (!ctx->tp->allreduce_f64(f.data() + o, std::min(64, G - 1 - o), 0, s, ctx->err)) return DEM_ERR_NCCL;
+    // 3. count quantiles (linear within a bin), each face moved by at most one skin: a particle
+    //    that changes owner lies within a skin of the old face, so all its contacts of the last
+    //    step (partners within 2 r_max) and their impulse history are inside the new owner's
+    //    ghost band (2 r_max + 2 skin) -- no history has to travel; interior slabs stay one band wide
+    long long tot = 0;
+    for (long long v : h) tot += v;
+    const double bw = (hi - lo) / n_bins, step = ctx->grid.skin;
+    std::vector<double> nf(f);
+    for (int k = 0; k < G - 1 && tot > 0; k++) {
+        const double want = (double)tot * (k + 1) / G;
+        double acc = 0.0, t = hi;
+        for (int b = 0; b < n_bins; b++) {
+            if (acc + h[b] >= want) { t = lo + bw * (b + (h[b] ? (want - acc) / h[b] : 0.0)); break; }
+            acc += h[b];
+        }
+        nf[k] = f[k] + std::max(-step, std::min(step, t - f[k]));
+    }
+    for (int k = 1; k < G - 1; k++) nf[k] = std::max(nf[k], nf[k - 1] + ctx->band_w);
+    for (int k = G - 3; k >= 0; k--) nf[k] = std::min(nf[k], nf[k + 1] - ctx->band_w);
+    if (ctx->rank > 0) ctx->slab_lo = nf[ctx->rank - 1];
+    if (ctx->rank < G - 1) ctx->slab_hi = nf[ctx->rank];
+    if (faces_out) for (int k = 0; k < G - 1; k++) faces_out[k] = nf[k];
+    ctx->need_rebuild = true;           // ownership follows the new faces at the next step's rebuild
+    return DEM_OK;
+}
 
 void *dem_loopback_create(int32_t world_size) { return world_size >= 1 ? (void *)new LoopGroup(world_size) : nullptr; }
 

@@ -217,6 +217,130 @@ Transport *make_loop_transport(int rank, LoopGroup *grp, std::string &err)
 // ------------------------------------------------------------------ kernels
 #define GRID(n) (unsigned)(((n) + 255) / 256), 256, 0, s
 
+// ------------------------------------------------------------------ history hand-over
+// A contact's impulse history is authoritative on a rank that owns one of its bodies (that rank
+// has held the contact since it formed).  At every rebuild each rank sends each neighbour the
+// authoritative entries whose bodies the neighbour will hold, so a contact that enters a rank's
+// local set -- a particle migrating, or a pair drifting into the ghost band -- arrives with its
+// history and every rank warm-starts it from the same impulses (bit-identity).
+__global__ void k_hist_auth(int64_t nh, const uint32_t *__restrict__ vals, const uint2 *__restrict__ cand,
+                            const uint8_t *__restrict__ own, uint8_t *__restrict__ auth)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nh) return;
+    const uint2 ij = cand[vals[t]];
+    auth[t] = (own[ij.x] || (!(ij.y & PARTNER_EXT) && own[ij.y])) ? 1 : 0;
+}
+__global__ void k_gid_list(int64_t n, const uint32_t *__restrict__ idx, const uint32_t *__restrict__ gid,
+                           uint64_t *__restrict__ out)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = gid[idx ? idx[t] : t];
+}
+__device__ __forceinline__ bool in_sorted(const uint64_t *__restrict__ a, int64_t n, uint64_t v)
+{
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    return lo < n && a[lo] == v;
+}
+__global__ void k_hist_select(int64_t nh, const uint64_t *__restrict__ hkey, const uint8_t *__restrict__ auth,
+                              const uint64_t *__restrict__ B, int64_t nB, uint32_t *__restrict__ flag)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nh) return;
+    const uint64_t k = hkey[t];
+    const uint32_t ga = (uint32_t)(k >> 32), gb = (uint32_t)k;
+    const bool ext = gb >= PLATE_KEY_BASE;                 // walls and plates: the particle alone
+    flag[t] = (auth[t] && in_sorted(B, nB, ga) && (ext || in_sorted(B, nB, gb))) ? 1u : 0u;
+}
+struct __align__(16) HistRec { unsigned long long key, pad; P4 a, b; };
+__global__ void k_hist_pack(int64_t n, const uint32_t *__restrict__ idx, const uint64_t *__restrict__ hkey,
+                            const P4 *__restrict__ hPa, const P4 *__restrict__ hPb, HistRec *__restrict__ out)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint32_t i = idx[t];
+    out[t] = HistRec{hkey[i], 0ull, hPa[i], hPb[i]};
+}
+__global__ void k_hist_unpack(int64_t n, const HistRec *__restrict__ in, uint64_t *__restrict__ key,
+                              uint32_t *__restrict__ val, uint32_t val0, P4 *__restrict__ Pa, P4 *__restrict__ Pb)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const HistRec r = in[t];
+    key[t] = r.key;
+    val[t] = val0 + (uint32_t)t;
+    Pa[t] = r.a;
+    Pb[t] = r.b;
+}
+__global__ void k_iota_keys(int64_t n, const uint64_t *__restrict__ hkey, uint64_t *__restrict__ key,
+                            uint32_t *__restrict__ val)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) { key[t] = hkey[t]; val[t] = (uint32_t)t; }
+}
+// after a stable sort of (key, entry index): keep the last entry of each key (received entries
+// were appended after the rank's own, so they win); output compacted in key order
+__global__ void k_hist_last(int64_t n, const uint64_t *__restrict__ key, uint32_t *__restrict__ flag)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) flag[t] = (t + 1 == n || key[t + 1] != key[t]) ? 1u : 0u;
+}
+__global__ void k_hist_emit(int64_t n, const uint32_t *__restrict__ flag, const uint32_t *__restrict__ scan,
+                            const uint64_t *__restrict__ key, const uint32_t *__restrict__ val,
+                            const P4 *__restrict__ Pa, const P4 *__restrict__ Pb, uint64_t *__restrict__ okey,
+                            P4 *__restrict__ oPa, P4 *__restrict__ oPb)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n || !flag[t]) return;
+    const uint32_t o = scan[t], v = val[t];
+    okey[o] = key[t];
+    oPa[o] = Pa[v];
+    oPb[o] = Pb[v];
+}
+#define G256(n) (unsigned)(((n) + 255) / 256), 256, 0, s
+void launch_hist_auth(int64_t nh, const uint32_t *vals, const uint2 *cand, const uint8_t *own, uint8_t *auth, cudaStream_t s)
+{ if (nh) k_hist_auth<<<G256(nh)>>>(nh, vals, cand, own, auth); }
+void launch_gid_list(int64_t n, const uint32_t *idx, const uint32_t *gid, uint64_t *out, cudaStream_t s)
+{ if (n) k_gid_list<<<G256(n)>>>(n, idx, gid, out); }
+void launch_hist_select(int64_t nh, const uint64_t *hkey, const uint8_t *auth, const uint64_t *B, int64_t nB, uint32_t *flag,
+                        cudaStream_t s)
+{ if (nh) k_hist_select<<<G256(nh)>>>(nh, hkey, auth, B, nB, flag); }
+void launch_hist_pack(int64_t n, const uint32_t *idx, const uint64_t *hkey, const P4 *hPa, const P4 *hPb, void *out,
+                      cudaStream_t s)
+{ if (n) k_hist_pack<<<G256(n)>>>(n, idx, hkey, hPa, hPb, (HistRec *)out); }
+void launch_hist_unpack(int64_t n, const void *in, uint64_t *key, uint32_t *val, uint32_t val0, P4 *Pa, P4 *Pb,
+                        cudaStream_t s)
+{ if (n) k_hist_unpack<<<G256(n)>>>(n, (const HistRec *)in, key, val, val0, Pa, Pb); }
+void launch_iota_keys(int64_t n, const uint64_t *hkey, uint64_t *key, uint32_t *val, cudaStream_t s)
+{ if (n) k_iota_keys<<<G256(n)>>>(n, hkey, key, val); }
+void launch_hist_last(int64_t n, const uint64_t *key, uint32_t *flag, cudaStream_t s)
+{ if (n) k_hist_last<<<G256(n)>>>(n, key, flag); }
+void launch_hist_emit(int64_t n, const uint32_t *flag, const uint32_t *scan, const uint64_t *key, const uint32_t *val,
+                      const P4 *Pa, const P4 *Pb, uint64_t *okey, P4 *oPa, P4 *oPb, cudaStream_t s)
+{ if (n) k_hist_emit<<<G256(n)>>>(n, flag, scan, key, val, Pa, Pb, okey, oPa, oPb); }
+#undef G256
+
+// histogram of the owned particles' x over [lo, hi) in nb bins (outside: edge bins)
+__global__ void k_hist_x(int64_t n, const uint8_t *__restrict__ own, const double4 *__restrict__ pos, double lo,
+                         double hi, int nb, unsigned long long *__restrict__ hist)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || (own && !own[i])) return;
+    int b = (int)floor((pos[i].x - lo) / (hi - lo) * nb);
+    b = b < 0 ? 0 : (b >= nb ? nb - 1 : b);
+    atomicAdd(&hist[b], 1ull);
+}
+void launch_hist_x(int64_t n, const uint8_t *own, const double4 *pos, double lo, double hi, int nb,
+                   unsigned long long *hist, cudaStream_t s)
+{
+    cudaMemsetAsync(hist, 0, nb * sizeof(unsigned long long), s);
+    if (n) k_hist_x<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, own, pos, lo, hi, nb, hist);
+}
+
 __global__ void k_slab_flags(int64_t n, const double4 *__restrict__ pos, double lo, double hi, uint32_t *__restrict__ flag)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

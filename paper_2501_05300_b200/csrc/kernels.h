@@ -76,6 +76,22 @@ void launch_plate_sum(int64_t nc, const uint8_t *own, const uint2 *cij, const G4
                       unsigned int *pcount, cudaStream_t s);
 void launch_boundary(DevBoundary *bnd, const unsigned long long *acc, const unsigned int *pcount, double h, StepScalars *sc,
                      cudaStream_t s);
+// dist.cu: history hand-over at rebuilds (HistRec = 48 bytes: key, pad, P_a, P_b)
+constexpr size_t HIST_REC_BYTES = 48;
+void launch_hist_auth(int64_t nh, const uint32_t *vals, const uint2 *cand, const uint8_t *own, uint8_t *auth, cudaStream_t s);
+void launch_gid_list(int64_t n, const uint32_t *idx, const uint32_t *gid, uint64_t *out, cudaStream_t s);
+void launch_hist_select(int64_t nh, const uint64_t *hkey, const uint8_t *auth, const uint64_t *B, int64_t nB, uint32_t *flag,
+                        cudaStream_t s);
+void launch_hist_pack(int64_t n, const uint32_t *idx, const uint64_t *hkey, const P4 *hPa, const P4 *hPb, void *out,
+                      cudaStream_t s);
+void launch_hist_unpack(int64_t n, const void *in, uint64_t *key, uint32_t *val, uint32_t val0, P4 *Pa, P4 *Pb,
+                        cudaStream_t s);
+void launch_iota_keys(int64_t n, const uint64_t *hkey, uint64_t *key, uint32_t *val, cudaStream_t s);
+void launch_hist_last(int64_t n, const uint64_t *key, uint32_t *flag, cudaStream_t s);
+void launch_hist_emit(int64_t n, const uint32_t *flag, const uint32_t *scan, const uint64_t *key, const uint32_t *val,
+                      const P4 *Pa, const P4 *Pb, uint64_t *okey, P4 *oPa, P4 *oPb, cudaStream_t s);
+void launch_hist_x(int64_t n, const uint8_t *own, const double4 *pos, double lo, double hi, int nb,
+                   unsigned long long *hist, cudaStream_t s);
 void launch_first_bad(int64_t nc, int64_t N, const uint8_t *own, const uint2 *cij, const uint32_t *gid, const P4 *Pa,
                       const P4 *Pb, const double4 *pos, const double4 *vel, const double4 *ang,
                       unsigned long long *out, cudaStream_t s);

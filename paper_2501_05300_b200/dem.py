@@ -126,7 +126,7 @@ CONTACT_DTYPE = np.dtype([("key", "<u8"), ("n", "<f8", (3,)), ("delta", "<f8"), 
 # every symbol include/dem.h declares (checked by tests/test_boundary.py)
 EXPORTS = ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts", "dem_get_forces",
            "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_get_wall", "dem_set_timing",
-           "dem_get_timing",
+           "dem_get_timing", "dem_rebalance",
            "dem_reset_timing", "dem_bench_sweeps", "dem_num_particles", "dem_num_local", "dem_nccl_unique_id",
            "dem_loopback_create", "dem_loopback_destroy", "dem_generator_count", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
            "dem_contact_network_length", "dem_plan_iterations", "dem_plan_timestep"]
@@ -154,6 +154,8 @@ def lib():
         L.dem_get_plate.argtypes = [vp, i32, C.POINTER(PlateState)]
         L.dem_drive_wall.argtypes = [vp, i32, d]
         L.dem_get_wall.argtypes = [vp, i32, C.POINTER(WallState)]
+        L.dem_rebalance.argtypes = [vp, i32, C.POINTER(C.c_double)]
+        L.dem_rebalance.restype = C.c_int
         L.dem_set_timing.argtypes = [vp, i32]
         L.dem_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.dem_reset_timing.argtypes = [vp]
@@ -350,6 +352,7 @@ class Bed:
         dist.rank, dist.world_size = 0, 1
         if dcfg:                   # decomposed (world_size 1 with a transport: the transport self-test)
             dist.rank, dist.world_size = int(dcfg["rank"]), int(dcfg["world_size"])
+            self._world = dist.world_size
             dist.slab_lo, dist.slab_hi = float(dcfg["slab"][0]), float(dcfg["slab"][1])
             if dcfg.get("transport", "nccl") == "loopback":
                 dist.transport, dist.loopback = 1, dcfg["group"].handle
@@ -507,6 +510,14 @@ class Bed:
         self._check(lib().dem_get_plate(self._h, plate, C.byref(s)))
         return {"pos": list(s.pos), "vel": list(s.vel), "force": list(s.force),
                 "motor_force": list(s.motor_force), "n_contacts": s.n_contacts}
+
+    def rebalance(self, n_bins=1024, world_size=None):
+        """dem_rebalance (collective): slab faces toward particle-count quantiles; returns the
+        new interior faces (world_size - 1 values; [] without a decomposition)."""
+        g = world_size or getattr(self, "_world", 1)
+        out = (C.c_double * max(g - 1, 1))()
+        self._check(lib().dem_rebalance(self._h, int(n_bins), out))
+        return list(out)[: g - 1]
 
     def get_wall(self, wall):
         """dem_get_wall: plane point, inward normal, normal velocity, contact reaction [N]."""

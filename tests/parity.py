@@ -135,7 +135,7 @@ def compare_step(bed, n_it=30, dt=1e-5, with_walls=True, hist=None, material=Non
     return res
 
 
-def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bounds=None):
+def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bounds=None, rebalance_every=0):
     """Run bed split into G x-slabs as G loopback ranks of this process (one host thread each,
     include/dem.h dem_loopback_create), n_steps; returns merged state (gid order), the merged
     contact list (key order), per-rank reports and the slab bounds."""
@@ -157,8 +157,14 @@ def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bo
                         dist=dict(rank=r, world_size=G, slab=(bounds[r], bounds[r + 1]), transport="loopback",
                                   group=grp))
             pids = [b.add_plate(**p) for p in plates]
-            reps = [b.step(1) for _ in range(n_steps)]
+            reps, faces, owned = [], [], []
+            for k in range(n_steps):
+                if rebalance_every and k % rebalance_every == 0:
+                    faces.append(b.rebalance(256))
+                reps.append(b.step(1))
+                owned.append(b.n_owned)
             res[r] = dict(state=b.get_state(), contacts=b.get_contacts(), forces=b.get_forces(), reports=reps,
+                          faces=faces, owned=owned,
                           plates=[b.get_plate(p) for p in pids], n_local=b.n_local, n_owned=b.n_owned,
                           walls=[b.get_wall(w) for w in range(6) if (box.get("wall_mask", 0x3F) >> w) & 1])
         except Exception as e:   # noqa: BLE001 -- surfaced by the caller

@@ -168,3 +168,43 @@ def test_contiguous_reduction_matches_to_rounding_only():
     vs = np.abs(ref["state"]["vel"]).max()
     assert np.abs(out["state"]["vel"] - ref["state"]["vel"]).max() <= 1e-9 * vs
     assert np.array_equal(out["contacts"]["key"], ref["contacts"]["key"])
+
+
+def test_rebalance_moves_faces_to_quantiles_bit_identically():
+    """dem_rebalance: from a lopsided split (rank 2 owns 2/3 of the bed) the
+    faces walk toward the particle-count quantiles, at most one skin per call (a migrating
+    particle's contacts and their history are then already on its new owner), and the
+    trajectory stays bit-identical to the single context."""
+    bed, box = drifting_bed(drift=0.0, seed=9)
+    solver = dict(dt=2e-5, n_iter=20)
+    n_steps = 60
+    ref = single(bed, n_steps, solver, box)
+    out = run_loopback(bed, 3, n_steps, solver, box, bounds=[0.0, 0.02, 0.04, 0.12], rebalance_every=1)
+    for k in ("gid", "pos", "vel", "angvel"):
+        assert np.array_equal(out["state"][k], ref["state"][k]), k
+    first = [r["owned"][0] for r in out["ranks"]]
+    last = [r["owned"][-1] for r in out["ranks"]]
+    assert sum(first) == sum(last) == len(bed.r)
+    print("owned first", first, "last", last, "faces", out["ranks"][0]["faces"][-1])
+    assert max(first) / min(first) > 3
+    assert max(last) < max(first) and min(last) > min(first)            # moving toward balance
+    f = [r["faces"] for r in out["ranks"]]
+    assert all(fi == f[0] for fi in f)                                  # every rank agrees
+    F = np.array(f[0])
+    assert np.all(np.diff(F, axis=0) >= 0)                               # monotone toward the quantiles
+    assert np.abs(np.diff(F, axis=0)).max() <= 0.1 * bed.r.min() * (1 + 1e-9)   # one skin per call
+
+
+@pytest.mark.parametrize("drift,G", [(5.0, 2), (-5.0, 3)])
+def test_long_drift_hands_over_contact_history(drift, G):
+    """The bed drifts 10 mm (two and a half lattice planes) through the faces over 100 steps:
+    contacts that formed on one rank enter the neighbour's ghost band and particles change owner
+    with their contacts' impulse history (handed over at the rebuilds).  Bit-identical to the
+    single context."""
+    bed, box = drifting_bed(drift=drift)
+    solver = dict(dt=2e-5, n_iter=30)
+    ref = single(bed, 100, solver, box)
+    out = run_loopback(bed, G, 100, solver, box, bounds=[0.0] + [0.12 * k / G + 3e-4 for k in range(1, G)] + [0.12])
+    for k in ("gid", "pos", "vel", "angvel"):
+        assert np.array_equal(out["state"][k], ref["state"][k]), k
+    assert np.array_equal(out["contacts"]["P"], ref["contacts"]["P"])
