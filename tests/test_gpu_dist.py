@@ -208,3 +208,16 @@ def test_long_drift_hands_over_contact_history(drift, G):
     for k in ("gid", "pos", "vel", "angvel"):
         assert np.array_equal(out["state"][k], ref["state"][k]), k
     assert np.array_equal(out["contacts"]["P"], ref["contacts"]["P"])
+
+
+def test_long_list_particle_on_a_face_bit_identical():
+    """A 12 mm sphere with > 100 contacts straddling a slab face (its list is packed in pieces on
+    its owner and its contacts are evaluated on both ranks): bit-identical to one context."""
+    from tests.test_gpu_parity import _big_sphere_bed
+    bed = _big_sphere_bed()
+    box = dict(lo=(0.0, 0.0, 0.0), hi=(0.06, 0.06, 0.06), wall_mask=0x3F)
+    solver = dict(dt=1e-5, n_iter=40)
+    ref = single(bed, 10, solver, box)
+    out = run_loopback(bed, 2, 10, solver, box, bounds=[0.0, 0.0301, 0.06])
+    for k in ("gid", "pos", "vel", "angvel"):
+        assert np.array_equal(out["state"][k], ref["state"][k]), k

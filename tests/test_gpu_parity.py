@@ -396,3 +396,37 @@ def test_divergence_names_first_offending_contact_and_rolls_back():
     msg = str(ei.value)
     assert "step 1 diverged" in msg and f"contact key {expect} " in msg, (msg, expect)
     assert np.array_equal(st0["pos"], st1["pos"])                       # rolled back
+
+
+def _big_sphere_bed():
+    """One 12 mm sphere inside a shell of 1.5 mm spheres pressed onto it (overlapping slightly),
+    plus a loose cloud: the big sphere's contact list has far more than 32 entries, so the
+    packed sweep cuts it into 32-entry pieces (sweep_t2.cu long-list path)."""
+    rng = np.random.default_rng(7)
+    R, r = 0.012, 1.5e-3
+    c = np.array([0.03, 0.03, 0.03])
+    n = 140
+    k = np.arange(n) + 0.5                                       # Fibonacci sphere directions
+    phi = np.arccos(1 - 2 * k / n)
+    th = np.pi * (1 + 5 ** 0.5) * k
+    d = np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], axis=1)
+    shell = c + (R + r - 2e-5) * d
+    cloud = synth.random_cloud(200, (0.0, 0.0, 0.0), (0.06, 0.06, 0.06), 1.2e-3, 2e-3, 8)
+    far = np.linalg.norm(cloud.x - c, axis=1) > R + 5e-3
+    x = np.concatenate([c[None], shell, cloud.x[far]])
+    rr = np.concatenate([[R], np.full(n, r), cloud.r[far]])
+    v = rng.normal(0, 0.01, x.shape)
+    b = synth.Bed(x=x, r=rr, v=v, w=np.zeros_like(x), gid=np.arange(len(rr), dtype=np.uint32),
+                  box_lo=(0.0, 0.0, 0.0), box_hi=(0.06, 0.06, 0.06), name="big-sphere")
+    return b
+
+
+def test_long_contact_list_vs_oracle():
+    bed = _big_sphere_bed()
+    res = compare_step(bed, n_it=40, dt=1e-5, n_steps=2)
+    assert res["pairs_equal"], res
+    assert res["force_err"] <= TOL_F and res["torque_err"] <= TOL_F, res
+    c_ref, _ = oracle_world(bed).detect(oracle_params(1, 1e-5))
+    ka = (c_ref["key"] >> np.uint64(32)).astype(np.int64)
+    kb = (c_ref["key"] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    assert int(((ka == 0) | (kb == 0)).sum()) > 100                    # > 3 chunks of 32
