@@ -85,6 +85,12 @@ struct dem_ctx {
     P8 *p8[2] = {nullptr, nullptr};
     int64_t pk_cap = 0, pk_n = 0;
     PackedInc pkv{};
+    // CUDA graphs of the packed sweep loops (single context): re-captured when a pointer, the
+    // particle count, the sweep count, the start parity or the solver parameters change
+    struct SweepGraph { cudaGraphExec_t exec = nullptr; std::vector<unsigned char> key; };
+    SweepGraph g_imp[4], g_main[4];   // small LRU caches (start parity, ping-pong pointer sets)
+    int64_t g_tick = 0;
+    int64_t g_used[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
     uint2 *inc = nullptr;
     // history
     int64_t nh = 0, cap_h = 0;
@@ -846,6 +852,72 @@ static dem_status pack_incidence(dem_ctx *ctx, int64_t N)
     return DEM_OK;
 }
 
+// Runs n packed sweeps (impulses ping-pong in p8[0/1] from p8[0]; velocities from vel[cur]),
+// replaying a captured CUDA graph when the launch configuration is unchanged (single context:
+// the sweep loop has no host step between launches).  ctx->cur ends n sweeps later.
+static dem_status packed_sweeps(dem_ctx *ctx, int stage, int n, const R4 *rows, const SolveParams &sp)
+{
+    cudaStream_t s = ctx->s;
+    const int64_t N = ctx->N;
+    const int c0 = ctx->cur;
+    auto body = [&]() {
+        for (int it = 0; it < n; it++) {
+            const int a = c0 ^ (it & 1);
+            ctx->pkv.row = rows;
+            ctx->pkv.p8in = ctx->p8[it & 1];
+            ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
+            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[a], ctx->ang[a], ctx->vel[a ^ 1], ctx->ang[a ^ 1],
+                         ctx->inc_start, ctx->inc, &ctx->pkv, ctx->geo, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         ctx->db, sp, s);
+        }
+    };
+    if (ctx->tp || n < 2 || getenv("DEM_NO_GRAPHS")) {
+        for (int it = 0; it < n; it++) {
+            const int a = ctx->cur;
+            ctx->pkv.row = rows;
+            ctx->pkv.p8in = ctx->p8[it & 1];
+            ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
+            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[a], ctx->ang[a], ctx->vel[a ^ 1], ctx->ang[a ^ 1],
+                         ctx->inc_start, ctx->inc, &ctx->pkv, ctx->geo, nullptr, nullptr, nullptr, nullptr, nullptr,
+                         ctx->db, sp, s);
+            ctx->cur ^= 1;
+            TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
+        }
+        return DEM_OK;
+    }
+    // key: everything the captured launches bake in
+    const void *ptrs[] = {ctx->vel[0], ctx->vel[1], ctx->ang[0], ctx->ang[1], ctx->inc_start, ctx->pk_inc, ctx->pk_start,
+                          ctx->pk_wbase, ctx->pk_geo, rows, ctx->p8[0], ctx->p8[1], ctx->db};
+    const int64_t ints[] = {N, n, c0};
+    std::vector<unsigned char> key(sizeof(ptrs) + sizeof(ints) + sizeof(SolveParams));
+    std::memcpy(key.data(), ptrs, sizeof(ptrs));
+    std::memcpy(key.data() + sizeof(ptrs), ints, sizeof(ints));
+    std::memcpy(key.data() + sizeof(ptrs) + sizeof(ints), &sp, sizeof(SolveParams));
+    dem_ctx::SweepGraph *cache = stage ? ctx->g_main : ctx->g_imp;
+    int64_t *used = ctx->g_used[stage ? 1 : 0];
+    int slot = -1, lru = 0;
+    for (int q = 0; q < 4; q++) {
+        if (cache[q].exec && cache[q].key == key) slot = q;
+        if (used[q] < used[lru]) lru = q;
+    }
+    if (slot < 0) slot = lru;
+    dem_ctx::SweepGraph &g = cache[slot];
+    used[slot] = ++ctx->g_tick;
+    if (!g.exec || g.key != key) {
+        if (g.exec) { cudaGraphExecDestroy(g.exec); g.exec = nullptr; }
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        body();
+        CK(cudaStreamEndCapture(s, &graph));
+        CK(cudaGraphInstantiate(&g.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        g.key = key;
+    }
+    CK(cudaGraphLaunch(g.exec, s));
+    ctx->cur = c0 ^ (n & 1);
+    return DEM_OK;
+}
+
 static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
 {
     cudaStream_t s = ctx->s;
@@ -922,10 +994,10 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         if (PKV(ctx)) {   // canonical reduction: packed rows, impulses in 32-byte slots
             pack_rows(ctx->pk_n, ctx->pk_inc, ctx->geo, ctx->row_imp, ctx->pk_geo, ctx->pk_rowi, s);
             CK(cudaMemsetAsync(ctx->p8[0], 0, nc * sizeof(P8), s));
-            ctx->pkv.row = ctx->pk_rowi;
             ctx->launches += 1;
+            TRY(packed_sweeps(ctx, 0, n_imp, ctx->pk_rowi, sp));
         }
-        for (int it = 0; it < n_imp; it++) {
+        for (int it = 0; it < (PKV(ctx) ? 0 : n_imp); it++) {
             const int pi = it & 1;
             ctx->pkv.p8in = ctx->p8[pi];
             ctx->pkv.p8out = ctx->p8[pi ^ 1];
@@ -970,7 +1042,8 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         pin_a = ctx->Pa[0];
         pin_b = ctx->Pb[0];
     }
-    for (int it = 0; it < (gs ? 0 : n_it); it++) {
+    if (pk) TRY(packed_sweeps(ctx, 1, n_it, ctx->pk_row, sp));
+    for (int it = 0; it < ((gs || pk) ? 0 : n_it); it++) {
         P4 *oa = ctx->Pa[it & 1], *ob = ctx->Pb[it & 1];
         ctx->pkv.p8in = ctx->p8[it & 1];
         ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
@@ -1799,6 +1872,9 @@ dem_status dem_destroy(dem_ctx *ctx)
 {
     if (!ctx) return DEM_ERR_INVALID;
     if (ctx->s) cudaStreamSynchronize(ctx->s);
+    for (int q = 0; q < 4; q++)
+        for (auto *g : {&ctx->g_imp[q], &ctx->g_main[q]})
+            if (g->exec) cudaGraphExecDestroy(g->exec);
     std::vector<void *> all = ctx->allocs;
     for (void *p : all) dfree(ctx, p);
     for (int e = 0; e < 8; e++) if (ctx->ev[e]) cudaEventDestroy(ctx->ev[e]);
