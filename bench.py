@@ -222,9 +222,19 @@ def main():
         bed.step(args.settle)             # coarse relaxation of the jammed packing (not timed)
     bed.set_solver(dt=w["dt"], n_iter=n_it, ordering=1 if args.ordering == "gs" else 0,
                    reduction=0 if args.reduction == "canonical" else 1)
+    wrep = None
     for _ in range(args.warmup):
-        bed.step(1)
+        wrep = bed.step(1)
     stream = bed.stream
+    # timing rule: inputs larger than L2, else flush L2 between timed steps (outside the events)
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    ws = ALG_B_PARTICLE * (N_total / world) + ALG_B_CONTACT * (wrep["n_contacts"] / world if wrep else 0)
+    flush = None
+    if ws < 2 * l2:
+        flush = torch.empty(4 * l2, dtype=torch.uint8, device=f"cuda:{local}")
+    l2_note = (f"per-sweep working set {ws / 1e6:.0f} MB < 2 x L2 ({l2 / 1e6:.0f} MB): L2 flushed between timed steps "
+               "(4 x L2 written outside the timed events)") if flush is not None else \
+        "inputs larger than L2 (no flush needed)"
     bed.set_timing(True)
     bed.reset_timing()
     clocks = ClockSampler(local)
@@ -233,16 +243,29 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
     reps = []
-    for _ in range(args.steps):
-        reps.append(bed.step(1))
-    e1.record(stream)
-    torch.cuda.synchronize()
+    if flush is None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            reps.append(bed.step(1))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    else:
+        ev = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            reps.append(bed.step(1))
+            b.record(stream)
+            ev.append((a, b))
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in ev)
     if dist:
         dist.barrier()
-    ms = e0.elapsed_time(e1)
     ck = clocks.stop() if not args.profile else None
     tm = bed.timing()
     if dist:
@@ -276,7 +299,7 @@ def main():
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "levels": len(w["bands"]),
                    "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)"
                    if (world > 1 or args.decompose) else "single GPU",
-                   "l2": "inputs larger than L2 (no flush needed)",
+                   "l2": l2_note,
                    "precision": "fp64 state and row math; fp64 normals/rows, fp32 impulses",
                    "ordering": "coloured Gauss-Seidel" if args.ordering == "gs" else "Jacobi (mass splitting)",
                    "reduction": args.reduction},
