@@ -1666,40 +1666,6 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     TRY(A(ctx, &md, 2));
     launch_row_bias(nc, ctx->row, cb, s);
     launch_tile_order(N, ctx->inc_start, ctx->order, s);
-    // tile-paired incidence (variants 20/21: tiles of 128/256 particles)
-    uint32_t *ca6 = nullptr, *bs6 = nullptr, *xc6 = nullptr, *xs6 = nullptr, *bsl6 = nullptr;
-    uint2 *xl6 = nullptr;
-    unsigned int *mb6 = nullptr, maxb = 0;
-    const int tile6 = variant == 21 ? 256 : 128;
-    if (variant >= 20) {
-        TRY(A(ctx, &ca6, N + 2)); TRY(A(ctx, &bs6, N + 2)); TRY(A(ctx, &xc6, N + 2)); TRY(A(ctx, &xs6, N + 2));
-        TRY(A(ctx, &bsl6, nc + 1)); TRY(A(ctx, &xl6, nc + 1)); TRY(A(ctx, &mb6, 1));
-        launch_inc6(N, tile6, ctx->co_start, ctx->cscan, ctx->inc_start, ctx->inc, ca6, bs6, xc6, xs6, bsl6, xl6, mb6,
-                    ctx->scan_tmp, s, &ctx->launches);
-        CK(cudaMemcpyAsync(&maxb, mb6, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-    }
-    uint4 *xl9 = nullptr;
-    unsigned int caps9[3] = {0, 0, 0};
-    if (variant == 50) {
-        TRY(A(ctx, &ca6, N + 2)); TRY(A(ctx, &xc6, N + 2)); TRY(A(ctx, &xs6, N + 2)); TRY(A(ctx, &xl9, nc + 1));
-        TRY(A(ctx, &mb6, 3));
-        launch_inc9(N, ctx->co_start, ctx->cscan, ctx->inc_start, ctx->inc, ca6, xc6, xs6, xl9, mb6, ctx->scan_tmp, s,
-                    &ctx->launches);
-        CK(cudaMemcpyAsync(caps9, mb6, 12, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        if (getenv("DEM_DEBUG"))
-            fprintf(stderr, "[dem] sweep9 tile %d caps A %u X %u smem %zu B\n", sweep9_tile(), caps9[0], caps9[1],
-                    sweep9_smem_bytes(caps9[0], caps9[1], caps9[2]));
-    }
-    uint4 *xl8 = nullptr;
-    if (variant == 30) {
-        TRY(A(ctx, &xl8, nc + 1));
-        launch_inc8(N, ctx->co_start, ctx->cscan, ctx->inc_start, ctx->inc, ca6, bs6, xc6, xs6, bsl6, xl8, mb6,
-                    ctx->scan_tmp, s, &ctx->launches);
-        CK(cudaMemcpyAsync(&maxb, mb6, 4, cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-    }
     P4 *spa = ctx->Pfa == ctx->Pa[0] ? ctx->Pa[1] : ctx->Pa[0];
     P4 *spb = ctx->Pfb == ctx->Pb[0] ? ctx->Pb[1] : ctx->Pb[0];
     double4 *vbuf[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel2}, *wbuf[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang2};
@@ -1734,9 +1700,6 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
             dfree(ctx, scr);
             dfree(ctx, r3);
             dfree(ctx, cb); dfree(ctx, ref); dfree(ctx, md);
-            for (void *q : {(void *)ca6, (void *)bs6, (void *)xc6, (void *)xs6, (void *)bsl6, (void *)xl6, (void *)mb6,
-                            (void *)xl8, (void *)xl9})
-                dfree(ctx, q);
             return DEM_OK;
         }
         const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
@@ -1755,18 +1718,6 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
                 set_sweep_variant(var);
                 launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, vi, wi, vo, wo, ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row,
                              pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
-            } else if (var == 50) {
-                launch_sweep9(N, caps9[0], caps9[1], caps9[2], vi, wi, vo, wo, ca6, xs6, xl9, ctx->inc_start, ctx->inc, ctx->cij,
-                              ctx->geo, ctx->row, pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
-            } else if (var == 30) {
-                launch_sweep8(N, maxb, vi, wi, vo, wo, ca6, bs6, xs6, xl8, ctx->cij, bsl6, ctx->geo, ctx->row, pai, pbi, pao,
-                              pbo, ctx->db, ctx->sp, s);
-            } else if (var == 22) {
-                launch_sweep7(N, maxb, vi, wi, vo, wo, ca6, bs6, xs6, xl6, ctx->cij, bsl6, ctx->geo, ctx->row, pai, pbi, pao,
-                              pbo, ctx->db, ctx->sp, s);
-            } else if (var >= 20) {
-                launch_sweep6(tile6, false, N, maxb, ctx->pos_prev, vi, wi, vo, wo, ca6, bs6, xs6, xl6, ctx->cij, bsl6, cb,
-                              pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
             } else {
                 // geometry from the positions the step's sweeps saw (before integration)
                 launch_sweep5(var - 10, false, N, ctx->order, ctx->pos_prev, vi, wi, vo, wo, ctx->inc_start, ctx->inc, cb,
@@ -1798,7 +1749,7 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     dfree(ctx, cb);
     dfree(ctx, ref);
     dfree(ctx, md);
-    for (void *q : {(void *)ca6, (void *)bs6, (void *)xc6, (void *)xs6, (void *)bsl6, (void *)xl6, (void *)mb6, (void *)xl8, (void *)xl9}) dfree(ctx, q);
+
     return DEM_OK;
 }
 

@@ -116,41 +116,11 @@ void launch_sweep5(int kind, bool impact, int64_t N, const uint32_t *order, cons
 void launch_row_bias(int64_t nc, const R4 *row, double *cb, cudaStream_t s);
 void launch_maxdiff(int64_t N, const double4 *a, const double4 *b, unsigned long long *out, cudaStream_t s);
 
-// sweep6.cu: tile-paired sweep (intra-tile contacts evaluated once) and its per-step incidence
-void launch_inc6(int64_t N, int tile, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start,
-                 const uint2 *inc, uint32_t *ca, uint32_t *bstart, uint32_t *xcnt, uint32_t *xstart, uint32_t *bslot,
-                 uint2 *xlist, unsigned int *max_b, void *scan_tmp, cudaStream_t s, long long *launches);
-size_t sweep6_smem_bytes(int tile, unsigned max_b);
-void launch_sweep6(int tile, bool impact, int64_t N, unsigned max_b, const double4 *pos, const double4 *vin,
-                   const double4 *win, double4 *vout, double4 *wout, const uint32_t *ca, const uint32_t *bstart,
-                   const uint32_t *xstart, const uint2 *xlist, const uint2 *cij, const uint32_t *bslot,
-                   const double *cb, const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
-                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
-// sweep6.cu (v8): slot sweep, block-strided items, no segmented scan
-void launch_inc8(int64_t N, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start, const uint2 *inc,
-                 uint32_t *ca, uint32_t *bstart, uint32_t *xcnt, uint32_t *xstart, uint32_t *bslot, uint4 *xlist,
-                 unsigned int *max_slots, void *scan_tmp, cudaStream_t s, long long *launches);
-size_t sweep8_smem_bytes(unsigned max_slots);
-void launch_sweep8(int64_t N, unsigned max_slots, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
-                   const uint32_t *ca, const uint32_t *bstart, const uint32_t *xstart, const uint4 *xlist,
-                   const uint2 *cij, const uint32_t *bslot, const G4 *geo, const R4 *row, const P4 *Pa_in,
-                   const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
 // sweep_t2.cu: tile sweep with 256-bit records and conflict-free shared staging
 void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
                      const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo, const R4 *row,
                      const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd,
                      const SolveParams &sp, cudaStream_t s);
-// sweep9.cu: staged tile sweep (each contact once per tile, cp.async staging, reduction from increments)
-void launch_inc9(int64_t N, const uint32_t *co_start, const uint32_t *cscan, const uint32_t *inc_start, const uint2 *inc,
-                 uint32_t *ca, uint32_t *xcnt, uint32_t *xstart, uint4 *xlist, unsigned int *caps, void *scan_tmp,
-                 cudaStream_t s, long long *launches);
-size_t sweep9_smem_bytes(unsigned capA, unsigned capX, unsigned capI);
-int sweep9_tile();
-void launch_sweep9(int64_t N, unsigned capA, unsigned capX, unsigned capI, const double4 *vin, const double4 *win, double4 *vout,
-                   double4 *wout, const uint32_t *ca, const uint32_t *xstart, const uint4 *xlist,
-                   const uint32_t *inc_start, const uint2 *inc, const uint2 *cij, const G4 *geo, const R4 *row,
-                   const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd,
-                   const SolveParams &sp, cudaStream_t s);
 void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin, const double4 *win, double4 *vbuf[2],
                   double4 *wbuf[2], const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
                   P4 *Pa[2], P4 *Pb[2], void *scratch, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s,
@@ -159,10 +129,6 @@ void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin,
 bool generate_bed(const dem_generator &g, const dem_box &box, double slab_lo, double slab_hi,
                   void *(*alloc)(size_t, void *), void *actx, cudaStream_t s, double **x, double **r, uint32_t **gid,
                   int64_t *n, std::string &err);
-void launch_sweep7(int64_t N, unsigned max_b, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
-                   const uint32_t *ca, const uint32_t *bstart, const uint32_t *xstart, const uint2 *xlist,
-                   const uint2 *cij, const uint32_t *bslot, const G4 *geo, const R4 *row, const P4 *Pa_in,
-                   const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
 // gs.cu: coloured Gauss-Seidel ordering
 int gs_color(int64_t nc, const uint2 *cij, const uint32_t *gid, const uint32_t *inc_start, const uint2 *inc,
              uint64_t *key, int *color, uint64_t *keys[2], uint32_t *vals[2], void *sort_tmp, unsigned int *dscr,
