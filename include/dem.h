@@ -317,7 +317,7 @@ dem_status dem_reset_timing(dem_ctx *ctx);
  * (0 shipped k_sweep_t2 with the context's reduction, 7 contiguous k_sweep_t2, 8 packed with
  * contact-indexed rows, 1 cp.async pipeline, 2 particle-per-thread, 3 tile with L1 prefetch, 4
  * first tile kernel; 10/11/12 the geometry-recomputing kernels of sweep5.cu; 41-43 timing
- * experiments; 60-64 layout experiments; 20-59 retired: DEM_ERR_INVALID) on the
+ * experiments; 60-64 layout experiments; 20-39 and 50-59 retired: DEM_ERR_INVALID) on the
  * last step's contacts, from the current velocities and the last step's final impulses.
  * Outputs: device ms per sweep, and max |v - v_ref| / max |v_ref| after n sweeps against
  * variant 0.  The particle state and contact getters are unchanged.  DEM_ERR_STATE before any
