@@ -1704,7 +1704,7 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
         }
         const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
         P4 *pai = ctx->Pwa, *pbi = ctx->Pwb, *pao = spa, *pbo = spb;
-        if ((var == 0 || var == 8) && PKV(ctx)) {
+        if ((var == 0 || var == 8 || var == 44 || var == 45) && PKV(ctx)) {
             p8_pack(nc, ctx->Pwa, ctx->Pwb, ctx->p8[0], s);
             ctx->pkv.geo = var == 8 ? ctx->geo : ctx->pk_geo;
             ctx->pkv.row = var == 8 ? ctx->row : ctx->pk_row;

@@ -47,6 +47,7 @@ void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const do
 // packed incidence of the canonical reduction (sweep_t2.cu): entries in 32-lane chunks, start[i]
 // = packed position of particle i's list, wbase[g] = first packed entry of warp g's particles
 extern bool g_t2_rows_by_contact;
+extern int g_t2_exp;
 struct PackedInc {
     const uint2 *inc;
     const uint32_t *start;

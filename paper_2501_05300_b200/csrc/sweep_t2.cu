@@ -30,6 +30,7 @@ __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { retu
 // every decomposition and warp grouping produces the same bits.
 constexpr uint32_t PK_HOLE = 0xFFFFFFFFu;
 bool g_t2_rows_by_contact = false;
+int g_t2_exp = 0;
 
 // one warp per 32 consecutive particles (the sweep's warp grouping): first-fit packing
 __global__ void k_pack_plan(int64_t N, const uint32_t *__restrict__ inc_start, uint32_t *__restrict__ off_local,
@@ -146,7 +147,22 @@ void p8_unpack(int64_t nc, const P8 *q, P4 *a, P4 *b, cudaStream_t s)
 // PACKED: the canonical reduction above (default); false: the contiguous CSR chunks (fastest
 // layout-independent of packing; bit-reproducible run to run but rounding depends on the warp
 // grouping, i.e. on the decomposition)
-template <bool PACKED, bool ROWS_PK = true>
+// EXP (timing experiments on the shipped kernel, dem_bench_sweeps 44/45): 1 the contact
+// arithmetic replaced by a few additions of its inputs (memory side only), 2 the contact records
+// and impulses not loaded (arithmetic on constants)
+__device__ __forceinline__ HalfOut t2_fake(const double4 VA, const double4 WA, const double4 VB, const double4 WB,
+                                           const G4 g, const R4 rw, const P4 pa, const P4 pb)
+{
+    HalfOut o;
+    o.dL = mk(1e-30 * (VA.x + VB.x + g.x + rw.x + pa.x), 1e-30 * (VA.y + WB.y + g.y + rw.y + pb.x),
+              1e-30 * (WA.z + VB.z + g.z + rw.z + pa.y));
+    o.dA = mk(1e-30 * (WA.x + g.w + rw.w + pa.z), 1e-30 * (WB.x + pa.w + pb.y), 1e-30 * pb.z);
+    o.Pa = pa;
+    o.Pb = pb;
+    return o;
+}
+
+template <bool PACKED, bool ROWS_PK = true, int EXP = 0>
 __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     k_sweep_t2(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win, double4 *__restrict__ vout,
                double4 *__restrict__ wout, const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
@@ -204,11 +220,18 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                 const uint32_t p = ent.y;
                 // PACKED: normals and rows duplicated per half-contact in packed order (coalesced),
                 // both impulse records of the contact in one 32-byte slot
-                const G4 g = ld4g(PACKED && ROWS_PK ? &geo[k] : &geo[c]);
-                const R4 rw = ld4g(PACKED && ROWS_PK ? &row[k] : &row[c]);
+                G4 g;
+                R4 rw;
                 P4 pa, pb;
-                if (PACKED) { const P8 q = ldP8(&P8_in[c]); pa = q.a; pb = q.b; }
-                else { pa = Pa_in[c]; pb = Pb_in[c]; }
+                if (EXP == 2) {
+                    g = mkG4(0.6, 0.0, 0.8, 1e-4); rw = mkR4(1e-3, 1e-3, 1e-3, 1e-3);
+                    pa = mkP4(1e-6, 0, 0, 0); pb = mkP4(0, 0, 0, 0);
+                } else {
+                    g = ld4g(PACKED && ROWS_PK ? &geo[k] : &geo[c]);
+                    rw = ld4g(PACKED && ROWS_PK ? &row[k] : &row[c]);
+                    if (PACKED) { const P8 q = ldP8(&P8_in[c]); pa = q.a; pb = q.b; }
+                    else { pa = Pa_in[c]; pb = Pb_in[c]; }
+                }
                 double4 VP, WP;
                 double mt = sp.mu_t;
                 if (!(p & PARTNER_EXT)) {
@@ -223,8 +246,9 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                     WP = make_double4(0.0, 0.0, 0.0, 0.0);
                 }
                 const double4 VS = cat2(sVa[o], sVb[o]), WS = cat2(sWa[o], sWb[o]);
-                const HalfOut r = half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt, g, rw,
-                                               pa, pb, sp.rolling_dims);
+                const HalfOut r = EXP == 1 ? t2_fake(VS, WS, VP, WP, g, rw, pa, pb)
+                                           : half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB,
+                                                          mt, g, rw, pa, pb, sp.rolling_dims);
                 if (!isB) {   // both halves compute the same impulses; body a stores them
                     if (PACKED) stP8(&P8_out[c], r.Pa, r.Pb);
                     else { Pa_out[c] = r.Pa; Pb_out[c] = r.Pb; }
@@ -272,6 +296,17 @@ void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 
 {
     if (!N) return;
     const unsigned gb = (unsigned)((N + TT - 1) / TT);
+    if (pk && g_t2_exp) {             // diagnostic (dem_bench_sweeps 44/45): timing experiments
+        if (g_t2_exp == 1)
+            k_sweep_t2<true, true, 1><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase,
+                                                        pk->geo, pk->row, nullptr, nullptr, nullptr, nullptr, pk->p8in,
+                                                        pk->p8out, bnd, sp);
+        else
+            k_sweep_t2<true, true, 2><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase,
+                                                        pk->geo, pk->row, nullptr, nullptr, nullptr, nullptr, pk->p8in,
+                                                        pk->p8out, bnd, sp);
+        return;
+    }
     if (pk && g_t2_rows_by_contact)   // diagnostic (dem_bench_sweeps 8): contact-indexed rows
         k_sweep_t2<true, false><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase,
                                                   pk->geo, pk->row, nullptr, nullptr, nullptr, nullptr, pk->p8in,
