@@ -80,7 +80,12 @@ typedef struct {
                                   for any number of GPUs/slabs; 1 contiguous -- ~4 %
                                   faster sweep (no packing holes), bit-reproducible run to run, but the
                                   rounding of the sums depends on the decomposition */
-    int32_t pad1;
+    int32_t plate_coupling;    /* force-driven plate axes: 0 staggered after the solve (reading R18,
+                                  default); 1 monolithic -- the axis is a body of the impact and
+                                  main-stage solves (reading R18b): V += (h F + sum of
+                                  its contacts' warm-start impulses)/M before the sweeps, V += sum of
+                                  the sweep's impulse increments / M after each, x += h V at the end
+                                  (Jacobi ordering only) */
 } dem_solver;
 
 /* Container: axis-aligned box; wall w = 2*axis + side (0:-x 1:+x 2:-y 3:+y 4:-z 5:+z). */

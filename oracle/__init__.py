@@ -45,6 +45,7 @@ class Params(C.Structure):
         ("e_H", C.c_double), ("k_lin", C.c_double), ("damp_steps", C.c_double),
         ("v_imp", C.c_double), ("g", C.c_double * 3),
         ("rolling_dims", C.c_int32), ("ordering", C.c_int32),
+        ("plate_coupling", C.c_int32), ("pad", C.c_int32),
     ]
 
 
@@ -204,6 +205,7 @@ def make_params(**kw) -> Params:
         p.g[k] = g[k]
     p.rolling_dims = kw.get("rolling_dims", 3)
     p.ordering = kw.get("ordering", 0)          # 0 Jacobi (R2), 1 coloured Gauss-Seidel (NEXT-1)
+    p.plate_coupling = kw.get("plate_coupling", 0)   # 0 staggered (R18), 1 monolithic (R18b)
     return p
 
 

@@ -344,8 +344,9 @@ static void body_b_vel(const or_world *w, const row *R, const double *v, const d
  */
 static void sweep(const or_world *w, const or_params *p, row *R, int64_t nc,
                   const int32_t *cnt, const double *minv, const double *Iinv,
-                  double *v, double *om, double *accL, double *accA)
+                  double *v, double *om, double *accL, double *accA, double *accP)
 {
+    if (accP) memset(accP, 0, sizeof(double) * 3 * (size_t)w->n_plates);
     const int64_t N = w->n;
     memset(accL, 0, sizeof(double) * 3 * (size_t)N);
     memset(accA, 0, sizeof(double) * 3 * (size_t)N);
@@ -421,6 +422,9 @@ static void sweep(const or_world *w, const or_params *p, row *R, int64_t nc,
                 accL[3 * b + k] += dPn * n[k] + dPt[k];
                 accA[3 * b + k] += tb[k] + dPr[k];
             }
+        } else if (r->g.kind == 2 && accP) {
+            /* monolithic plate (R18b): the plate receives +(dPn n + dPt) */
+            for (int k = 0; k < 3; k++) accP[3 * r->g.idx + k] += dPn * n[k] + dPt[k];
         }
         r->P[0] = Pn;
         for (int k = 0; k < 3; k++) { r->P[1 + k] = Pt[k]; r->P[4 + k] = Pr[k]; }
@@ -713,10 +717,20 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
             r->S = 0.0;
             r->bias = r->impacting ? -p->e_rest * r->un_minus : 0.0;
         }
+        /* monolithic plates (R18b): force-driven axes take their contacts' impact impulses too */
+        const int mono_i = p->plate_coupling == 1 && !gs && w->n_plates > 0;
+        double *accPi = mono_i ? (double *)calloc(3 * (size_t)w->n_plates, sizeof(double)) : NULL;
         for (int32_t s = 0; s < n_imp; s++) {
             if (gs) sweep_gs(w, p, R, nc, order, minv, Iinv, w->v, w->w);
-            else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA);
+            else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA, accPi);
+            if (mono_i)
+                for (int32_t q = 0; q < w->n_plates; q++) {
+                    or_plate *P = &w->plates[q];
+                    for (int k = 0; k < 3; k++)
+                        if (P->mode[k] == 2) P->vel[k] += accPi[3 * q + k] / P->mass;
+                }
         }
+        free(accPi);
     }
 
     /* 4. main-stage rows (SPOOK; reading R4):
@@ -754,11 +768,39 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
         for (int k = 0; k < 3; k++) w->v[3 * i + k] += h * p->g[k];
     apply_impulses(w, R, nc, minv, Iinv, w->v, w->w);
 
+    /* 6b. monolithic plates (R18b): a force-driven axis is a body of this solve -- it takes the
+     *     external impulse h F and the warm-start impulses of its contacts, V += (h F + sum L)/M,
+     *     and after every sweep the increments of its contacts, V += sum dL / M (Jacobi with the
+     *     real mass = the mass-splitting average over its contacts); likewise in the impact stage.
+     *     In the contact rows the plate keeps an infinite mass (the diagonal only sets the step
+     *     of the projected iteration; the fixed point is the coupled MCP's) */
+    const int mono = p->plate_coupling == 1 && !gs && w->n_plates > 0;
+    double *accP = mono ? (double *)calloc(3 * (size_t)w->n_plates, sizeof(double)) : NULL;
+    if (mono) {
+        for (int64_t c = 0; c < nc; c++) {
+            row *r = &R[c];
+            if (r->g.kind != 2) continue;
+            for (int k = 0; k < 3; k++) accP[3 * r->g.idx + k] += r->P[0] * r->g.n[k] + r->P[1 + k];
+        }
+        for (int32_t q = 0; q < w->n_plates; q++) {
+            or_plate *P = &w->plates[q];
+            for (int k = 0; k < 3; k++)
+                if (P->mode[k] == 2) P->vel[k] += (h * P->target[k] + accP[3 * q + k]) / P->mass;
+        }
+    }
+
     /* 7. N_it sweeps: Jacobi, or coloured Gauss-Seidel */
     for (int32_t s = 0; s < p->n_it; s++) {
         if (gs) sweep_gs(w, p, R, nc, order, minv, Iinv, w->v, w->w);
-        else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA);
+        else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA, accP);
+        if (mono)
+            for (int32_t q = 0; q < w->n_plates; q++) {
+                or_plate *P = &w->plates[q];
+                for (int k = 0; k < 3; k++)
+                    if (P->mode[k] == 2) P->vel[k] += accP[3 * q + k] / P->mass;
+            }
     }
+    free(accP);
 
     /* 8. outputs: forces/torques (P/h sums), plate reactions, residuals (O6, O9) */
     if (F) memset(F, 0, sizeof(double) * 3 * (size_t)N);
@@ -815,8 +857,9 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
         or_plate *P = &w->plates[q];
         for (int k = 0; k < 3; k++) P->pos[k] += h * P->vel[k];
         for (int k = 0; k < 3; k++) {
-            if (P->mode[k] == 2) {                                          /* staggered force axis */
-                P->vel[k] += h * (P->target[k] + P->force[k]) / P->mass;
+            if (P->mode[k] == 2) {
+                /* staggered force axis (R18); monolithic (R18b): the solve set V already */
+                if (p->plate_coupling != 1 || gs) P->vel[k] += h * (P->target[k] + P->force[k]) / P->mass;
                 P->motor[k] = P->target[k];
                 continue;
             }

@@ -36,6 +36,10 @@ typedef struct {
     int32_t rolling_dims;     /* 3 (default) or 2 (rolling row projected on tangent plane) */
     int32_t ordering;         /* 0: Jacobi with mass splitting (reading R2); 1: coloured projected
                                  Gauss-Seidel (P:134 PGS), see or_color_contacts */
+    int32_t plate_coupling;   /* force-driven plate axes: 0 staggered after the solve (reading R18);
+                                 1 monolithic: the plate is a body of the main-stage solve (reading
+                                 R18b; Jacobi ordering only) */
+    int32_t pad;
 } or_params;
 
 /* Static or kinematic plane wall: contact iff (X-p).n < r (reading R17). */

@@ -58,6 +58,7 @@ __device__ __forceinline__ uint64_t partner_key(uint32_t p, const uint32_t *__re
 #define PLATE_KEY_BASE 0xFFFFF000u       // public key of plate p box b: 2^32-4096+16p+b
 #define FIXED_SCALE 1099511627776.0      // 2^40: int64 fixed point for plate impulse sums
 #define NB_SLOTS (DEM_MAX_PLATES + 6)    // boundary-body sums: plates 0..7, walls 8..13
+#define HUB_SCALE 4503599627370496.0     // 2^52: int64 fixed point of the per-sweep plate increments
 
 // Storage precision of the contact arrays: -DDEM_P64 / -DDEM_G64 / -DDEM_R64
 // store impulses / normals / row constants as fp64 instead of fp32 (all row arithmetic is fp64).
@@ -173,6 +174,7 @@ struct DevBoundary {
     int wpresent[6];
     double wall_mu_t, wall_mu_r;
     int n_plates;
+    int mono;                           // monolithic force-driven plate axes (solver.plate_coupling)
     int nbox[DEM_MAX_PLATES];
     double lo[DEM_MAX_PLATES][DEM_MAX_BOXES][3], hi[DEM_MAX_PLATES][DEM_MAX_BOXES][3];
     double ppos[DEM_MAX_PLATES][3], pvel[DEM_MAX_PLATES][3];

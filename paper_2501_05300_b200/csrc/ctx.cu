@@ -104,6 +104,10 @@ struct dem_ctx {
     unsigned long long *pacc = nullptr;
     unsigned int *pcount = nullptr;
     unsigned long long *dscr_bad = nullptr;
+    // monolithic plates (R18b): the step's owned plate contacts and the per-sweep impulse sums
+    uint32_t *plist = nullptr;
+    int64_t n_plist = 0;
+    unsigned long long *hub_acc = nullptr;
     StepScalars *dsc = nullptr, *hsc = nullptr;
     uint32_t *hnc = nullptr;
     // status
@@ -218,6 +222,7 @@ static void setup_solve_params(dem_ctx *ctx)
 {
     SolveParams &sp = ctx->sp;
     const dem_solver &so = ctx->sol;
+    ctx->hb.mono = so.plate_coupling == 1 ? 1 : 0;
     sp.h = so.dt;
     sp.Ups = 1.0 / (1.0 + 4.0 * so.damping_steps);
     sp.e_H = so.hertz_exp;
@@ -328,6 +333,8 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
         TRY(A(ctx, &ctx->db, 1));
         TRY(A(ctx, &ctx->pacc, 3 * DEM_MAX_PLATES));
         TRY(A(ctx, &ctx->pcount, NB_SLOTS));
+        TRY(A(ctx, &ctx->hub_acc, 3 * DEM_MAX_PLATES));
+        CK(cudaMemsetAsync(ctx->hub_acc, 0, 3 * DEM_MAX_PLATES * sizeof(unsigned long long), ctx->s));
         TRY(A(ctx, &ctx->dsc, 1));
     }
     ctx->capN = cap;
@@ -361,6 +368,7 @@ static dem_status ensure_cand(dem_ctx *ctx, int64_t n)
     for (int k = 0; k < 2; k++) { TRY(regrow(ctx, &ctx->Pa[k], cap)); TRY(regrow(ctx, &ctx->Pb[k], cap)); }
     TRY(regrow(ctx, &ctx->ccand, cap));
     TRY(regrow(ctx, &ctx->p8[0], cap)); TRY(regrow(ctx, &ctx->p8[1], cap));
+    TRY(regrow(ctx, &ctx->plist, cap + 1));
     TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
     if (!ctx->gs_scr) TRY(A(ctx, &ctx->gs_scr, 260));
     TRY(regrow(ctx, &ctx->inc, 2 * cap));
@@ -852,6 +860,25 @@ static dem_status pack_incidence(dem_ctx *ctx, int64_t N)
     return DEM_OK;
 }
 
+// monolithic plates (R18b): the impulse the force-driven plate axes received between pin and pout
+// (pin == nullptr: all of pout; first: plus the external impulse h F), summed over the ranks
+static bool mono_active(const dem_ctx *ctx) { return ctx->hb.mono && ctx->hb.n_plates > 0 && ctx->sol.ordering == 0; }
+static dem_status plate_hub(dem_ctx *ctx, bool p8, const void *pin, const void *pout, int first)
+{
+    cudaStream_t s = ctx->s;
+    launch_plate_hub(p8, ctx->n_plist, ctx->plist, ctx->cij, ctx->geo, pin, pout, ctx->hub_acc, s);
+    if (ctx->tp) {
+        long long v[3 * DEM_MAX_PLATES];
+        CK(cudaMemcpyAsync(v, ctx->hub_acc, sizeof(v), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (!ctx->tp->allreduce_i64(v, 3 * DEM_MAX_PLATES, 0, s, ctx->err)) return DEM_ERR_NCCL;
+        CK(cudaMemcpyAsync(ctx->hub_acc, v, sizeof(v), cudaMemcpyHostToDevice, s));
+    }
+    launch_plate_kick(ctx->db, ctx->hub_acc, ctx->sp.h, first, s);
+    ctx->launches += 2;
+    return DEM_OK;
+}
+
 // Runs n packed sweeps (impulses ping-pong in p8[0/1] from p8[0]; velocities from vel[cur]),
 // replaying a captured CUDA graph when the launch configuration is unchanged (single context:
 // the sweep loop has no host step between launches).  ctx->cur ends n sweeps later.
@@ -860,6 +887,7 @@ static dem_status packed_sweeps(dem_ctx *ctx, int stage, int n, const R4 *rows, 
     cudaStream_t s = ctx->s;
     const int64_t N = ctx->N;
     const int c0 = ctx->cur;
+    const bool hub = mono_active(ctx);
     auto body = [&]() {
         for (int it = 0; it < n; it++) {
             const int a = c0 ^ (it & 1);
@@ -869,6 +897,11 @@ static dem_status packed_sweeps(dem_ctx *ctx, int stage, int n, const R4 *rows, 
             launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[a], ctx->ang[a], ctx->vel[a ^ 1], ctx->ang[a ^ 1],
                          ctx->inc_start, ctx->inc, &ctx->pkv, ctx->geo, nullptr, nullptr, nullptr, nullptr, nullptr,
                          ctx->db, sp, s);
+            if (hub) {
+                launch_plate_hub(true, ctx->n_plist, ctx->plist, ctx->cij, ctx->geo, ctx->p8[it & 1],
+                                 ctx->p8[(it & 1) ^ 1], ctx->hub_acc, s);
+                launch_plate_kick(ctx->db, ctx->hub_acc, sp.h, 0, s);
+            }
         }
     };
     if (ctx->tp || n < 2 || getenv("DEM_NO_GRAPHS")) {
@@ -880,6 +913,7 @@ static dem_status packed_sweeps(dem_ctx *ctx, int stage, int n, const R4 *rows, 
             launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[a], ctx->ang[a], ctx->vel[a ^ 1], ctx->ang[a ^ 1],
                          ctx->inc_start, ctx->inc, &ctx->pkv, ctx->geo, nullptr, nullptr, nullptr, nullptr, nullptr,
                          ctx->db, sp, s);
+            if (hub) TRY(plate_hub(ctx, true, ctx->p8[it & 1], ctx->p8[(it & 1) ^ 1], 0));
             ctx->cur ^= 1;
             TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
         }
@@ -887,8 +921,9 @@ static dem_status packed_sweeps(dem_ctx *ctx, int stage, int n, const R4 *rows, 
     }
     // key: everything the captured launches bake in
     const void *ptrs[] = {ctx->vel[0], ctx->vel[1], ctx->ang[0], ctx->ang[1], ctx->inc_start, ctx->pk_inc, ctx->pk_start,
-                          ctx->pk_wbase, ctx->pk_geo, rows, ctx->p8[0], ctx->p8[1], ctx->db};
-    const int64_t ints[] = {N, n, c0};
+                          ctx->pk_wbase, ctx->pk_geo, rows, ctx->p8[0], ctx->p8[1], ctx->db, ctx->plist, ctx->cij,
+                          ctx->geo, ctx->hub_acc};
+    const int64_t ints[] = {N, n, c0, hub ? ctx->n_plist : -1};
     std::vector<unsigned char> key(sizeof(ptrs) + sizeof(ints) + sizeof(SolveParams));
     std::memcpy(key.data(), ptrs, sizeof(ptrs));
     std::memcpy(key.data() + sizeof(ptrs), ints, sizeof(ints));
@@ -953,6 +988,18 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->gid, ctx->inc_cnt,
                ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
     if (ctx->sol.reduction == 0 && ctx->sol.ordering == 0) TRY(pack_incidence(ctx, N));
+    ctx->n_plist = 0;
+    if (mono_active(ctx) && nc) {
+        // monolithic plates: this step's owned plate contacts (cflag/cscan are free again)
+        launch_plate_list_flags(nc, OWN(ctx), ctx->cij, ctx->cflag, s);
+        scan_u32(ctx->cflag, ctx->cscan, nc, ctx->scan_tmp, s, &ctx->launches);
+        uint32_t np = 0;
+        CK(cudaMemcpyAsync(&np, ctx->cscan + nc, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        launch_compact_idx(nc, ctx->cflag, ctx->cscan, ctx->plist, s);
+        ctx->n_plist = np;
+        ctx->launches += 2;
+    }
     launch_prepare(N, ctx->inc_start, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], sp.rho, s);
     TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));      // ghosts' weights c/m, c/I from their owners
     if (sweep_uses_order()) launch_tile_order(N, ctx->inc_start, ctx->order, s);
@@ -1004,6 +1051,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
             launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                          ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row_imp, ctx->Pa[pi],
                          ctx->Pb[pi], ctx->Pa[pi ^ 1], ctx->Pb[pi ^ 1], ctx->db, sp, s);
+            if (mono_active(ctx)) TRY(plate_hub(ctx, false, ctx->Pa[pi], ctx->Pa[pi ^ 1], 0));
             ctx->cur ^= 1;
             TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
         }
@@ -1020,6 +1068,8 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     ctx->cur ^= 1;
     ctx->launches += 2;
     TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
+    // monolithic plates: the external impulse h F and the warm-start impulses of their contacts
+    if (mono_active(ctx)) TRY(plate_hub(ctx, false, nullptr, ctx->Pwa, 1));
     tstart(ctx, 3);
     const int n_it = ctx->sol.n_iter;
     const P4 *pin_a = ctx->Pwa, *pin_b = ctx->Pwb;
@@ -1050,6 +1100,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
                      ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
                      ctx->db, sp, s);
+        if (mono_active(ctx)) TRY(plate_hub(ctx, false, pin_a, oa, 0));
         ctx->cur ^= 1;
         TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
         pin_a = oa;
@@ -1269,6 +1320,7 @@ dem_status dem_create_bed(const dem_bed_desc *desc, const dem_dist_desc *dist, d
     if (!valid_material(desc->mat)) { g_create_err = "invalid material"; return DEM_ERR_INVALID; }
     const dem_solver &so = desc->solver;
     if (!(so.dt > 0) || so.n_iter < 1 || !(so.ordering == 0 || so.ordering == 1) || !(so.reduction == 0 || so.reduction == 1) ||
+        !(so.plate_coupling == 0 || so.plate_coupling == 1) || (so.plate_coupling == 1 && so.ordering == 1) ||
         !(so.hertz_exp == 1.25 || so.hertz_exp == 1.0) ||
         (so.hertz_exp == 1.0 && !(so.k_lin > 0)) || so.damping_steps < 0) {
         g_create_err = "invalid solver settings (dt > 0, n_iter >= 1, hertz_exp 1.25 or 1 with k_lin > 0)";
@@ -1373,7 +1425,8 @@ dem_status dem_step(dem_ctx *ctx, int32_t n_steps, dem_step_report *last)
 
 static bool valid_solver(const dem_solver &so)
 {
-    return (so.ordering == 0 || so.ordering == 1) && (so.reduction == 0 || so.reduction == 1) && so.dt > 0 &&
+    return (so.ordering == 0 || so.ordering == 1) && (so.reduction == 0 || so.reduction == 1) &&
+           (so.plate_coupling == 0 || (so.plate_coupling == 1 && so.ordering == 0)) && so.dt > 0 &&
            so.n_iter >= 1 && (so.hertz_exp == 1.25 || so.hertz_exp == 1.0) &&
            !(so.hertz_exp == 1.0 && !(so.k_lin > 0)) && so.damping_steps >= 0;
 }
@@ -1387,7 +1440,7 @@ dem_status dem_set_solver(dem_ctx *ctx, const dem_solver *so)
     ctx->sol = *so;
     setup_solve_params(ctx);
     ctx->grid.skin = skin;
-    return DEM_OK;
+    return upload_boundary(ctx);
 }
 
 dem_status dem_get_state(dem_ctx *ctx, dem_state_view *v)

@@ -96,6 +96,10 @@ void launch_hist_x(int64_t n, const uint8_t *own, const double4 *pos, double lo,
 void launch_first_bad(int64_t nc, int64_t N, const uint8_t *own, const uint2 *cij, const uint32_t *gid, const P4 *Pa,
                       const P4 *Pb, const double4 *pos, const double4 *vel, const double4 *ang,
                       unsigned long long *out, cudaStream_t s);
+void launch_plate_list_flags(int64_t nc, const uint8_t *own, const uint2 *cij, uint32_t *flag, cudaStream_t s);
+void launch_plate_hub(bool p8, int64_t n, const uint32_t *list, const uint2 *cij, const G4 *geo, const void *pin,
+                      const void *pout, unsigned long long *acc, cudaStream_t s);
+void launch_plate_kick(DevBoundary *bnd, unsigned long long *acc, double h, int first, cudaStream_t s);
 void launch_residuals(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const R4 *row, const double4 *vel,
                       const P4 *Pa, const P4 *Pb, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
                       cudaStream_t s);

@@ -667,7 +667,8 @@ __global__ void k_boundary(DevBoundary *bnd, const unsigned long long *__restric
             const int md = bnd->mode[q][k];
             const double v = bnd->pvel[q][k], fc = bnd->pforce[q][k], m = bnd->pmass[q];
             if (md == 2) {
-                bnd->pvel[q][k] = v + h * (bnd->target[q][k] + fc) / m;
+                // staggered (R18); monolithic (R18b): the solve already set the velocity
+                if (!bnd->mono) bnd->pvel[q][k] = v + h * (bnd->target[q][k] + fc) / m;
                 bnd->pmotor[q][k] = bnd->target[q][k];
                 continue;
             }
@@ -696,6 +697,62 @@ __global__ void k_boundary(DevBoundary *bnd, const unsigned long long *__restric
     bnd->time = t1;
     sc->bnd_disp = disp;
 }
+
+// ------------------------------------------------------------------ monolithic plates (R18b)
+// owned plate contacts of the step (each contact counted once over the ranks)
+__global__ void k_plate_flag(int64_t nc, const uint8_t *__restrict__ own, const uint2 *__restrict__ cij,
+                             uint32_t *__restrict__ flag)
+{
+    const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const uint32_t j = cij[c].y;
+    flag[c] = ((j & (PARTNER_EXT | PARTNER_PLATE)) == (PARTNER_EXT | PARTNER_PLATE) && (!own || own[cij[c].x])) ? 1u : 0u;
+}
+// the impulse the plate received over a sweep: sum of (P_n n + P_t)(out) - (...)(in), int64 fixed
+// point (exact, order-free); in == nullptr: the whole impulse of `out` (the warm start)
+template <bool P8L>
+__global__ void k_plate_hub(int64_t n, const uint32_t *__restrict__ list, const uint2 *__restrict__ cij,
+                            const G4 *__restrict__ geo, const void *__restrict__ pin, const void *__restrict__ pout,
+                            unsigned long long *__restrict__ acc)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const uint32_t c = list[t];
+    const int q = (cij[c].y >> 4) & 0xF;
+    const G4 g = geo[c];
+    const P4 o = P8L ? ((const P8 *)pout)[c].a : ((const P4 *)pout)[c];
+    P4 i = mkP4(0, 0, 0, 0);
+    if (pin) i = P8L ? ((const P8 *)pin)[c].a : ((const P4 *)pin)[c];
+    const double dPn = (double)o.x - (double)i.x;
+    const double d[3] = {dPn * g.x + ((double)o.y - (double)i.y), dPn * g.y + ((double)o.z - (double)i.z),
+                         dPn * g.z + ((double)o.w - (double)i.w)};
+    for (int k = 0; k < 3; k++) atomicAdd(&acc[3 * q + k], (unsigned long long)llrint(d[k] * HUB_SCALE));
+}
+// force-driven axes take the increments (first: also the external impulse h F); acc is cleared
+__global__ void k_plate_kick(DevBoundary *bnd, unsigned long long *acc, double h, int first)
+{
+    if (threadIdx.x || blockIdx.x) return;
+    for (int q = 0; q < bnd->n_plates; q++)
+        for (int k = 0; k < 3; k++) {
+            const double dl = (double)(long long)acc[3 * q + k] / HUB_SCALE;
+            acc[3 * q + k] = 0ull;
+            if (bnd->mode[q][k] != 2) continue;
+            bnd->pvel[q][k] += ((first ? h * bnd->target[q][k] : 0.0) + dl) / bnd->pmass[q];
+        }
+}
+#define PGRID(n) (unsigned)(((n) + 255) / 256), 256, 0, s
+void launch_plate_list_flags(int64_t nc, const uint8_t *own, const uint2 *cij, uint32_t *flag, cudaStream_t s)
+{ if (nc) k_plate_flag<<<PGRID(nc)>>>(nc, own, cij, flag); }
+void launch_plate_hub(bool p8, int64_t n, const uint32_t *list, const uint2 *cij, const G4 *geo, const void *pin,
+                      const void *pout, unsigned long long *acc, cudaStream_t s)
+{
+    if (!n) return;
+    if (p8) k_plate_hub<true><<<PGRID(n)>>>(n, list, cij, geo, pin, pout, acc);
+    else k_plate_hub<false><<<PGRID(n)>>>(n, list, cij, geo, pin, pout, acc);
+}
+void launch_plate_kick(DevBoundary *bnd, unsigned long long *acc, double h, int first, cudaStream_t s)
+{ k_plate_kick<<<1, 32, 0, s>>>(bnd, acc, h, first); }
+#undef PGRID
 
 // step report: at the final velocities, per owned contact
 // the normal complementarity residual |min(P_n, u_n + Sigma P_n - b)| and the cone excesses

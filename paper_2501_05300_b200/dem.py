@@ -39,7 +39,7 @@ class Solver(C.Structure):
     _fields_ = [("dt", C.c_double), ("n_iter", C.c_int32), ("n_iter_impact", C.c_int32),
                 ("hertz_exp", C.c_double), ("k_lin", C.c_double), ("damping_steps", C.c_double),
                 ("v_impact", C.c_double), ("gravity", C.c_double * 3), ("rolling_dims", C.c_int32),
-                ("ordering", C.c_int32), ("skin", C.c_double), ("reduction", C.c_int32), ("pad1", C.c_int32)]
+                ("ordering", C.c_int32), ("skin", C.c_double), ("reduction", C.c_int32), ("plate_coupling", C.c_int32)]
 
 
 class Box(C.Structure):
@@ -316,7 +316,7 @@ class Bed:
         material = mat
         sol = dict(dt=1e-5, n_iter=92, n_iter_impact=0, hertz_exp=1.25, k_lin=0.0, damping_steps=4.5,
                    v_impact=-1.0, gravity=(0.0, 0.0, -9.81), rolling_dims=3, ordering=0, skin=0.0,
-                   reduction=0)
+                   reduction=0, plate_coupling=0)
         sol.update(solver or {})
         bx = dict(lo=(0.0, 0.0, 0.0), hi=(1.0, 1.0, 1.0), wall_mask=0x3F, wall_mu_t=0.0, wall_mu_r=0.0)
         bx.update(box or {})

@@ -190,3 +190,45 @@ def run_loopback(bed, G, n_steps, solver, box=None, material=None, plates=(), bo
     c = np.concatenate([r["contacts"] for r in res])
     c = c[np.argsort(c["key"], kind="stable")]
     return dict(state=st, forces=(F, T), contacts=c, ranks=res, bounds=bounds)
+
+
+def run_loopback_driven(bed, G, n_steps, solver, box, plate, axis, mode, target):
+    """run_loopback with one plate whose axis is driven (dem_drive_plate) before the steps."""
+    import threading
+
+    from paper_2501_05300_b200 import dem
+    bounds = dem.slab_bounds(bed.x[:, 0], G, box["lo"][0], box["hi"][0])
+    grp = dem.LoopbackGroup(G)
+    res = [None] * G
+    err = [None] * G
+
+    def rank_main(r):
+        b = None
+        try:
+            m = (bed.x[:, 0] >= bounds[r]) & (bed.x[:, 0] < bounds[r + 1])
+            b = dem.Bed(bed.x[m], bed.r[m], bed.v[m], bed.w[m], bed.gid[m], solver=solver, box=box,
+                        dist=dict(rank=r, world_size=G, slab=(bounds[r], bounds[r + 1]), transport="loopback",
+                                  group=grp))
+            pid = b.add_plate(**plate)
+            b.drive_plate(pid, axis, mode, target)
+            for _ in range(n_steps):
+                b.step(1)
+            res[r] = dict(state=b.get_state(), plate=b.get_plate(pid))
+        except Exception as e:   # noqa: BLE001 -- surfaced by the caller
+            err[r] = e
+        finally:
+            if b is not None:
+                b.close()
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(G)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    grp.close()
+    for e in err:
+        if e is not None:
+            raise e
+    st = {k: np.concatenate([r["state"][k] for r in res]) for k in res[0]["state"]}
+    o = np.argsort(st["gid"])
+    return dict(state={k: v[o] for k, v in st.items()}, ranks=res)

@@ -221,3 +221,31 @@ def test_long_list_particle_on_a_face_bit_identical():
     out = run_loopback(bed, 2, 10, solver, box, bounds=[0.0, 0.0301, 0.06])
     for k in ("gid", "pos", "vel", "angvel"):
         assert np.array_equal(out["state"][k], ref["state"][k]), k
+
+
+def test_monolithic_plate_across_slabs_bit_identical():
+    """R18b with a decomposition: the per-sweep plate impulse sums are exact int64 sums over the
+    ranks, so a force-driven plate spanning both slabs moves bit-identically to one context."""
+    bed, box = drifting_bed(drift=0.0, seed=5)
+    top = float((bed.x[:, 2] + bed.r).max())
+    plate = dict(boxes_lo=[(-0.05, -0.015, 0.0)], boxes_hi=[(0.05, 0.015, 0.004)], pos=(0.06, 0.02, top - 0.0005),
+                 mass=0.5)
+    solver = dict(dt=2e-5, n_iter=30, gravity=(0.0, 0.0, -9.81), plate_coupling=1)
+
+    def run_single():
+        D = dem()
+        b = D.Bed(bed.x, bed.r, bed.v, bed.w, bed.gid, solver=solver, box=box)
+        pid = b.add_plate(**plate)
+        b.drive_plate(pid, 2, D.AXIS_FORCE, -2.0)
+        for _ in range(10):
+            b.step(1)
+        out = dict(state=b.get_state(), plate=b.get_plate(pid))
+        b.close()
+        return out
+    ref = run_single()
+    from tests.parity import run_loopback_driven
+    out = run_loopback_driven(bed, 2, 10, solver, box, plate, axis=2, mode=2, target=-2.0)
+    for k in ("pos", "vel", "angvel"):
+        assert np.array_equal(out["state"][k], ref["state"][k]), k
+    for r in out["ranks"]:
+        assert r["plate"]["pos"] == ref["plate"]["pos"] and r["plate"]["vel"] == ref["plate"]["vel"]

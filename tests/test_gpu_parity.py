@@ -174,9 +174,11 @@ def _small_bed_for_plates(seed):
     return b
 
 
-def test_plates_kinematic_and_force_axes_vs_oracle():
+@pytest.mark.parametrize("coupling", [0, 1])
+def test_plates_kinematic_and_force_axes_vs_oracle(coupling):
     """A grouser plate (3 boxes) pressed down kinematically and a flat plate on a force axis,
-    20 steps on both sides: pair sets every step, plate forces and positions."""
+    20 steps on both sides: pair sets every step, plate forces and positions; the force axis
+    staggered (R18) or monolithic (R18b, solver.plate_coupling = 1)."""
     bed = _small_bed_for_plates(41)
     lo = [(-0.006, -0.006, 0.0), (-0.006, -0.006, -0.003), (0.003, -0.006, -0.003)]
     hi = [(0.006, 0.006, 0.002), (-0.004, 0.006, 0.0), (0.005, 0.006, 0.0)]
@@ -186,8 +188,8 @@ def test_plates_kinematic_and_force_axes_vs_oracle():
     P2 = O.make_plate([(-0.004, -0.004, 0.0)], [(0.004, 0.004, 0.002)], pos=(0.022, 0.015, top - 1e-3), mass=0.01)
     P2.mode[2], P2.target[2] = 2, -0.5
     Wo = oracle_world(bed, plates=[P1, P2])
-    po = oracle_params(30, 1e-5)
-    gb = gpu_bed(bed, dt=1e-5, n_iter=30)
+    po = oracle_params(30, 1e-5, plate_coupling=coupling)
+    gb = gpu_bed(bed, dt=1e-5, n_iter=30, plate_coupling=coupling)
     p1 = gb.add_plate(lo, hi, (0.009, 0.015, top), 0.05)
     gb.drive_plate(p1, 2, 1, -0.05)
     p2 = gb.add_plate([(-0.004, -0.004, 0.0)], [(0.004, 0.004, 0.002)], (0.022, 0.015, top - 1e-3), 0.01)
@@ -430,3 +432,49 @@ def test_long_contact_list_vs_oracle():
     ka = (c_ref["key"] >> np.uint64(32)).astype(np.int64)
     kb = (c_ref["key"] & np.uint64(0xFFFFFFFF)).astype(np.int64)
     assert int(((ka == 0) | (kb == 0)).sum()) > 100                    # > 3 chunks of 32
+
+
+def test_monolithic_plate_momentum_and_oracle():
+    """R18b: a free plate (all axes force-driven, F = 0) strikes a free sphere with gravity off:
+    total momentum conserved at every step (the plate takes exactly the impulses the sphere
+    gives, through the impact and main stages), and the trajectory matches the oracle's."""
+    D = dem()
+    r = 4.25e-3
+    m_s = 2200.0 * 4.0 / 3.0 * np.pi * r ** 3
+    x0 = np.array([[0.05 - 0.01 - r - 2e-5, 0.001, 0.048]])
+    P = O.make_plate([(-0.01, -0.01, -0.01)], [(0.01, 0.01, 0.01)], pos=(0.05, 0.0, 0.05), mass=0.02)
+    for k in range(3):
+        P.mode[k], P.target[k] = 2, 0.0
+    P.vel[0] = -0.3
+    Wo = O.OracleWorld(x0, np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], plates=[P])
+    po = O.make_params(h=1e-5, n_it=30, E=1e9, nu=0.15, rho=2200.0, g=(0, 0, 0), plate_coupling=1)
+    b = D.Bed(x0, [r], box=dict(lo=(-1, -1, -1), hi=(1, 1, 1), wall_mask=0),
+              material=dict(density=2200.0, youngs=1e9, poisson=0.15),
+              solver=dict(dt=1e-5, n_iter=30, gravity=(0, 0, 0), plate_coupling=1))
+    pid = b.add_plate([(-0.01, -0.01, -0.01)], [(0.01, 0.01, 0.01)], (0.05, 0.0, 0.05), 0.02)
+    for k in range(3):
+        b.drive_plate(pid, k, D.AXIS_FORCE, 0.0)
+    # the plate starts at -0.3 m/s along x: one kinematic step sets that velocity on both sides
+    b.drive_plate(pid, 0, D.AXIS_VELOCITY, -0.3)
+    Wo.plates[0].mode[0], Wo.plates[0].target[0], Wo.plates[0].vel[0] = 1, -0.3, -0.3
+    b.step(1)
+    Wo.step(po)
+    b.drive_plate(pid, 0, D.AXIS_FORCE, 0.0)
+    Wo.plates[0].mode[0], Wo.plates[0].target[0] = 2, 0.0
+    try:
+        st = b.get_state()
+        mom0 = 0.02 * np.array(b.get_plate(pid)["vel"]) + m_s * st["vel"][0]
+        hit = 0
+        for _ in range(80):
+            rep = b.step(1)
+            Wo.step(po)
+            hit += rep["n_plate"]
+            st = b.get_state()
+            g = b.get_plate(pid)
+            mom = 0.02 * np.array(g["vel"]) + m_s * st["vel"][0]
+            assert np.abs(mom - mom0).max() <= 1e-9 * 0.02 * 0.3
+            assert g["pos"][0] == pytest.approx(Wo.plates[0].pos[0], abs=1e-12)
+            assert st["vel"][0][0] == pytest.approx(Wo.v[0, 0], rel=1e-5, abs=1e-9)
+    finally:
+        b.close()
+    assert hit > 0 and st["vel"][0][0] < -0.05

@@ -591,3 +591,50 @@ def test_motor_force_limits(oracle_mod):
     assert W.plates[0].force[2] == pytest.approx(F0, rel=0.01)
     f = {int(k) & 0xFFFFFFFF: c["P"][i, 0] / h for i, k in enumerate(c["key"])}
     assert f[oracle_mod.WALL_KEY_BASE + 4] == pytest.approx(F0 + mp * 9.81, rel=0.01)
+
+
+def test_monolithic_plate_coupling(oracle_mod):
+    """Reading R18b (SURVEY NEXT-3 'monolithic plate coupling'): a force-driven plate axis as a
+    body of the main-stage solve.  Pins: (1) a free plate under a constant force F integrates
+    symplectically, x_n = x_0 + a h^2 n(n+1)/2 (the staggered R18 gives n(n-1)/2); (2) pressing
+    a sphere onto the floor it reaches the static balance F_p = -F, floor = F + m g; (3) a free
+    plate (all axes force-driven, F = 0) striking a free sphere conserves the total momentum to
+    rounding at every step (the plate takes exactly the impulses the sphere gives)."""
+    r, h = 4.25e-3, 1e-4
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    F, m = 0.2, 0.05
+    P = oracle_mod.make_plate([(-0.01, -0.01, 0.0)], [(0.01, 0.01, 0.005)], pos=(0.5, 0.5, 0.5), mass=m)
+    P.mode[0], P.target[0] = 2, F
+    W = oracle_mod.OracleWorld([[0, 0, r]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], walls=floor, plates=[P])
+    p = oracle_mod.make_params(h=h, n_it=20, E=1e9, nu=0.15, rho=2200.0, plate_coupling=1)
+    x0 = W.plates[0].pos[0]
+    for n in range(1, 101):
+        W.step(p)
+        assert W.plates[0].pos[0] - x0 == pytest.approx(F / m * h * h * n * (n + 1) / 2, rel=1e-12, abs=2.5e-16 * n)
+    # (2) static press
+    F0 = 2.0
+    P = oracle_mod.make_plate([(-0.01, -0.01, 0.0)], [(0.01, 0.01, 0.005)], pos=(0, 0, 2 * r - 1e-6), mass=0.05)
+    P.mode[2], P.target[2] = 2, -F0
+    W = oracle_mod.OracleWorld([[0, 0, r]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], walls=floor, plates=[P])
+    p = oracle_mod.make_params(h=h, n_it=50, E=1e9, nu=0.15, rho=2200.0, plate_coupling=1)
+    c, _, _ = W.step(p, 1500)
+    mp, _ = oracle_mod.mass_inertia(2 * r, 2200.0)
+    assert W.plates[0].force[2] == pytest.approx(F0, rel=0.01)
+    f = {int(k) & 0xFFFFFFFF: c["P"][i, 0] / h for i, k in enumerate(c["key"])}
+    assert f[oracle_mod.WALL_KEY_BASE + 4] == pytest.approx(F0 + mp * 9.81, rel=0.01)
+    # (3) momentum
+    P = oracle_mod.make_plate([(-0.01, -0.01, -0.01)], [(0.01, 0.01, 0.01)], pos=(0.05, 0.0, 0.0), mass=0.02)
+    for k in range(3):
+        P.mode[k], P.target[k] = 2, 0.0
+    P.vel[0] = -0.3
+    W = oracle_mod.OracleWorld([[0.05 - 0.01 - r - 2e-5, 0.001, -0.002]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0],
+                               plates=[P])
+    p = oracle_mod.make_params(h=1e-5, n_it=30, E=1e9, nu=0.15, rho=2200.0, g=(0, 0, 0), plate_coupling=1)
+    mom0 = 0.02 * np.array(W.plates[0].vel[:])
+    hit = False
+    for _ in range(60):
+        c, _, _ = W.step(p)
+        hit = hit or len(c) > 0
+        mom = 0.02 * np.array(W.plates[0].vel[:]) + mp * W.v[0]
+        assert np.abs(mom - mom0).max() <= 1e-12 * 0.02 * 0.3
+    assert hit and W.v[0, 0] < -0.05                                 # the sphere was struck
