@@ -70,13 +70,16 @@ class BedSpec:
     material: dict = field(default_factory=lambda: dict(PAPER_MATERIAL))
     seed: int = 0
     dt: float = None                             # None: Eq. 9 with eps 0.02 and sigma = rho g H
-    n_iter: int = 30                             # relaxation sweeps per step
+    n_iter: int = None                           # sweeps per step; None: Eq. 8 (eps 0.02) on the bed's
+                                                 # contact-network length n_d = sum of thickness / d_n,
+                                                 # at least 30
     spacing: float = 1.5                         # emitter grid spacing / d_n
     drop_speed: float = 0.05                     # initial downward speed of emitted particles [m/s]
     ke_threshold: float = 1e-8                   # settle: mean KE per particle [J]
     v_threshold: float = 1e-3                    # settle: max |v| [m/s]
     v_emit: float = 0.02                         # next plane once max |v| is below this [m/s]
-    layer_budget: float = 10.0                   # simulated seconds per layer (5 s; 10 here)
+    layer_budget: float = 10.0                   # simulated seconds per layer settle (5 s; 10 here)
+    plane_budget: float = 2.0                    # simulated seconds an emitted plane may take to calm down
     check_every: int = 20                        # steps between settle checks
 
 
@@ -162,7 +165,7 @@ class _World:
         m = self.spec.material["density"] * 4.0 / 3.0 * np.pi * st["radius"] ** 3
         return float(0.5 * (m * (st["vel"] ** 2).sum(axis=1)).sum()) / max(len(m), 1)
 
-    def run_until(self, v_max, ke_max, budget):
+    def run_until(self, v_max, ke_max, budget, ke_any=None):
         """Steps until max |v| < v_max and the mean translational kinetic energy per particle
         < ke_max (checked every check_every steps; the spins' share is left out: with the large
         Eq. 9 step the unconverged torques keep a small rotational jitter that carries no
@@ -173,6 +176,8 @@ class _World:
             self.stepped = True
             self.t += self.spec.check_every * self.dt
             ke = rep["ke"] / max(len(self.r), 1)
+            if ke_any is not None and ke < ke_any:
+                return rep
             if rep["max_v"] < v_max:
                 if ke < ke_max or (np.isfinite(ke_max) and self.ke_translational() < ke_max):
                     return rep
@@ -191,6 +196,9 @@ def build_bed(spec: BedSpec, device=0, bed_factory=None):
     rng = np.random.default_rng(spec.seed)
     rho = spec.material["density"]
     dt = spec.dt or D.plan_timestep(spec.d_min, 0.02, rho, rho * 9.81 * max(Lz, 1e-3))
+    if spec.n_iter is None:
+        n_d = sum((bot - top) / d for (d, top, bot) in sched) if sched else 1.0
+        spec = BedSpec(**{**spec.__dict__, "n_iter": max(30, D.plan_iterations(n_d, 0.02))})
     W = _World(spec, dt, device, bed_factory)
     gid0 = 0
     try:
@@ -212,7 +220,10 @@ def build_bed(spec: BedSpec, device=0, bed_factory=None):
                 gid0 += len(rad)
                 W.add(p, rad, v, g, li)
                 W.open(spec.relax_mu)
-                W.run_until(spec.v_emit, np.inf, spec.layer_budget - (W.t - t_layer))
+                # next plane once the bed is nearly at rest: max |v| < v_emit, or the mean kinetic
+                # energy that of every sphere moving at v_emit / 4 (a single rattler may not hold it up)
+                m_n = rho * np.pi / 6.0 * d_n ** 3
+                W.run_until(spec.v_emit, np.inf, spec.plane_budget, ke_any=0.5 * m_n * (0.25 * spec.v_emit) ** 2)
             # the layer is full: settle, then remove the excess above its top
             if W.bed is not None:
                 W.run_until(spec.v_threshold, spec.ke_threshold, spec.layer_budget)

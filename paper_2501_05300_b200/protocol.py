@@ -48,8 +48,8 @@ def run_plate_test(bed: "D.Bed", plate: int, proto: PlateProtocol, dt: float, z_
     if not proto.F_N > 0:
         raise ExperimentFault("F_N <= 0: the traction coefficient is undefined (SPEC S:476)")
     lost = 0.0
-    n_steps = int(round(proto.t_end / dt))
-    n_I = int(round(proto.t_I_end / dt))
+    n_steps = int(np.ceil(proto.t_end / dt - 1e-9))     # the series covers [0, t_end]
+    n_I = int(np.ceil(proto.t_I_end / dt - 1e-9))
     cols = {k: [] for k in ("t", "sinkage", "F_N_applied", "F_N_measured", "F_T", "traction", "plate_x", "n_contacts")}
     bed.drive_plate(plate, 0, D.AXIS_LOCKED, 0.0)
     for s in range(n_steps):
