@@ -70,7 +70,9 @@ class BedSpec:
     material: dict = field(default_factory=lambda: dict(PAPER_MATERIAL))
     seed: int = 0
     dt: float = None                             # None: Eq. 9 with eps 0.02 and sigma = rho g H
-    n_iter: int = None                           # sweeps per step; None: Eq. 8 (eps 0.02) on the bed's
+    n_iter_emit: int = None                      # sweeps per step while planes are emitted; None: n_iter
+                                                 # (30 was measured slower: the planes take longer to calm)
+    n_iter: int = None                           # sweeps per step of the settles; None: Eq. 8 (eps 0.02) on the bed's
                                                  # contact-network length n_d = sum of thickness / d_n,
                                                  # at least 30
     spacing: float = 1.5                         # emitter grid spacing / d_n
@@ -123,11 +125,12 @@ class _World:
         m["mu_t"], m["mu_r"] = mu
         return m
 
-    def open(self, mu):
+    def open(self, mu, n_iter=None):
         self.close()
+        self.n_iter_now = n_iter or self.spec.n_iter
         Lx, Ly, Lz = self.spec.dims
         self.bed = self.factory(pos=self.x, radius=self.r, vel=self.v, angvel=self.w, gid=self.gid,
-                                solver=dict(dt=self.dt, n_iter=self.spec.n_iter),
+                                solver=dict(dt=self.dt, n_iter=self.n_iter_now),
                                 box=dict(lo=(0.0, 0.0, 0.0), hi=(Lx, Ly, Lz), wall_mask=0x3F, wall_mu_t=0.0,
                                          wall_mu_r=0.0),
                                 material=self._mat(mu))
@@ -164,6 +167,11 @@ class _World:
         st = self.bed.get_state()
         m = self.spec.material["density"] * 4.0 / 3.0 * np.pi * st["radius"] ** 3
         return float(0.5 * (m * (st["vel"] ** 2).sum(axis=1)).sum()) / max(len(m), 1)
+
+    def sweeps(self, n_iter):
+        if self.bed is not None and n_iter != self.n_iter_now:
+            self.bed.set_solver(n_iter=n_iter)
+            self.n_iter_now = n_iter
 
     def run_until(self, v_max, ke_max, budget, ke_any=None, strict=True):
         """Steps until max |v| < v_max and the mean translational kinetic energy per particle
@@ -221,7 +229,7 @@ def build_bed(spec: BedSpec, device=0, bed_factory=None):
                 p[:, 2] = np.minimum(p[:, 2], Lz - 0.6 * d_n)
                 gid0 += len(rad)
                 W.add(p, rad, v, g, li)
-                W.open(spec.relax_mu)
+                W.open(spec.relax_mu, spec.n_iter_emit)
                 # next plane once the bed is nearly at rest: max |v| < v_emit, or the mean kinetic
                 # energy that of every sphere moving at v_emit / 4 (a single rattler may not hold it up)
                 m_n = rho * np.pi / 6.0 * d_n ** 3
@@ -229,8 +237,9 @@ def build_bed(spec: BedSpec, device=0, bed_factory=None):
                 # frictionless floor -- is buried by the next one: only the layer settle is strict)
                 W.run_until(spec.v_emit, np.inf, spec.plane_budget, ke_any=0.5 * m_n * (0.25 * spec.v_emit) ** 2,
                             strict=False)
-            # the layer is full: settle, then remove the excess above its top
+            # the layer is full: settle (Eq. 8 sweeps), then remove the excess above its top
             if W.bed is not None:
+                W.sweeps(spec.n_iter)
                 W.run_until(spec.v_threshold, spec.ke_threshold, spec.layer_budget)
                 W.pull()
                 W.keep(W.x[:, 2] <= top)

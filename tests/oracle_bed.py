@@ -24,6 +24,10 @@ class OracleBed:
         self.params = O.make_params(h=solver.get("dt", 1e-5), n_it=solver.get("n_iter", 30), **m)
         self.order = np.argsort(self.W.gid)
 
+    def set_solver(self, n_iter=None, **_):
+        if n_iter is not None:
+            self.params.n_it = n_iter
+
     def set_state(self, pos, radius, vel=None, angvel=None, gid=None, hist=None):
         self.W.hist = hist if hist is not None else np.zeros(0, dtype=O.CONTACT_DTYPE)
 
