@@ -478,3 +478,51 @@ def test_monolithic_plate_momentum_and_oracle():
     finally:
         b.close()
     assert hit > 0 and st["vel"][0][0] < -0.05
+
+
+@pytest.mark.slow
+def test_full_size_bench_configuration_sampled():
+    """The bench workload itself (config4-geom, 14.6 M spheres from the on-device generator,
+    N_it = 226, the shipped canonical packed sweep), walls and gravity off: sampled pair sets of
+    300 spheres against the oracle's brute force over the whole bed, cones at fp32 rounding (step
+    report), total momentum conserved, and the step bit-reproducible run to run."""
+    import bench
+    D = dem()
+    w = bench.WORKLOADS["config4-geom"]
+    gen = bench.device_generator("config4-geom")
+    box = dict(lo=(0.0, 0.0, 0.0), hi=w["dims"], wall_mask=0)
+    solver = dict(dt=w["dt"], n_iter=226, gravity=(0.0, 0.0, 0.0))
+
+    def run():
+        b = D.Bed(generator=gen, solver=solver, box=box)
+        st0 = b.get_state()
+        rep = b.step(1)
+        st1 = b.get_state()
+        c = b.get_contacts()
+        b.close()
+        return st0, rep, st1, c
+    st0, rep, st1, c = run()
+    n = len(st0["radius"])
+    assert n > 14_000_000 and rep["n_contacts"] > 30_000_000
+    # cones: the report's max excess is the fp32 rounding of P
+    Pn_max = float(c["P"][:, 0].max())
+    assert rep["max_cone_excess"] <= 1e-6 * Pn_max
+    # momentum (inter-particle impulses cancel)
+    m = 2600.0 * np.pi * (2 * st0["radius"]) ** 3 / 6
+    p0 = (m[:, None] * st0["vel"]).sum(0)
+    p1 = (m[:, None] * st1["vel"]).sum(0)
+    assert np.abs(p1 - p0).max() <= 1e-9 * (m[:, None] * np.abs(st1["vel"])).sum()
+    # sampled pair sets on the initial state, brute force over all 14.6 M spheres
+    rng = np.random.default_rng(4)
+    sample = rng.choice(n, 300, replace=False)
+    Wo = O.OracleWorld(st0["pos"], st0["vel"], st0["angvel"], st0["radius"], st0["gid"])
+    ref = Wo.contacts_of(sample)
+    sg = set(st0["gid"][sample].tolist())
+    ka = (c["key"] >> np.uint64(32)).astype(np.int64)
+    kb = (c["key"] & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    sel = np.isin(ka, list(sg)) | np.isin(kb, list(sg))
+    np.testing.assert_array_equal(np.sort(c["key"][sel]), ref["key"])
+    assert len(ref) > 500
+    # run to run
+    _, rep2, st2, _ = run()
+    assert np.array_equal(st1["vel"], st2["vel"]) and rep2["n_contacts"] == rep["n_contacts"]
