@@ -128,6 +128,10 @@ struct dem_ctx {
     uint64_t *gs_key = nullptr;
     int *gs_col = nullptr;
     uint32_t *gs_ord = nullptr;
+    uint2 *gs_cij = nullptr;        // contact records in colour order (coalesced per colour)
+    G4 *gs_geo = nullptr;
+    R4 *gs_row = nullptr;
+    P4 *gs_Pa = nullptr, *gs_Pb = nullptr;
     unsigned int *gs_scr = nullptr;
     std::vector<uint32_t> gs_cstart;
     // timing
@@ -370,6 +374,10 @@ static dem_status ensure_cand(dem_ctx *ctx, int64_t n)
     TRY(regrow(ctx, &ctx->p8[0], cap)); TRY(regrow(ctx, &ctx->p8[1], cap));
     TRY(regrow(ctx, &ctx->plist, cap + 1));
     TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
+    if (ctx->sol.ordering == 1 || ctx->gs_cij) {
+        TRY(regrow(ctx, &ctx->gs_cij, cap)); TRY(regrow(ctx, &ctx->gs_geo, cap)); TRY(regrow(ctx, &ctx->gs_row, cap));
+        TRY(regrow(ctx, &ctx->gs_Pa, cap)); TRY(regrow(ctx, &ctx->gs_Pb, cap));
+    }
     if (!ctx->gs_scr) TRY(A(ctx, &ctx->gs_scr, 260));
     TRY(regrow(ctx, &ctx->inc, 2 * cap));
     ctx->cap_cand = cap;
@@ -1023,13 +1031,21 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
                                   ctx->vals, ctx->sort_tmp, ctx->gs_scr, ctx->gs_cstart, s, &ctx->launches);
         if (ncol < 0) { ctx->err = "Gauss-Seidel colouring needs more than 256 colours"; return DEM_ERR_INVALID; }
         if (nc) CK(cudaMemcpyAsync(ctx->gs_ord, ctx->vals[0], nc * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        if (!ctx->gs_cij) {   // ordering switched on after the buffers were sized
+            const int64_t cap = ctx->cap_cand;
+            TRY(regrow(ctx, &ctx->gs_cij, cap)); TRY(regrow(ctx, &ctx->gs_geo, cap)); TRY(regrow(ctx, &ctx->gs_row, cap));
+            TRY(regrow(ctx, &ctx->gs_Pa, cap)); TRY(regrow(ctx, &ctx->gs_Pb, cap));
+        }
+        gs_gather(nc, ctx->gs_ord, ctx->cij, ctx->geo, nullptr, nullptr, nullptr, ctx->gs_cij, ctx->gs_geo, nullptr,
+                  nullptr, nullptr, s);
+        ctx->launches += 1;
     }
     if (impact && gs) {
         // Newton impact stage (reading R13) in Gauss-Seidel order, in place
-        CK(cudaMemsetAsync(ctx->Pa[0], 0, nc * sizeof(P4), s));
-        CK(cudaMemsetAsync(ctx->Pb[0], 0, nc * sizeof(P4), s));
+        gs_gather(nc, ctx->gs_ord, ctx->cij, ctx->geo, ctx->row_imp, nullptr, nullptr, nullptr, nullptr, ctx->gs_row,
+                  ctx->gs_Pa, ctx->gs_Pb, s);
         for (int it = 0; it < n_imp; it++)
-            gs_sweep(ctx->gs_cstart, ctx->gs_ord, ctx->cij, ctx->geo, ctx->row_imp, ctx->Pa[0], ctx->Pb[0],
+            gs_sweep(ctx->gs_cstart, nullptr, ctx->gs_cij, ctx->gs_geo, ctx->gs_row, ctx->gs_Pa, ctx->gs_Pb,
                      ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->inc_start, ctx->db, sp, s, &ctx->launches);
         ctx->tm.n_sweep_launches += n_imp;
         ctx->tm.contact_sweeps += (int64_t)n_imp * nc;
@@ -1082,13 +1098,13 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     }
     if (gs) {
         // N_it coloured Gauss-Seidel sweeps, impulses and velocities updated in place
-        if (nc) {
-            CK(cudaMemcpyAsync(ctx->Pa[0], ctx->Pwa, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
-            CK(cudaMemcpyAsync(ctx->Pb[0], ctx->Pwb, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
-        }
+        gs_gather(nc, ctx->gs_ord, ctx->cij, ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, nullptr, nullptr, ctx->gs_row,
+                  ctx->gs_Pa, ctx->gs_Pb, s);
         for (int it = 0; it < n_it; it++)
-            gs_sweep(ctx->gs_cstart, ctx->gs_ord, ctx->cij, ctx->geo, ctx->row, ctx->Pa[0], ctx->Pb[0], ctx->vel[ctx->cur],
-                     ctx->ang[ctx->cur], ctx->inc_start, ctx->db, sp, s, &ctx->launches);
+            gs_sweep(ctx->gs_cstart, nullptr, ctx->gs_cij, ctx->gs_geo, ctx->gs_row, ctx->gs_Pa, ctx->gs_Pb,
+                     ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->inc_start, ctx->db, sp, s, &ctx->launches);
+        gs_scatter(nc, ctx->gs_ord, ctx->gs_Pa, ctx->gs_Pb, ctx->Pa[0], ctx->Pb[0], s);
+        ctx->launches += 3;
         pin_a = ctx->Pa[0];
         pin_b = ctx->Pb[0];
     }

@@ -105,7 +105,7 @@ __global__ void k_gs_color(uint32_t n, const uint32_t *__restrict__ ord, const u
 {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
-    const uint32_t c = ord[t];
+    const uint32_t c = ord ? ord[t] : t;      // ord == nullptr: the arrays are already in colour order
     const uint2 ij = cij[c];
     const uint32_t a = ij.x, p = ij.y;
     // real inverse masses: the stored weights are c/m, c/I (mass splitting) -> divide by c
@@ -193,9 +193,42 @@ void gs_sweep(const std::vector<uint32_t> &cstart, const uint32_t *ord, const ui
               const SolveParams &sp, cudaStream_t s, long long *launches)
 {
     for (size_t q = 0; q + 1 < cstart.size(); q++) {
-        const uint32_t n = cstart[q + 1] - cstart[q];
+        const uint32_t n = cstart[q + 1] - cstart[q], o = cstart[q];
         if (!n) continue;
-        k_gs_color<<<(n + 127) / 128, 128, 0, s>>>(n, ord + cstart[q], cij, geo, row, Pa, Pb, vel, ang, inc_start, bnd, sp);
+        if (ord)
+            k_gs_color<<<(n + 127) / 128, 128, 0, s>>>(n, ord + o, cij, geo, row, Pa, Pb, vel, ang, inc_start, bnd, sp);
+        else   // colour-ordered records: each colour reads a contiguous, coalesced range
+            k_gs_color<<<(n + 127) / 128, 128, 0, s>>>(n, nullptr, cij + o, geo + o, row + o, Pa + o, Pb + o, vel, ang,
+                                                       inc_start, bnd, sp);
         *launches += 1;
     }
 }
+
+// contact records into colour order (once per step and stage) and the impulses back
+__global__ void k_gs_gather(int64_t nc, const uint32_t *__restrict__ ord, const uint2 *__restrict__ cij,
+                            const G4 *__restrict__ geo, const R4 *__restrict__ row, const P4 *__restrict__ Pa,
+                            const P4 *__restrict__ Pb, uint2 *__restrict__ cijO, G4 *__restrict__ geoO,
+                            R4 *__restrict__ rowO, P4 *__restrict__ PaO, P4 *__restrict__ PbO)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nc) return;
+    const uint32_t c = ord[t];
+    if (cijO) cijO[t] = cij[c];
+    if (geoO) geoO[t] = geo[c];
+    if (rowO) rowO[t] = row[c];
+    if (PaO) { PaO[t] = Pa ? Pa[c] : mkP4(0, 0, 0, 0); PbO[t] = Pb ? Pb[c] : mkP4(0, 0, 0, 0); }
+}
+__global__ void k_gs_scatter(int64_t nc, const uint32_t *__restrict__ ord, const P4 *__restrict__ PaO,
+                             const P4 *__restrict__ PbO, P4 *__restrict__ Pa, P4 *__restrict__ Pb)
+{
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nc) return;
+    const uint32_t c = ord[t];
+    Pa[c] = PaO[t];
+    Pb[c] = PbO[t];
+}
+void gs_gather(int64_t nc, const uint32_t *ord, const uint2 *cij, const G4 *geo, const R4 *row, const P4 *Pa,
+               const P4 *Pb, uint2 *cijO, G4 *geoO, R4 *rowO, P4 *PaO, P4 *PbO, cudaStream_t s)
+{ if (nc) k_gs_gather<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(nc, ord, cij, geo, row, Pa, Pb, cijO, geoO, rowO, PaO, PbO); }
+void gs_scatter(int64_t nc, const uint32_t *ord, const P4 *PaO, const P4 *PbO, P4 *Pa, P4 *Pb, cudaStream_t s)
+{ if (nc) k_gs_scatter<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(nc, ord, PaO, PbO, Pa, Pb); }

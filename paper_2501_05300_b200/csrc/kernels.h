@@ -138,6 +138,9 @@ bool generate_bed(const dem_generator &g, const dem_box &box, double slab_lo, do
 int gs_color(int64_t nc, const uint2 *cij, const uint32_t *gid, const uint32_t *inc_start, const uint2 *inc,
              uint64_t *key, int *color, uint64_t *keys[2], uint32_t *vals[2], void *sort_tmp, unsigned int *dscr,
              std::vector<uint32_t> &cstart, cudaStream_t s, long long *launches);
+void gs_gather(int64_t nc, const uint32_t *ord, const uint2 *cij, const G4 *geo, const R4 *row, const P4 *Pa,
+               const P4 *Pb, uint2 *cijO, G4 *geoO, R4 *rowO, P4 *PaO, P4 *PbO, cudaStream_t s);
+void gs_scatter(int64_t nc, const uint32_t *ord, const P4 *PaO, const P4 *PbO, P4 *Pa, P4 *Pb, cudaStream_t s);
 void gs_sweep(const std::vector<uint32_t> &cstart, const uint32_t *ord, const uint2 *cij, const G4 *geo, const R4 *row,
               P4 *Pa, P4 *Pb, double4 *vel, double4 *ang, const uint32_t *inc_start, const DevBoundary *bnd,
               const SolveParams &sp, cudaStream_t s, long long *launches);
