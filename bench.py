@@ -177,6 +177,7 @@ def main():
     ap.add_argument("--workload", default="config4-geom", choices=sorted(WORKLOADS))
     ap.add_argument("--n-it", type=int, default=0)
     ap.add_argument("--settle", type=int, default=20)
+    ap.add_argument("--settle-dt", type=float, default=1e-4, help="time step of the coarse relaxation (untimed)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no baseline, no clocks")
@@ -216,7 +217,7 @@ def main():
         if dist:
             dist.broadcast_object_list(obj, src=0)
         dcfg = dict(rank=rank, world_size=world, slab=(rank * L, (rank + 1) * L), transport="nccl", nccl_id=obj[0])
-    bed = dem.Bed(generator=gen, device=local, solver=dict(dt=1e-4, n_iter=20), box=box, dist=dcfg)
+    bed = dem.Bed(generator=gen, device=local, solver=dict(dt=args.settle_dt, n_iter=20), box=box, dist=dcfg)
     N_total = dem.generator_count(gen, box)
     if args.settle > 0:
         bed.step(args.settle)             # coarse relaxation of the jammed packing (not timed)
