@@ -14,7 +14,10 @@
 #ifndef SWEEPT2_MINB
 #define SWEEPT2_MINB 6
 #endif
-constexpr int TT = 128;
+#ifndef SWEEPT2_TILE
+#define SWEEPT2_TILE 128
+#endif
+constexpr int TT = SWEEPT2_TILE;   // particles per block tile (4 warps of 32 at the default)
 constexpr int NWT = TT / 32;
 
 __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { return make_double4(a.x, a.y, b.x, b.y); }
