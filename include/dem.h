@@ -257,7 +257,10 @@ dem_status dem_step(dem_ctx *ctx, int32_t n_steps, dem_step_report *last);
  * next step; the Verlet skin is kept. */
 dem_status dem_set_solver(dem_ctx *ctx, const dem_solver *solver);
 
-/* Copy particle state out (gid order).  view->n must be >= particle count. */
+/* Copy particle state out (gid order).  view->n must be >= the owned particle count (else
+ * DEM_ERR_INVALID with view->n set to it); on return view->n = the count.  Any field pointer may
+ * be NULL: that field is not copied (the field mask of SURVEY §8(b)).  on_device selects device or
+ * host buffers.  Decomposed: this rank's owned particles. */
 dem_status dem_get_state(dem_ctx *ctx, dem_state_view *view);
 
 /* Replace particle state (same gid set and radii as at create) and the contact history used
