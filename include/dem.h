@@ -291,6 +291,17 @@ dem_status dem_drive_plate(dem_ctx *ctx, int32_t plate, int32_t axis, int32_t mo
                            double f_min, double f_max /* N, velocity mode (Eq. 4) */);
 dem_status dem_get_plate(dem_ctx *ctx, int32_t plate, dem_plate_state *out);
 
+/* Change the particle set of a single context (the bed builder's emitter and trimming, SURVEY
+ * NEXT-2).  dem_add_particles appends n particles (pos 3n, radius n, vel/angvel 3n or
+ * NULL = 0, gid n: unique over the whole bed, < 2^32-4096; on_device: device pointers);
+ * dem_remove_particles removes every particle whose coordinate `axis` lies outside [lo, hi] and
+ * reports how many.  The state of the other particles and the contact history (the next step's
+ * warm start) are kept; the next step rebuilds.  DEM_ERR_INVALID: bad arguments, a decomposed
+ * context, or the validation of dem_create_bed (radius, finite positions, duplicate gid). */
+dem_status dem_add_particles(dem_ctx *ctx, int64_t n, const double *pos, const double *radius, const double *vel,
+                             const double *angvel, const uint32_t *gid, int32_t on_device);
+dem_status dem_remove_particles(dem_ctx *ctx, int32_t axis, double lo, double hi, int64_t *n_removed);
+
 /* Load balance of the x-slab decomposition; collective, a no-op without a
  * decomposition.  The owned particles' x are histogrammed over the box in n_bins >= 2 bins and
  * summed over the ranks; each interior face moves toward its particle-count quantile by at most

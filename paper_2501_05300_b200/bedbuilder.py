@@ -169,7 +169,7 @@ class _World:
         return float(0.5 * (m * (st["vel"] ** 2).sum(axis=1)).sum()) / max(len(m), 1)
 
     def sweeps(self, n_iter):
-        if self.bed is not None and n_iter != self.n_iter_now:
+        if self.bed is not None and n_iter and n_iter != self.n_iter_now:
             self.bed.set_solver(n_iter=n_iter)
             self.n_iter_now = n_iter
 
@@ -229,7 +229,12 @@ def build_bed(spec: BedSpec, device=0, bed_factory=None):
                 p[:, 2] = np.minimum(p[:, 2], Lz - 0.6 * d_n)
                 gid0 += len(rad)
                 W.add(p, rad, v, g, li)
-                W.open(spec.relax_mu, spec.n_iter_emit)
+                if W.bed is not None and hasattr(W.bed, "add_particles"):
+                    W.bed.add_particles(p, rad, v, None, g)      # dem_add_particles: state and history kept
+                    W.sweeps(spec.n_iter_emit or spec.n_iter)
+                    W.stepped = False
+                else:
+                    W.open(spec.relax_mu, spec.n_iter_emit)
                 # next plane once the bed is nearly at rest: max |v| < v_emit, or the mean kinetic
                 # energy that of every sphere moving at v_emit / 4 (a single rattler may not hold it up)
                 m_n = rho * np.pi / 6.0 * d_n ** 3
@@ -243,7 +248,11 @@ def build_bed(spec: BedSpec, device=0, bed_factory=None):
                 W.run_until(spec.v_threshold, spec.ke_threshold, spec.layer_budget)
                 W.pull()
                 W.keep(W.x[:, 2] <= top)
-                W.open(spec.relax_mu)
+                if hasattr(W.bed, "remove_particles"):
+                    W.bed.remove_particles(2, -np.inf, top)         # dem_remove_particles
+                    W.stepped = False
+                else:
+                    W.open(spec.relax_mu)
         if W.bed is not None:
             W.run_until(spec.v_threshold, spec.ke_threshold, spec.layer_budget)
             W.pull()

@@ -335,14 +335,15 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
     if (!ctx->lvbox) {
         TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
         TRY(A(ctx, &ctx->db, 1));
-        TRY(A(ctx, &ctx->pacc, 3 * DEM_MAX_PLATES));
+        TRY(A(ctx, &ctx->pacc, 3 * NB_SLOTS));
         TRY(A(ctx, &ctx->pcount, NB_SLOTS));
         TRY(A(ctx, &ctx->hub_acc, 3 * DEM_MAX_PLATES));
         CK(cudaMemsetAsync(ctx->hub_acc, 0, 3 * DEM_MAX_PLATES * sizeof(unsigned long long), ctx->s));
         TRY(A(ctx, &ctx->dsc, 1));
     }
     ctx->capN = cap;
-    ctx->cap_keys = 0;          // key/scan scratch is sized from capN at the next ensure_keys
+    // the key/scan scratch is not reset: it also serves the candidate and history sorts
+    // (ensure_cand sized it to cap_cand, which a particle reallocation leaves unchanged)
     return DEM_OK;
 }
 
@@ -782,9 +783,22 @@ static dem_status finish_decomposition(dem_ctx *ctx, const uint32_t *perm)
     return DEM_OK;
 }
 
+static dem_status sync_check(dem_ctx *ctx, const char *where)
+{
+    if (!getenv("DEM_SYNC_CHECK")) return DEM_OK;
+    const cudaError_t e = cudaStreamSynchronize(ctx->s);
+    const cudaError_t e2 = cudaGetLastError();
+    if (e != cudaSuccess || e2 != cudaSuccess) {
+        ctx->err = std::string("sync check at ") + where + ": " + cudaGetErrorString(e != cudaSuccess ? e : e2);
+        return DEM_ERR_CUDA;
+    }
+    return DEM_OK;
+}
+
 static dem_status rebuild(dem_ctx *ctx)
 {
     cudaStream_t s = ctx->s;
+    TRY(sync_check(ctx, "rebuild entry"));
     if (!ctx->hist_pending) TRY(export_history(ctx));
     ctx->hist_pending = false;
     if (ctx->tp) {
@@ -1226,6 +1240,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     }
     launch_scatter_P(nc, ctx->ccand, ctx->Pfa, ctx->Pfb, ctx->Pca, ctx->Pcb, s);
     ctx->launches += nc ? 1 : 0;
+    TRY(sync_check(ctx, "step end"));
     if (ctx->timing) {
         ctx->tm.ms_rebuild += telapsed(ctx, 0, 1);
         ctx->tm.ms_detect += telapsed(ctx, 1, 2);
@@ -1827,6 +1842,79 @@ void *dem_stream(dem_ctx *ctx) { return ctx ? (void *)ctx->s : nullptr; }
 int64_t dem_num_particles(const dem_ctx *ctx) { return ctx ? ctx->N_own : -1; }
 
 int64_t dem_num_local(const dem_ctx *ctx) { return ctx ? ctx->N : -1; }
+
+// the particle set changes (emitter, trimming): the current state is exported in
+// gid order on the device, edited, and loaded as a fresh set; the contact history is exported
+// first and handed to the next rebuild (dem_set_state's path), so the warm start survives
+static dem_status export_particles(dem_ctx *ctx, int64_t extra, double **x, double **r, double **v, double **w,
+                                   uint32_t **g)
+{
+    const int64_t N = ctx->N, M = N + extra;
+    TRY(A(ctx, x, 3 * M + 3)); TRY(A(ctx, r, M + 1)); TRY(A(ctx, v, 3 * M + 3)); TRY(A(ctx, w, 3 * M + 3));
+    TRY(A(ctx, g, M + 1));
+    if (ctx->have_step && !ctx->hist_pending) TRY(export_history(ctx));
+    ctx->hist_pending = true;
+    if (ctx->hauth && ctx->nh) CK(cudaMemsetAsync(ctx->hauth, 0, ctx->nh, ctx->s));
+    TRY(sync_check(ctx, "export_particles entry"));
+    launch_to_gid_order(N, N, nullptr, ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], *x,
+                        *v, *w, *r, *g, ctx->s);
+    ctx->launches++;
+    TRY(sync_check(ctx, "export_particles to_gid_order"));
+    return DEM_OK;
+}
+
+dem_status dem_add_particles(dem_ctx *ctx, int64_t n, const double *pos, const double *radius, const double *vel,
+                             const double *angvel, const uint32_t *gid, int32_t on_device)
+{
+    if (!ctx || n < 0 || (n && (!pos || !radius || !gid))) return DEM_ERR_INVALID;
+    if (ctx->tp) { ctx->err = "dem_add_particles needs a single undecomposed context"; return DEM_ERR_INVALID; }
+    if (!n) return DEM_OK;
+    cudaStream_t s = ctx->s;
+    const int64_t N = ctx->N;
+    double *x = nullptr, *r = nullptr, *v = nullptr, *w = nullptr;
+    uint32_t *g = nullptr;
+    TRY(export_particles(ctx, n, &x, &r, &v, &w, &g));
+    const cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(x + 3 * N, pos, 3 * n * 8, k, s));
+    CK(cudaMemcpyAsync(r + N, radius, n * 8, k, s));
+    CK(cudaMemcpyAsync(g + N, gid, n * 4, k, s));
+    if (vel) CK(cudaMemcpyAsync(v + 3 * N, vel, 3 * n * 8, k, s)); else CK(cudaMemsetAsync(v + 3 * N, 0, 3 * n * 8, s));
+    if (angvel) CK(cudaMemcpyAsync(w + 3 * N, angvel, 3 * n * 8, k, s)); else CK(cudaMemsetAsync(w + 3 * N, 0, 3 * n * 8, s));
+    CK(cudaStreamSynchronize(s));
+    const dem_status st = load_particles(ctx, N + n, x, r, v, w, g, 1, true);
+    for (void *q : {(void *)x, (void *)r, (void *)v, (void *)w, (void *)g}) dfree(ctx, q);
+    if (st == DEM_OK) TRY(sync_check(ctx, "add_particles end"));
+    return st;
+}
+
+dem_status dem_remove_particles(dem_ctx *ctx, int32_t axis, double lo, double hi, int64_t *n_removed)
+{
+    if (!ctx || axis < 0 || axis > 2 || std::isnan(lo) || std::isnan(hi)) return DEM_ERR_INVALID;
+    if (ctx->tp) { ctx->err = "dem_remove_particles needs a single undecomposed context"; return DEM_ERR_INVALID; }
+    cudaStream_t s = ctx->s;
+    const int64_t N = ctx->N;
+    double *x = nullptr, *r = nullptr, *v = nullptr, *w = nullptr;
+    uint32_t *g = nullptr, *flag = nullptr, *scan = nullptr;
+    TRY(export_particles(ctx, 0, &x, &r, &v, &w, &g));
+    TRY(A(ctx, &flag, N + 2)); TRY(A(ctx, &scan, N + 2));
+    launch_keep(N, x, axis, lo, hi, flag, s);
+    scan_u32(flag, scan, N, ctx->scan_tmp, s, &ctx->launches);
+    uint32_t keep = 0;
+    CK(cudaMemcpyAsync(&keep, scan + N, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    double *x2 = nullptr, *r2 = nullptr, *v2 = nullptr, *w2 = nullptr;
+    uint32_t *g2 = nullptr;
+    TRY(A(ctx, &x2, 3 * (int64_t)keep + 3)); TRY(A(ctx, &r2, keep + 1)); TRY(A(ctx, &v2, 3 * (int64_t)keep + 3));
+    TRY(A(ctx, &w2, 3 * (int64_t)keep + 3)); TRY(A(ctx, &g2, keep + 1));
+    launch_keep_gather(N, flag, scan, x, r, v, w, g, x2, r2, v2, w2, g2, s);
+    CK(cudaStreamSynchronize(s));
+    const dem_status st = load_particles(ctx, keep, x2, r2, v2, w2, g2, 1, true);
+    for (void *q : {(void *)x, (void *)r, (void *)v, (void *)w, (void *)g, (void *)flag, (void *)scan, (void *)x2,
+                    (void *)r2, (void *)v2, (void *)w2, (void *)g2})
+        dfree(ctx, q);
+    if (n_removed) *n_removed = N - (int64_t)keep;
+    return st;
+}
 
 dem_status dem_rebalance(dem_ctx *ctx, int32_t n_bins, double *faces_out)
 {

@@ -100,6 +100,10 @@ void launch_plate_list_flags(int64_t nc, const uint8_t *own, const uint2 *cij, u
 void launch_plate_hub(bool p8, int64_t n, const uint32_t *list, const uint2 *cij, const G4 *geo, const void *pin,
                       const void *pout, unsigned long long *acc, cudaStream_t s);
 void launch_plate_kick(DevBoundary *bnd, unsigned long long *acc, double h, int first, cudaStream_t s);
+void launch_keep(int64_t n, const double *x, int axis, double lo, double hi, uint32_t *flag, cudaStream_t s);
+void launch_keep_gather(int64_t n, const uint32_t *flag, const uint32_t *scan, const double *x, const double *r,
+                        const double *v, const double *w, const uint32_t *g, double *ox, double *orr, double *ov,
+                        double *ow, uint32_t *og, cudaStream_t s);
 void launch_residuals(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const R4 *row, const double4 *vel,
                       const P4 *Pa, const P4 *Pb, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
                       cudaStream_t s);

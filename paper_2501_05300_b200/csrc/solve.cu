@@ -827,6 +827,33 @@ __global__ void k_to_gid_order(int64_t N, const uint8_t *__restrict__ own, const
     if (ogid) ogid[o] = gv;
 }
 
+// keep particles with lo <= x[axis] <= hi: compaction of the gid-ordered export
+__global__ void k_keep_flags(int64_t n, const double *__restrict__ x, int axis, double lo, double hi,
+                             uint32_t *__restrict__ flag)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) { const double v = x[3 * i + axis]; flag[i] = (v >= lo && v <= hi) ? 1u : 0u; }
+}
+__global__ void k_keep_gather(int64_t n, const uint32_t *__restrict__ flag, const uint32_t *__restrict__ scan,
+                              const double *__restrict__ x, const double *__restrict__ r, const double *__restrict__ v,
+                              const double *__restrict__ w, const uint32_t *__restrict__ g, double *__restrict__ ox,
+                              double *__restrict__ orr, double *__restrict__ ov, double *__restrict__ ow,
+                              uint32_t *__restrict__ og)
+{
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !flag[i]) return;
+    const uint32_t o = scan[i];
+    for (int k = 0; k < 3; k++) { ox[3 * o + k] = x[3 * i + k]; ov[3 * o + k] = v[3 * i + k]; ow[3 * o + k] = w[3 * i + k]; }
+    orr[o] = r[i];
+    og[o] = g[i];
+}
+void launch_keep(int64_t n, const double *x, int axis, double lo, double hi, uint32_t *flag, cudaStream_t s)
+{ if (n) k_keep_flags<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, x, axis, lo, hi, flag); }
+void launch_keep_gather(int64_t n, const uint32_t *flag, const uint32_t *scan, const double *x, const double *r,
+                        const double *v, const double *w, const uint32_t *g, double *ox, double *orr, double *ov,
+                        double *ow, uint32_t *og, cudaStream_t s)
+{ if (n) k_keep_gather<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, flag, scan, x, r, v, w, g, ox, orr, ov, ow, og); }
+
 // caller arrays -> internal double4 layout
 __global__ void k_load_state(int64_t N, const double *__restrict__ x, const double *__restrict__ r,
                              const double *__restrict__ v, const double *__restrict__ w,

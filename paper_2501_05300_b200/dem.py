@@ -126,7 +126,7 @@ CONTACT_DTYPE = np.dtype([("key", "<u8"), ("n", "<f8", (3,)), ("delta", "<f8"), 
 # every symbol include/dem.h declares (checked by tests/test_boundary.py)
 EXPORTS = ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts", "dem_get_forces",
            "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_get_wall", "dem_set_timing",
-           "dem_get_timing", "dem_rebalance",
+           "dem_get_timing", "dem_rebalance", "dem_add_particles", "dem_remove_particles",
            "dem_reset_timing", "dem_bench_sweeps", "dem_num_particles", "dem_num_local", "dem_nccl_unique_id",
            "dem_loopback_create", "dem_loopback_destroy", "dem_generator_count", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
            "dem_contact_network_length", "dem_plan_iterations", "dem_plan_timestep"]
@@ -155,6 +155,10 @@ def lib():
         L.dem_drive_wall.argtypes = [vp, i32, d]
         L.dem_get_wall.argtypes = [vp, i32, C.POINTER(WallState)]
         L.dem_rebalance.argtypes = [vp, i32, C.POINTER(C.c_double)]
+        L.dem_add_particles.argtypes = [vp, C.c_int64, vp, vp, vp, vp, vp, i32]
+        L.dem_add_particles.restype = C.c_int
+        L.dem_remove_particles.argtypes = [vp, i32, d, d, C.POINTER(C.c_int64)]
+        L.dem_remove_particles.restype = C.c_int
         L.dem_rebalance.restype = C.c_int
         L.dem_set_timing.argtypes = [vp, i32]
         L.dem_get_timing.argtypes = [vp, C.POINTER(Timing)]
@@ -510,6 +514,23 @@ class Bed:
         self._check(lib().dem_get_plate(self._h, plate, C.byref(s)))
         return {"pos": list(s.pos), "vel": list(s.vel), "force": list(s.force),
                 "motor_force": list(s.motor_force), "n_contacts": s.n_contacts}
+
+    def add_particles(self, pos, radius, vel=None, angvel=None, gid=None):
+        """dem_add_particles (single context): append particles, keeping state and contact history."""
+        pos, radius = _f64(pos, (-1, 3)), _f64(radius)
+        vel, angvel = _f64(vel, (-1, 3)), _f64(angvel, (-1, 3))
+        gid = np.ascontiguousarray(gid, dtype=np.uint32)
+        self._check(lib().dem_add_particles(self._h, len(radius), _ptr(pos), _ptr(radius), _ptr(vel), _ptr(angvel),
+                                            _ptr(gid), 0))
+        self.n = self.n_owned
+
+    def remove_particles(self, axis, lo, hi):
+        """dem_remove_particles (single context): drop particles with x[axis] outside [lo, hi];
+        returns how many were removed."""
+        out = C.c_int64()
+        self._check(lib().dem_remove_particles(self._h, int(axis), float(lo), float(hi), C.byref(out)))
+        self.n = self.n_owned
+        return out.value
 
     def rebalance(self, n_bins=1024, world_size=None):
         """dem_rebalance (collective): slab faces toward particle-count quantiles; returns the

@@ -551,3 +551,42 @@ def test_checkpoint_resume_bit_identical(tmp_path):
     finally:
         a.close()
         b.close()
+
+
+def test_add_and_remove_particles_match_recreate():
+    """dem_add_particles / dem_remove_particles keep the state and the contact history: the run
+    continues bit-identically to re-creating the bed from the edited state with the history
+    handed back through dem_set_state."""
+    D = dem()
+    bed = synth.random_cloud(400, (0.002, 0.002, 0.002), (0.038, 0.038, 0.025), 1.5e-3, 3e-3, 13, v_scale=0.05)
+    kw = dict(solver=dict(dt=2e-5, n_iter=30), box=dict(lo=(0, 0, 0), hi=(0.04, 0.04, 0.06)))
+    extra = synth.random_cloud(60, (0.005, 0.005, 0.04), (0.035, 0.035, 0.05), 1.5e-3, 2.5e-3, 14)
+    xg = (np.arange(60) + 1000).astype(np.uint32)
+    a = D.Bed(bed.x, bed.r, bed.v, bed.w, bed.gid, **kw)
+    a.step(15)
+    st, c = a.get_state(), a.get_contacts()
+    a.add_particles(extra.x, extra.r, gid=xg)
+    a.step(10)
+    removed = a.remove_particles(2, -1.0, 0.02)
+    a.step(10)
+    # the same through re-creation
+    x = np.concatenate([st["pos"], extra.x]); r = np.concatenate([st["radius"], extra.r])
+    v = np.concatenate([st["vel"], np.zeros((60, 3))]); w = np.concatenate([st["angvel"], np.zeros((60, 3))])
+    g = np.concatenate([st["gid"], xg])
+    b = D.Bed(x, r, v, w, g, **kw)
+    b.set_state(x, r, v, w, g, hist=c)
+    b.step(10)
+    st2, c2 = b.get_state(), b.get_contacts()
+    keep = st2["pos"][:, 2] <= 0.02
+    b.close()
+    b = D.Bed(st2["pos"][keep], st2["radius"][keep], st2["vel"][keep], st2["angvel"][keep], st2["gid"][keep], **kw)
+    b.set_state(st2["pos"][keep], st2["radius"][keep], st2["vel"][keep], st2["angvel"][keep], st2["gid"][keep], hist=c2)
+    b.step(10)
+    try:
+        assert removed == int((~keep).sum()) and removed > 0
+        sa, sb = a.get_state(), b.get_state()
+        for k in ("gid", "pos", "vel", "angvel"):
+            assert np.array_equal(sa[k], sb[k]), k
+    finally:
+        a.close()
+        b.close()
