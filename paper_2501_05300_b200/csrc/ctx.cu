@@ -1755,6 +1755,8 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     double4 *vbuf[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel2}, *wbuf[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang2};
     float ms = 0.f;
     double4 *vres = nullptr;
+    G4 *plg = nullptr;
+    R4 *plr = nullptr;
     for (int pass = 0; pass < 2; pass++) {
         const int var = pass == 0 ? 0 : variant;
         CK(cudaMemcpyAsync(ctx->Pwa, ctx->Pfa, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
@@ -1788,10 +1790,17 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
         }
         const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
         P4 *pai = ctx->Pwa, *pbi = ctx->Pwb, *pao = spa, *pbo = spb;
-        if ((var == 0 || var == 8 || var == 44 || var == 45) && PKV(ctx)) {
+        if ((var == 0 || var == 8 || var == 9 || var == 44 || var == 45) && PKV(ctx)) {
             p8_pack(nc, ctx->Pwa, ctx->Pwb, ctx->p8[0], s);
             ctx->pkv.geo = var == 8 ? ctx->geo : ctx->pk_geo;
             ctx->pkv.row = var == 8 ? ctx->row : ctx->pk_row;
+            if (var == 9) {   // the staged kernel reads chunk-plane records
+                if (!plg) { TRY(A(ctx, &plg, ctx->pk_n)); TRY(A(ctx, &plr, ctx->pk_n)); }
+                to_planes(ctx->pk_n, ctx->pk_geo, plg, s);
+                to_planes(ctx->pk_n, ctx->pk_row, plr, s);
+                ctx->pkv.geo = plg;
+                ctx->pkv.row = plr;
+            }
         }
         cudaEventRecord(ctx->ev[6], s);
         for (int it = 0; it < n; it++) {
@@ -1833,6 +1842,8 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     dfree(ctx, cb);
     dfree(ctx, ref);
     dfree(ctx, md);
+    dfree(ctx, plg);
+    dfree(ctx, plr);
 
     return DEM_OK;
 }

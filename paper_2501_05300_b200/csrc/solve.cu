@@ -897,14 +897,16 @@ void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin
         k_sweep_pipe<<<(unsigned)((N + TPP - 1) / TPP), TPP, sizeof(PipeSmem), s>>>(
             N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
     } else if (mode == SWEEP_MODE_SWEEP && (g_sweep_variant == 0 || g_sweep_variant == 7 || g_sweep_variant == 8 ||
-                                            g_sweep_variant == 44 || g_sweep_variant == 45)) {
+                                            g_sweep_variant == 9 || g_sweep_variant == 44 || g_sweep_variant == 45)) {
         // 0: the context's reduction (packed canonical if pk, else contiguous); 7: contiguous;
         // 8: packed with contact-indexed normals/rows (diagnostic; pk->geo/row set by the caller)
         g_t2_rows_by_contact = g_sweep_variant == 8;
+        g_t2_stage = g_sweep_variant == 9;
         g_t2_exp = g_sweep_variant == 44 ? 1 : (g_sweep_variant == 45 ? 2 : 0);
         launch_sweep_t2(N, vin, win, vout, wout, inc_start, inc, g_sweep_variant == 7 ? nullptr : pk, geo, row, Pa_in,
                         Pb_in, Pa_out, Pb_out, bnd, sp, s);
         g_t2_rows_by_contact = false;
+        g_t2_stage = false;
         g_t2_exp = 0;
     }
     else if (mode == SWEEP_MODE_SWEEP)

@@ -33,6 +33,7 @@ __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { retu
 // every decomposition and warp grouping produces the same bits.
 constexpr uint32_t PK_HOLE = 0xFFFFFFFFu;
 bool g_t2_rows_by_contact = false;
+bool g_t2_stage = false;
 int g_t2_exp = 0;
 
 // one warp per 32 consecutive particles (the sweep's warp grouping): first-fit packing
@@ -165,7 +166,64 @@ __device__ __forceinline__ HalfOut t2_fake(const double4 VA, const double4 WA, c
     return o;
 }
 
-template <bool PACKED, bool ROWS_PK = true, int EXP = 0>
+// ---- one-chunk-ahead TMA staging (STG): the chunk's packed incidence, normals and rows are
+// contiguous (1 KB + 1 KB + 256 B), so one lane per warp moves them with 1D bulk copies
+// (cp.async.bulk, completion on an mbarrier) into a two-slot ring while the warp computes the
+// previous chunk: no registers held for the prefetch, no LSU instructions for the records.
+constexpr int STG_BYTES = 32 * (int)sizeof(G4) + 32 * (int)sizeof(R4) + 32 * (int)sizeof(uint2);
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+struct __align__(128) StgSlot { G4 g[32]; R4 r[32]; uint2 e[32]; };
+__device__ __forceinline__ void stg_issue(StgSlot *sl, uint64_t *bar, const G4 *geo, const R4 *row, const uint2 *inc,
+                                          uint32_t kb)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads of the slot before the refill
+    mbar_expect_tx(bar, STG_BYTES);
+    bulk_g2s(sl->g, geo + kb, 32 * sizeof(G4), bar);
+    bulk_g2s(sl->r, row + kb, 32 * sizeof(R4), bar);
+    bulk_g2s(sl->e, inc + kb, 32 * sizeof(uint2), bar);
+}
+// a staged chunk's records are stored as two planes (x,y of the 32 lanes, then z,w): each
+// LDS.128 of the warp then reads 512 contiguous bytes, conflict-free
+__device__ __forceinline__ double4 lds_plane(const double4 *base, int lane)
+{
+    const double2 *p = reinterpret_cast<const double2 *>(base);
+    const double2 a = p[lane], b = p[32 + lane];
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+__global__ void k_to_planes(int64_t np, const double4 *__restrict__ in, double2 *__restrict__ out)
+{
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= np) return;
+    const double4 v = in[k];
+    const int64_t c = k >> 5, l = k & 31;
+    out[64 * c + l] = make_double2(v.x, v.y);
+    out[64 * c + 32 + l] = make_double2(v.z, v.w);
+}
+void to_planes(int64_t np, const double4 *in, double4 *out, cudaStream_t s)
+{ if (np) k_to_planes<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(np, in, reinterpret_cast<double2 *>(out)); }
+
+template <bool PACKED, bool ROWS_PK = true, int EXP = 0, bool STG = false>
 __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     k_sweep_t2(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win, double4 *__restrict__ vout,
                double4 *__restrict__ wout, const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
@@ -180,7 +238,14 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
     __shared__ uint8_t sOwn[NWT][32];
     __shared__ uint32_t sI[TT + 1];
     __shared__ uint32_t sPS[PACKED ? TT : 1];
+    __shared__ StgSlot sStg[STG ? NWT : 1][STG ? 2 : 1];
+    __shared__ uint64_t sBar[NWT][2];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (STG && lane == 0) {
+        mbar_init(&sBar[w][0], 1);
+        mbar_init(&sBar[w][1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     const int64_t p0 = (int64_t)blockIdx.x * TT;
     const int np = (int)min((int64_t)TT, N - p0);
     if (t < np) {
@@ -201,13 +266,30 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
         const uint32_t k0 = PACKED ? wbase[(p0 >> 5) + w] : sI[lo_p];
         const uint32_t k1 = PACKED ? wbase[(p0 >> 5) + w + 1] : sI[hi_p];
         uint2 ent_next = make_uint2(0, 0);
-        if (k0 + lane < k1) ent_next = inc[k0 + lane];
+        if (STG) {
+            if (lane == 0) {
+                stg_issue(&sStg[w][0], &sBar[w][0], geo, row, inc, k0);
+                if (k0 + 32 < k1) stg_issue(&sStg[w][1], &sBar[w][1], geo, row, inc, k0 + 32);
+            }
+        } else if (k0 + lane < k1) ent_next = inc[k0 + lane];
         int carry = 0;
-        for (uint32_t kb = k0; kb < k1; kb += 32) {
+        uint32_t it = 0;
+        for (uint32_t kb = k0; kb < k1; kb += 32, it++) {
             const uint32_t k = kb + lane;
-            const uint2 ent = ent_next;
+            uint2 ent = ent_next;
+            G4 gs;
+            R4 rs;
+            if (STG) {
+                // chunk it sits in slot it & 1, filled for the (it >> 1)-th time
+                StgSlot *sl = &sStg[w][it & 1];
+                mbar_wait(&sBar[w][it & 1], (it >> 1) & 1u);
+                ent = sl->e[lane];
+                if (ent.x != PK_HOLE) { gs = lds_plane(sl->g, lane); rs = lds_plane(sl->r, lane); }
+                __syncwarp();
+                if (lane == 0 && kb + 64 < k1) stg_issue(sl, &sBar[w][it & 1], geo, row, inc, kb + 64);
+            }
             const bool valid = k < k1 && (!PACKED || ent.x != PK_HOLE);
-            if (kb + 32 + lane < k1) ent_next = inc[kb + 32 + lane];
+            if (!STG && kb + 32 + lane < k1) ent_next = inc[kb + 32 + lane];
             const bool starts = e_me > s_me && s_me >= kb && s_me < kb + 32;
             const unsigned smask = __reduce_or_sync(0xffffffffu, starts ? (1u << (s_me - kb)) : 0u);
             if (starts) sOwn[w][s_me - kb] = (uint8_t)lane;
@@ -230,8 +312,11 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                     g = mkG4(0.6, 0.0, 0.8, 1e-4); rw = mkR4(1e-3, 1e-3, 1e-3, 1e-3);
                     pa = mkP4(1e-6, 0, 0, 0); pb = mkP4(0, 0, 0, 0);
                 } else {
-                    g = ld4g(PACKED && ROWS_PK ? &geo[k] : &geo[c]);
-                    rw = ld4g(PACKED && ROWS_PK ? &row[k] : &row[c]);
+                    if (STG) { g = gs; rw = rs; }
+                    else {
+                        g = ld4g(PACKED && ROWS_PK ? &geo[k] : &geo[c]);
+                        rw = ld4g(PACKED && ROWS_PK ? &row[k] : &row[c]);
+                    }
                     if (PACKED) { const P8 q = ldP8(&P8_in[c]); pa = q.a; pb = q.b; }
                     else { pa = Pa_in[c]; pb = Pb_in[c]; }
                 }
@@ -310,7 +395,11 @@ void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 
                                                         pk->p8out, bnd, sp);
         return;
     }
-    if (pk && g_t2_rows_by_contact)   // diagnostic (dem_bench_sweeps 8): contact-indexed rows
+    if (pk && g_t2_stage)             // dem_bench_sweeps 9: TMA-staged records
+        k_sweep_t2<true, true, 0, true><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start,
+                                                          pk->wbase, pk->geo, pk->row, nullptr, nullptr, nullptr, nullptr,
+                                                          pk->p8in, pk->p8out, bnd, sp);
+    else if (pk && g_t2_rows_by_contact)   // diagnostic (dem_bench_sweeps 8): contact-indexed rows
         k_sweep_t2<true, false><<<gb, TT, 0, s>>>(N, vin, win, vout, wout, inc_start, pk->inc, pk->start, pk->wbase,
                                                   pk->geo, pk->row, nullptr, nullptr, nullptr, nullptr, pk->p8in,
                                                   pk->p8out, bnd, sp);
