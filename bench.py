@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -44,6 +45,10 @@ WORKLOADS = {
                          dt=5e-6, seed=1004),
     "config1": dict(dims=(0.4, 0.4, 0.3), bands=[(0.0, 0.06, 2e-3), (0.06, 0.3, 4e-3)], dt=5e-6, seed=1001),
     "config3-geom": dict(dims=(1.0, 0.5, 0.3), bands=[(0.0, 0.3, 2e-3)], dt=5e-6, seed=1003),
+    "config3-count": dict(dims=(4.3, 0.5, 0.3), bands=[(0.0, 0.3, 2e-3)], dt=5e-6, seed=1003),
+    # config 2: diameter linear in depth (Eq. 1), d 4 -> 32 mm over the 0.5 m depth (gamma 0.056)
+    "config2-geom": dict(dims=(1.0, 0.5, 0.5), profile=(4e-3, 0.056, 32e-3), dt=5e-6, seed=1002),
+    "config2-count": dict(dims=(7.8, 0.5, 0.5), profile=(4e-3, 0.056, 32e-3), dt=5e-6, seed=1002),
 }
 ALG_B_PARTICLE = 112     # algorithmic bytes per particle per sweep
 ALG_B_CONTACT = 72       # ... per contact per sweep
@@ -54,9 +59,37 @@ def network_length(bands):
     return sum((b - a) / (2 * r) for a, b, r in bands)
 
 
-def make_bed(wl, seed_offset=0, spacing=2.0):
+def workload_network_length(w):
+    """n_d of a workload: discrete bands, or Eq. 10 for the linear profile d = d_min + gamma z
+    (capped at d_max): int_0^H dz / d(z)."""
+    if "bands" in w:
+        return network_length(w["bands"])
+    d_min, gamma, d_max = w["profile"]
+    H = w["dims"][2]
+    z_cap = (d_max - d_min) / gamma
+    if z_cap >= H:
+        return math.log((d_min + gamma * H) / d_min) / gamma
+    return math.log(d_max / d_min) / gamma + (H - z_cap) / d_max
+
+
+def make_bed(wl, seed_offset=0, spacing=2.0, dims=None):
+    """The workload bed on the host (synth); dims overrides the box (bounded oracle samples)."""
     w = WORKLOADS[wl]
-    return synth.banded_bed(w["dims"], w["bands"], w["seed"] + seed_offset, spacing=spacing, name=wl)
+    dims = tuple(dims or w["dims"])
+    if "profile" in w:
+        d_min, gamma, d_max = w["profile"]
+        H = dims[2]
+        return synth.graded_bed(dims, d_min / 2, min(d_max, d_min + gamma * H) / 2, min(H, (d_max - d_min) / gamma),
+                                w["seed"] + seed_offset, spacing=spacing, name=wl)
+    return synth.banded_bed(dims, w["bands"], w["seed"] + seed_offset, spacing=spacing, name=wl)
+
+
+def workload_levels(w):
+    """Size classes of the multi-level grid (factor-2 radius bins): bands, or the profile's span."""
+    if "bands" in w:
+        return len(w["bands"])
+    d_min, gamma, d_max = w["profile"]
+    return int(math.ceil(math.log2(min(d_max, d_min + gamma * w["dims"][2]) / d_min) - 1e-9))
 
 
 def make_slab(wl, rank, world):
@@ -69,6 +102,10 @@ def device_generator(wl):
     """The workload bed as an on-device generator (include/dem.h dem_generator, kind bands): the
     same lattice recipe as synth.banded_bed (tests/test_boundary.py checks the site counts)."""
     w = WORKLOADS[wl]
+    if "profile" in w:
+        d_min, gamma, d_max = w["profile"]
+        return dict(kind="profile", d_min=d_min, gamma=gamma, d_max=d_max, spacing_factor=2.0, pos_jitter=0.01,
+                    size_jitter=0.10, seed=w["seed"])
     return dict(kind="bands", bands=[(b, r) for (_, b, r) in w["bands"]], spacing_factor=2.0, pos_jitter=0.01,
                 size_jitter=0.10, seed=w["seed"])
 
@@ -122,7 +159,7 @@ def cpu_baseline(wl, n_it, dt, budget_s=15.0):
     w = WORKLOADS[wl]
     dims = w["dims"]
     col = (0.06, 0.06, dims[2])
-    b = synth.banded_bed(col, w["bands"], w["seed"] + 77, spacing=2.0)
+    b = make_bed(wl, seed_offset=77, dims=col)
     Wd = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi))
     p = O.make_params(h=dt, n_it=n_it)
     t0 = time.perf_counter()
@@ -141,12 +178,12 @@ def cpu_baseline(wl, n_it, dt, budget_s=15.0):
 def run_reference(args, rank, world):
     wl = args.workload
     w = WORKLOADS[wl]
-    n_it = args.n_it or int(np.ceil(0.1 * network_length(w["bands"]) / 0.02 - 1e-9))
+    n_it = args.n_it or int(np.ceil(0.1 * workload_network_length(w) / 0.02 - 1e-9))
     if rank != 0:
         return
     import oracle as O
     dims = w["dims"]
-    b = synth.banded_bed((0.05, 0.05, dims[2]), w["bands"], w["seed"] + 99, spacing=2.0)
+    b = make_bed(wl, seed_offset=99, dims=(0.05, 0.05, dims[2]))
     Wd = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi))
     p = O.make_params(h=w["dt"], n_it=n_it)
     for _ in range(args.warmup):
@@ -205,7 +242,7 @@ def main():
 
     wl = args.workload
     w = WORKLOADS[wl]
-    n_it = args.n_it or dem.plan_iterations(network_length(w["bands"]), 0.02)
+    n_it = args.n_it or dem.plan_iterations(workload_network_length(w), 0.02)
     # the bed is generated on the device (dem_generator): N workload beds end to end along x for
     # N ranks, rank r generating the sites of its slab [r L, (r+1) L) under global gids
     L = w["dims"][0]
@@ -299,7 +336,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "n_particles": int(N_total), "generator": "on-device (dem_generator)", "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "rebuilds_per_step": rebuild_rate,
-                   "levels": len(w["bands"]),
+                   "levels": workload_levels(w),
                    "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)"
                    if (world > 1 or args.decompose) else "single GPU",
                    "l2": l2_note,

@@ -27,7 +27,7 @@ def main():
     from paper_2501_05300_b200 import dem
     w = bench.WORKLOADS[a.workload]
     b = bench.make_bed(a.workload)
-    n_it = dem.plan_iterations(bench.network_length(w["bands"]), 0.02)
+    n_it = dem.plan_iterations(bench.workload_network_length(w), 0.02)
     bed = dem.Bed(b.x, b.r, b.v, b.w, b.gid, device=0, solver=dict(dt=1e-4, n_iter=20),
                   box=dict(lo=b.box_lo, hi=b.box_hi))
     if a.settle:
