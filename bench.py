@@ -282,14 +282,16 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     reps = []
+    step_ms = []
     if flush is None:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        evs[0].record(stream)
+        for k in range(args.steps):
             reps.append(bed.step(1))
-        e1.record(stream)
+            evs[k + 1].record(stream)
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1)
+        ms = evs[0].elapsed_time(evs[-1])
+        step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     else:
         ev = []
         for _ in range(args.steps):
@@ -301,7 +303,8 @@ def main():
             b.record(stream)
             ev.append((a, b))
         torch.cuda.synchronize()
-        ms = sum(a.elapsed_time(b) for a, b in ev)
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        ms = sum(step_ms)
     if dist:
         dist.barrier()
     ck = clocks.stop() if not args.profile else None
@@ -332,7 +335,10 @@ def main():
             traffic = None
     out = {
         "metric": "particle-steps/s", "value": value, "unit": "particle-steps/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "ms_per_step_spread": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms),
+                               "rank": rank} if step_ms else None,
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "n_particles": int(N_total), "generator": "on-device (dem_generator)", "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "rebuilds_per_step": rebuild_rate,
