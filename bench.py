@@ -148,8 +148,14 @@ class ClockSampler:
             for k, n in enumerate(names):
                 if r[5 + k].strip() == "Active":
                     reasons.add(n)
+        pw = []
+        for r in rows:
+            try:
+                pw.append(float(r[3]))
+            except ValueError:
+                pass
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
-                "samples": len(rows)}
+                "samples": len(rows), "power_w": float(np.median(pw)) if pw else None}
 
 
 def cpu_baseline(wl, n_it, dt, budget_s=15.0):
