@@ -412,9 +412,28 @@ __global__ void k_level_bbox(int64_t N, const double4 *__restrict__ pos, double 
     }
     __syncthreads();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < N) {
-        const double4 p = pos[i];
-        const int L = level_of(p.w, rmin, nlev);
+    // warp-level min/max first when the warp's particles share a level (the sorted order makes
+    // that the rule), so only lane 0 touches the shared box: per-thread shared atomics on the
+    // same 7 words serialised the kernel (1.2 ms for 14.6 M particles)
+    const bool act = i < N;
+    double4 p = act ? pos[i] : make_double4(0.0, 0.0, 0.0, 0.0);
+    const int L = act ? level_of(p.w, rmin, nlev) : -1;
+    const int L0 = __shfl_sync(0xffffffffu, L, 0);
+    if (__all_sync(0xffffffffu, L == L0) && L0 >= 0) {
+        unsigned long long v[6];
+        const double c[3] = {p.x, p.y, p.z};
+        for (int k = 0; k < 3; k++) { v[k] = ord_bits(c[k]); v[3 + k] = v[k]; }
+        for (int o = 16; o; o >>= 1)
+            for (int k = 0; k < 3; k++) {
+                v[k] = min(v[k], __shfl_xor_sync(0xffffffffu, v[k], o));
+                v[3 + k] = max(v[3 + k], __shfl_xor_sync(0xffffffffu, v[3 + k], o));
+            }
+        if ((threadIdx.x & 31) == 0) {
+            unsigned long long *b = sb + 8 * L0;
+            for (int k = 0; k < 3; k++) { atomicMin(&b[k], v[k]); atomicMax(&b[3 + k], v[3 + k]); }
+            atomicAdd(&b[6], 32ULL);
+        }
+    } else if (act) {
         unsigned long long *b = sb + 8 * L;
         const double c[3] = {p.x, p.y, p.z};
         for (int k = 0; k < 3; k++) {
