@@ -204,7 +204,7 @@ def run_reference(args, rank, world):
     print(json.dumps({
         "impl": "reference", "metric": "particle-steps/s", "value": val, "unit": "particle-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl + " (oracle sample)", "n_particles": b.n, "n_it": n_it, "dt": w["dt"]},
         "cpu_baseline": {"value": val, "unit": "particle-steps/s", "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": val, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -219,6 +219,8 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--workload", default="config4-geom", choices=sorted(WORKLOADS))
     ap.add_argument("--n-it", type=int, default=0)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: one workload bed per GPU (default); strong: the workload bed split into N slabs")
     ap.add_argument("--settle", type=int, default=20)
     ap.add_argument("--settle-dt", type=float, default=1e-4, help="time step of the coarse relaxation (untimed)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -251,8 +253,10 @@ def main():
     n_it = args.n_it or dem.plan_iterations(workload_network_length(w), 0.02)
     # the bed is generated on the device (dem_generator): N workload beds end to end along x for
     # N ranks, rank r generating the sites of its slab [r L, (r+1) L) under global gids
-    L = w["dims"][0]
-    box = dict(lo=(0.0, 0.0, 0.0), hi=(world * L, w["dims"][1], w["dims"][2]))
+    # weak: N workload lengths end to end, one per rank; strong: the workload's own bed cut into N slabs
+    L_total = w["dims"][0] * (world if args.scaling == "weak" else 1)
+    L = L_total / world
+    box = dict(lo=(0.0, 0.0, 0.0), hi=(L_total, w["dims"][1], w["dims"][2]))
     gen = device_generator(wl)
     dcfg = None
     if world > 1 or args.decompose:
@@ -345,7 +349,7 @@ def main():
         "ms_per_step_spread": {"min": min(step_ms), "median": float(np.median(step_ms)), "max": max(step_ms),
                                "rank": rank} if step_ms else None,
         "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl, "n_particles": int(N_total), "generator": "on-device (dem_generator)", "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "rebuilds_per_step": rebuild_rate,
                    "levels": workload_levels(w),
