@@ -590,3 +590,37 @@ def test_add_and_remove_particles_match_recreate():
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.gpu
+def test_add_particles_on_dense_bed_matches_recreate():
+    """Regression: a particle reallocation must leave the candidate-sized key/sort scratch intact.
+    On a jammed FCC bed the candidate count is several times N, so history export and the
+    candidate sorts after dem_add_particles overran a scratch resized to 1.5 N."""
+    D = dem()
+    bed = synth.banded_bed((0.05, 0.05, 0.03), [(0.0, 0.03, 1.5e-3)], 21, spacing=2.0)
+    kw = dict(solver=dict(dt=1e-5, n_iter=20), box=dict(lo=(0, 0, 0), hi=(0.05, 0.05, 0.06)))
+    n_x = 40
+    extra = synth.random_cloud(n_x, (0.006, 0.006, 0.04), (0.044, 0.044, 0.05), 1.2e-3, 1.5e-3, 22)
+    xg = (np.arange(n_x) + bed.n + 100).astype(np.uint32)
+    a = D.Bed(bed.x, bed.r, bed.v, bed.w, bed.gid, **kw)
+    rep = a.step(3)
+    assert rep["n_contacts"] > 2 * bed.n
+    st, c = a.get_state(), a.get_contacts()
+    a.add_particles(extra.x, extra.r, gid=xg)
+    a.step(6)
+    x = np.concatenate([st["pos"], extra.x]); r = np.concatenate([st["radius"], extra.r])
+    v = np.concatenate([st["vel"], np.zeros((n_x, 3))]); w = np.concatenate([st["angvel"], np.zeros((n_x, 3))])
+    g = np.concatenate([st["gid"], xg])
+    b = D.Bed(x, r, v, w, g, **kw)
+    b.set_state(x, r, v, w, g, hist=c)
+    b.step(6)
+    try:
+        sa, sb = a.get_state(), b.get_state()
+        for k in ("gid", "pos", "vel", "angvel"):
+            assert np.array_equal(sa[k], sb[k]), k
+        ca, cb = a.get_contacts(), b.get_contacts()
+        assert np.array_equal(ca["key"], cb["key"]) and np.array_equal(ca["P"], cb["P"])
+    finally:
+        a.close()
+        b.close()
