@@ -131,8 +131,16 @@ def lib():
         L.or_color_contacts.restype = i32
         L.or_splitmix64.argtypes = [C.c_uint64]
         L.or_splitmix64.restype = C.c_uint64
+        L.or_set_binning.argtypes = [i32]
+        L.or_set_binning.restype = None
         _lib = L
     return _lib
+
+
+def set_binning(on: bool) -> None:
+    """SURVEY §8(c) binning mode: particle pairs from a uniform cell list (identical contact set
+    and order as the brute force, pinned in tests/test_oracle_pins.py); for big-bed timing."""
+    lib().or_set_binning(1 if on else 0)
 
 
 # ----------------------------------------------------------------------------- pure helpers

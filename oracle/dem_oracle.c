@@ -142,32 +142,113 @@ static int cmp_raw(const void *x, const void *y)
     return a < b ? -1 : (a > b ? 1 : 0);
 }
 
-/* All contacts of the current configuration, brute force, sorted by key. */
+/* Binning mode (SURVEY §8(c) "--binning": an independent CPU cell list, used for big-bed
+ * timing).  Off by default; when on, the particle pairs are enumerated from a uniform grid of
+ * cell 2 r_max instead of all N^2 pairs.  Every pair with d < r_a + r_b <= 2 r_max lies in
+ * neighbouring cells, and each candidate goes through the same test as the brute force, so the
+ * contact set, its values and (after the key sort) its order are identical; pinned against the
+ * brute force by tests/test_oracle_pins.py. */
+static int g_binning = 0;
+void or_set_binning(int32_t on) { g_binning = on != 0; }
+
+/* one particle pair (i, j): contact iff (dx^2+dy^2)+dz^2 < (r_a+r_b)^2 (reading R14) */
+static int pair_test(const or_world *w, int64_t i, int64_t j, raw_list *L, int64_t *n_degen)
+{
+    int64_t a = i, b = j;
+    if (w->gid[j] < w->gid[i]) { a = j; b = i; }
+    double dx = w->x[3 * b + 0] - w->x[3 * a + 0];
+    double dy = w->x[3 * b + 1] - w->x[3 * a + 1];
+    double dz = w->x[3 * b + 2] - w->x[3 * a + 2];
+    double d2 = (dx * dx + dy * dy) + dz * dz;
+    double R = w->r[a] + w->r[b];
+    if (!(d2 < R * R)) return 0;
+    if (d2 == 0.0) { (*n_degen)++; return 0; }   /* coincident centres: flag+skip */
+    double d = sqrt(d2);
+    raw_contact c;
+    c.key = ((uint64_t)w->gid[a] << 32) | (uint64_t)w->gid[b];
+    c.a = a; c.b = b; c.kind = 0; c.idx = -1;
+    c.n[0] = dx / d; c.n[1] = dy / d; c.n[2] = dz / d;
+    c.delta = R - d;
+    return push(L, &c);
+}
+
+/* particle pairs through the cell list; returns 1 if it cannot bin (non-finite input), so the
+ * caller falls back to the brute force */
+static int pairs_binned(const or_world *w, raw_list *L, int64_t *n_degen)
+{
+    const int64_t N = w->n;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY}, rmax = 0.0;
+    for (int64_t i = 0; i < N; i++) {
+        for (int k = 0; k < 3; k++) {
+            const double x = w->x[3 * i + k];
+            if (!isfinite(x)) return 1;
+            if (x < lo[k]) lo[k] = x;
+            if (x > hi[k]) hi[k] = x;
+        }
+        if (!isfinite(w->r[i])) return 1;
+        if (w->r[i] > rmax) rmax = w->r[i];
+    }
+    double cell = 2.0 * rmax;
+    int64_t n[3];
+    for (;;) {                          /* at most ~8 cells per particle */
+        int64_t tot = 1;
+        for (int k = 0; k < 3; k++) { n[k] = (int64_t)floor((hi[k] - lo[k]) / cell) + 1; tot *= n[k]; }
+        if (tot <= 8 * N + 64) break;
+        cell *= 2.0;
+    }
+    const int64_t nc = n[0] * n[1] * n[2];
+    int64_t *cnt = (int64_t *)calloc((size_t)nc + 1, sizeof(int64_t));
+    int64_t *cid = (int64_t *)malloc((size_t)(N ? N : 1) * sizeof(int64_t));
+    int64_t *lst = (int64_t *)malloc((size_t)(N ? N : 1) * sizeof(int64_t));
+    if (!cnt || !cid || !lst) { free(cnt); free(cid); free(lst); return -1; }
+    for (int64_t i = 0; i < N; i++) {
+        int64_t c[3];
+        for (int k = 0; k < 3; k++) {
+            c[k] = (int64_t)floor((w->x[3 * i + k] - lo[k]) / cell);
+            if (c[k] > n[k] - 1) c[k] = n[k] - 1;
+        }
+        cid[i] = c[0] + n[0] * (c[1] + n[1] * c[2]);
+        cnt[cid[i] + 1]++;
+    }
+    for (int64_t c = 0; c < nc; c++) cnt[c + 1] += cnt[c];          /* cell starts */
+    int64_t *fill = (int64_t *)malloc((size_t)nc * sizeof(int64_t));
+    if (!fill) { free(cnt); free(cid); free(lst); return -1; }
+    memcpy(fill, cnt, (size_t)nc * sizeof(int64_t));
+    for (int64_t i = 0; i < N; i++) lst[fill[cid[i]]++] = i;
+    free(fill);
+    int rc = 0;
+    for (int64_t i = 0; i < N && !rc; i++) {
+        const int64_t cx = cid[i] % n[0], cy = (cid[i] / n[0]) % n[1], cz = cid[i] / (n[0] * n[1]);
+        for (int64_t z = cz - 1; z <= cz + 1; z++)
+            for (int64_t y = cy - 1; y <= cy + 1; y++)
+                for (int64_t x = cx - 1; x <= cx + 1; x++) {
+                    if (x < 0 || y < 0 || z < 0 || x >= n[0] || y >= n[1] || z >= n[2]) continue;
+                    const int64_t c = x + n[0] * (y + n[1] * z);
+                    for (int64_t t = cnt[c]; t < cnt[c + 1] && !rc; t++)
+                        if (lst[t] > i) rc = pair_test(w, i, lst[t], L, n_degen);
+                }
+    }
+    free(cnt); free(cid); free(lst);
+    return rc;
+}
+
+/* All contacts of the current configuration, brute force (or binned), sorted by key. */
 static int detect_all(const or_world *w, raw_list *L, int64_t *n_degen)
 {
     const int64_t N = w->n;
     *n_degen = 0;
-    /* particle pairs: contact iff (dx^2+dy^2)+dz^2 < (r_a+r_b)^2 (reading R14) */
-    for (int64_t i = 0; i < N; i++) {
-        for (int64_t j = i + 1; j < N; j++) {
-            int64_t a = i, b = j;
-            if (w->gid[j] < w->gid[i]) { a = j; b = i; }
-            double dx = w->x[3 * b + 0] - w->x[3 * a + 0];
-            double dy = w->x[3 * b + 1] - w->x[3 * a + 1];
-            double dz = w->x[3 * b + 2] - w->x[3 * a + 2];
-            double d2 = (dx * dx + dy * dy) + dz * dz;
-            double R = w->r[a] + w->r[b];
-            if (!(d2 < R * R)) continue;
-            if (d2 == 0.0) { (*n_degen)++; continue; }   /* coincident centres: flag+skip */
-            double d = sqrt(d2);
-            raw_contact c;
-            c.key = ((uint64_t)w->gid[a] << 32) | (uint64_t)w->gid[b];
-            c.a = a; c.b = b; c.kind = 0; c.idx = -1;
-            c.n[0] = dx / d; c.n[1] = dy / d; c.n[2] = dz / d;
-            c.delta = R - d;
-            if (push(L, &c)) return -1;
-        }
+    int binned = 1;
+    if (g_binning) {
+        const int rc = pairs_binned(w, L, n_degen);
+        if (rc < 0) return -1;
+        if (rc == 1) { binned = 0; L->n = 0; *n_degen = 0; }
+    } else {
+        binned = 0;
     }
+    if (!binned)
+        for (int64_t i = 0; i < N; i++)
+            for (int64_t j = i + 1; j < N; j++)
+                if (pair_test(w, i, j, L, n_degen)) return -1;
     /* walls: s = (X-p).n_w < r -> n = -n_w, delta = r - s */
     for (int64_t i = 0; i < N; i++) {
         for (int32_t k = 0; k < w->n_walls; k++) {

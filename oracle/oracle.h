@@ -114,6 +114,10 @@ double or_contact_network_length(double d_min, double d_max, double r, double et
 int32_t or_solver_iterations(double n_d, double eps);
 double or_planned_timestep(double d, double eps, double rho, double sigma);
 
+/* SURVEY §8(c) binning mode: particle pairs from a uniform cell list instead of all N^2 pairs
+ * (identical contact set and order; off by default) */
+void or_set_binning(int32_t on);
+
 /* brute-force O(N^2) detection: contacts sorted by key; returns 0 or -1 (cap) */
 int32_t or_detect(const or_world *w, const or_params *p, or_contact *out, int64_t cap,
                   int64_t *n_out, int64_t *n_degenerate);

@@ -136,6 +136,48 @@ def test_pair_set_vs_distance_matrix(oracle_mod, seed, n):
     np.testing.assert_allclose(np.linalg.norm(c["n"], axis=1), 1.0, rtol=1e-14)
 
 
+@pytest.mark.parametrize("case", ["cloud8x", "jammed_bands", "coincident", "sparse"])
+def test_binning_mode_equals_brute_force(oracle_mod, case):
+    """SURVEY §8(c) binning mode: the cell-list pair enumeration returns the brute force's
+    contacts bit for bit (keys, normals, depths, degenerate count), and a whole step with it
+    (detection inside or_step) is bit-identical.  Pinned to the distance matrix through the
+    brute force (test_pair_set_vs_distance_matrix)."""
+    import synth
+    if case == "cloud8x":
+        b = synth.random_cloud(1500, (0, 0, 0), (0.1, 0.1, 0.1), 1e-3, 8e-3, 11, loguniform=True, v_scale=0.1)
+    elif case == "jammed_bands":
+        b = synth.banded_bed((0.03, 0.03, 0.03), [(0.0, 0.01, 1e-3), (0.01, 0.03, 2.5e-3)], 12, spacing=2.0)
+    elif case == "coincident":    # duplicated centres: degenerate pairs counted the same way
+        b = synth.random_cloud(300, (0, 0, 0), (0.03, 0.03, 0.03), 1e-3, 2e-3, 13)
+        b.x[1::7] = b.x[0:-1:7][: len(b.x[1::7])]
+    else:                         # sparse pairs in a 1 m cube: the cell-size cap (cells doubled)
+        rng = np.random.default_rng(14)
+        c = rng.uniform(0, 1, (150, 3))
+        x = np.concatenate([c, c + rng.uniform(-1.5e-3, 1.5e-3, (150, 3))])
+        b = synth.Bed(x=x, r=np.full(300, 1e-3), v=np.zeros((300, 3)), w=np.zeros((300, 3)),
+                      gid=rng.permutation(300).astype(np.uint32), box_lo=(0, 0, 0), box_hi=(1, 1, 1))
+    try:
+        oracle_mod.set_binning(False)
+        c0, d0 = _world(oracle_mod, b.x, b.r, gid=b.gid).detect()
+        oracle_mod.set_binning(True)
+        c1, d1 = _world(oracle_mod, b.x, b.r, gid=b.gid).detect()
+        assert d0 == d1 and len(c0) == len(c1) > 0
+        for k in ("key", "n", "delta"):
+            assert np.array_equal(c0[k], c1[k]), k
+        if case == "cloud8x":
+            p = oracle_mod.make_params(h=1e-4, n_it=20)
+            out = []
+            for on in (False, True):
+                oracle_mod.set_binning(on)
+                W = oracle_mod.OracleWorld(b.x, b.v, b.w, b.r, b.gid)
+                W.step(p, 2)
+                out.append((W.x.copy(), W.v.copy(), W.w.copy()))
+            for u, v in zip(out[0], out[1]):
+                assert np.array_equal(u, v)
+    finally:
+        oracle_mod.set_binning(False)
+
+
 def test_plate_box_closest_point_dense_sampling(oracle_mod):
     """Sphere vs grouser box edge/corner: delta and normal match a dense sampling of the box
     surface (S:309)."""
