@@ -18,3 +18,13 @@ def oracle_mod():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="module")
+def oracle_binning():
+    """The oracle's SURVEY §8(c) binning mode for the mini-curve runs (protocol, curves, triaxial):
+    cell-list pair enumeration, bit-identical to the brute force (tests/test_oracle_pins.py)."""
+    import oracle
+    oracle.set_binning(True)
+    yield
+    oracle.set_binning(False)

@@ -23,7 +23,7 @@ import oracle as O
 import synth
 from tests.parity import gpu_bed, oracle_params, oracle_world
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow, pytest.mark.usefixtures("oracle_binning")]
 HERE = os.path.dirname(os.path.abspath(__file__))
 TOL_RMS = 0.02
 

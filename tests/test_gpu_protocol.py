@@ -11,7 +11,7 @@ from paper_2501_05300_b200 import protocol as PR
 from tests.parity import gpu_bed, oracle_params, oracle_world
 from tests.test_gpu_curves import mini_bed
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow, pytest.mark.usefixtures("oracle_binning")]
 
 DT, N_IT = 2e-5, 40
 LO, HI = [(-0.01, -0.01, 0.0)], [(0.01, 0.01, 0.004)]
@@ -55,7 +55,7 @@ class OracleBed:
 
 
 @pytest.fixture(scope="module")
-def runs():
+def runs(oracle_binning):
     bed, hist = mini_bed()
     top = float((bed.x[:, 2] + bed.r).max())
     pos = (0.02, 0.02, top + 2e-4)

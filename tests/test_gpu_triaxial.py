@@ -16,7 +16,7 @@ import synth
 from paper_2501_05300_b200 import triaxial as TX
 from tests.parity import gpu_bed, oracle_params, oracle_world
 
-pytestmark = pytest.mark.gpu
+pytestmark = [pytest.mark.gpu, pytest.mark.usefixtures("oracle_binning")]
 
 
 def wall_sums(contacts, h):
