@@ -355,6 +355,7 @@ def main():
         "config": {"workload": wl, "n_particles": int(N_total), "generator": "on-device (dem_generator)", "n_contacts_mean": nc_mean, "nc_per_np": nc_mean / N,
                    "n_it": n_it, "dt": w["dt"], "impact_stage_rate": imp_rate, "rebuilds_per_step": rebuild_rate,
                    "levels": workload_levels(w),
+                   "device_memory_gb": torch.cuda.max_memory_allocated(local) / 1e9,
                    "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)"
                    if (world > 1 or args.decompose) else "single GPU",
                    "l2": l2_note,
