@@ -624,3 +624,30 @@ def test_add_particles_on_dense_bed_matches_recreate():
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.gpu
+def test_remove_all_then_add_matches_fresh_bed():
+    """Edge cases of the particle-set edits: removing every particle leaves a valid empty bed that
+    steps; particles added to it then evolve bit-identically to a fresh bed of the same particles."""
+    D = dem()
+    kw = dict(solver=dict(dt=2e-5, n_iter=25), box=dict(lo=(0, 0, 0), hi=(0.04, 0.04, 0.06)))
+    b0 = synth.random_cloud(300, (0.003, 0.003, 0.003), (0.037, 0.037, 0.03), 1.5e-3, 3e-3, 31, v_scale=0.05)
+    b1 = synth.random_cloud(200, (0.003, 0.003, 0.003), (0.037, 0.037, 0.03), 1.5e-3, 3e-3, 32, v_scale=0.05)
+    a = D.Bed(b0.x, b0.r, b0.v, b0.w, b0.gid, **kw)
+    f = D.Bed(b1.x, b1.r, b1.v, b1.w, b1.gid, **kw)
+    try:
+        a.step(5)
+        assert a.remove_particles(2, 1.0, 2.0) == 300    # every centre lies outside [1, 2]
+        assert a.get_state()["pos"].shape == (0, 3)
+        a.step(2)                                   # an empty bed steps
+        assert a.remove_particles(0, -1.0, 1.0) == 0     # nothing to remove from an empty bed
+        a.add_particles(b1.x, b1.r, b1.v, b1.w, gid=b1.gid)
+        a.step(8)
+        f.step(8)
+        sa, sf = a.get_state(), f.get_state()
+        for k in ("gid", "pos", "vel", "angvel"):
+            assert np.array_equal(sa[k], sf[k]), k
+    finally:
+        a.close()
+        f.close()
