@@ -320,23 +320,30 @@ __global__ void __launch_bounds__(TT, SWEEPT2_MINB)
                     if (PACKED) { const P8 q = ldP8(&P8_in[c]); pa = q.a; pb = q.b; }
                     else { pa = Pa_in[c]; pb = Pb_in[c]; }
                 }
-                double4 VP, WP;
+                // operands in the canonical (a, b) order.  Particle pairs: bodies a and b are
+                // loaded by index straight into their slots (shared memory inside the tile, else
+                // global), so no per-value selects between self and partner (measured: same
+                // time as the load-then-select form, bit-identical); boundary partners are body b.
+                double4 VA, WA, VB, WB;
                 double mt = sp.mu_t;
                 if (!(p & PARTNER_EXT)) {
-                    const int64_t pl = (int64_t)p - p0;
-                    if (pl >= 0 && pl < np) { VP = cat2(sVa[pl], sVb[pl]); WP = cat2(sWa[pl], sWb[pl]); }
-                    else { VP = ld4g(&vin[p]); WP = ld4g(&win[p]); }
+                    const int64_t ga = isB ? (int64_t)p : p0 + o, gb = isB ? p0 + o : (int64_t)p;
+                    const int64_t la = ga - p0, lb = gb - p0;
+                    if (la >= 0 && la < np) { VA = cat2(sVa[la], sVb[la]); WA = cat2(sWa[la], sWb[la]); }
+                    else { VA = ld4g(&vin[ga]); WA = ld4g(&win[ga]); }
+                    if (lb >= 0 && lb < np) { VB = cat2(sVa[lb], sVb[lb]); WB = cat2(sWa[lb], sWb[lb]); }
+                    else { VB = ld4g(&vin[gb]); WB = ld4g(&win[gb]); }
                 } else {
                     d3 bv;
                     double mr;
                     boundary_body(p, bnd, bv, mt, mr);
-                    VP = make_double4(bv.x, bv.y, bv.z, 0.0);
-                    WP = make_double4(0.0, 0.0, 0.0, 0.0);
+                    VA = cat2(sVa[o], sVb[o]);
+                    WA = cat2(sWa[o], sWb[o]);
+                    VB = make_double4(bv.x, bv.y, bv.z, 0.0);
+                    WB = make_double4(0.0, 0.0, 0.0, 0.0);
                 }
-                const double4 VS = cat2(sVa[o], sVb[o]), WS = cat2(sWa[o], sWb[o]);
-                const HalfOut r = EXP == 1 ? t2_fake(VS, WS, VP, WP, g, rw, pa, pb)
-                                           : half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB,
-                                                          mt, g, rw, pa, pb, sp.rolling_dims);
+                const HalfOut r = EXP == 1 ? t2_fake(VA, WA, VB, WB, g, rw, pa, pb)
+                                           : half_contact(VA, WA, VB, WB, isB, mt, g, rw, pa, pb, sp.rolling_dims);
                 if (!isB) {   // both halves compute the same impulses; body a stores them
                     if (PACKED) stP8(&P8_out[c], r.Pa, r.Pb);
                     else { Pa_out[c] = r.Pa; Pb_out[c] = r.Pb; }
