@@ -2,6 +2,7 @@
 #include <dlfcn.h>
 
 #include <cstring>
+#include <mutex>
 
 #include <nccl.h>
 
@@ -28,6 +29,8 @@ NcclApi &nccl(std::string &err)
 {
     static NcclApi api;
     static bool tried = false;
+    static std::mutex mu;                 // contexts may be created from several host threads
+    std::lock_guard<std::mutex> lock(mu);
     if (tried) {
         if (!api.ok) err = "libnccl.so.2 could not be loaded";
         return api;

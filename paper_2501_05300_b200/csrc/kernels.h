@@ -46,10 +46,10 @@ void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const do
                  cudaStream_t s);
 // packed incidence of the canonical reduction (sweep_t2.cu): entries in 32-lane chunks, start[i]
 // = packed position of particle i's list, wbase[g] = first packed entry of warp g's particles
-extern bool g_t2_rows_by_contact;
-extern bool g_t2_stage;
+extern thread_local bool g_t2_rows_by_contact;
+extern thread_local bool g_t2_stage;
 void to_planes(int64_t np, const double4 *in, double4 *out, cudaStream_t s);
-extern int g_t2_exp;
+extern thread_local int g_t2_exp;
 struct PackedInc {
     const uint2 *inc;
     const uint32_t *start;

@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(TPT, SWEEP_MINB_PPT) k_sweep_ppt(int64_t N, co
     wout[i] = Wn;
 }
 
-static int g_sweep_variant = SWEEP_KERNEL;
+static thread_local int g_sweep_variant = SWEEP_KERNEL;   // per host thread: contexts may step concurrently
 void set_sweep_variant(int v) { g_sweep_variant = v; }
 bool sweep_uses_order() { return g_sweep_variant == 2; }
 void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s)

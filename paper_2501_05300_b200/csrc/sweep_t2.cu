@@ -32,9 +32,9 @@ __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { retu
 // packing depends only on list lengths, the sums only on the lists (ordered by partner gid), so
 // every decomposition and warp grouping produces the same bits.
 constexpr uint32_t PK_HOLE = 0xFFFFFFFFu;
-bool g_t2_rows_by_contact = false;
-bool g_t2_stage = false;
-int g_t2_exp = 0;
+thread_local bool g_t2_rows_by_contact = false;   // diagnostic variant flags, per host thread
+thread_local bool g_t2_stage = false;
+thread_local int g_t2_exp = 0;
 
 // one warp per 32 consecutive particles (the sweep's warp grouping): first-fit packing
 __global__ void k_pack_plan(int64_t N, const uint32_t *__restrict__ inc_start, uint32_t *__restrict__ off_local,
