@@ -136,6 +136,41 @@ def test_pair_set_vs_distance_matrix(oracle_mod, seed, n):
     np.testing.assert_allclose(np.linalg.norm(c["n"], axis=1), 1.0, rtol=1e-14)
 
 
+def test_contacts_of_vs_distance_matrix(oracle_mod):
+    """or_contacts_of (the reference of the full-size sampled GPU checks): the contacts of a sample
+    of particles equal the distance-matrix pairs that involve a sampled particle, plus the walls
+    whose signed distance is below the radius; keys deduplicated (pairs of two sampled particles
+    once) and sorted, depths r_a + r_b - d."""
+    import synth
+    b = synth.random_cloud(800, (0, 0, 0), (0.06, 0.06, 0.06), 1e-3, 6e-3, 17, loguniform=True)
+    lo, hi = (0.0, 0.0, 0.0), (0.06, 0.06, 0.06)
+    W = oracle_mod.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=oracle_mod.box_walls(lo, hi))
+    sample = np.random.default_rng(5).choice(b.n, 60, replace=False)
+    got = W.contacts_of(sample)
+    D = cdist(b.x, b.x)
+    S = b.r[:, None] + b.r[None, :]
+    ii, jj = np.nonzero(np.triu(D < S, 1))
+    insample = np.zeros(b.n, bool)
+    insample[sample] = True
+    keep = insample[ii] | insample[jj]
+    ga, gb = np.minimum(b.gid[ii[keep]], b.gid[jj[keep]]), np.maximum(b.gid[ii[keep]], b.gid[jj[keep]])
+    want = list((ga.astype(np.uint64) << np.uint64(32)) | gb.astype(np.uint64))
+    for i in sample:                       # walls: key (gid, 2^32 - 16 + w), w = -x,+x,-y,+y,-z,+z
+        for ax in range(3):
+            for side in range(2):
+                s_ = b.x[i, ax] - lo[ax] if side == 0 else hi[ax] - b.x[i, ax]
+                if s_ < b.r[i]:
+                    want.append((np.uint64(b.gid[i]) << np.uint64(32)) | np.uint64(0xFFFFFFF0 + 2 * ax + side))
+    want = np.sort(np.array(want, dtype=np.uint64))
+    np.testing.assert_array_equal(got["key"], want)
+    assert len(got) > 60
+    pp = (got["key"] & np.uint64(0xFFFFFFFF)) < np.uint64(0xFFFFF000)
+    inv = np.argsort(b.gid)
+    a_i = inv[(got["key"][pp] >> np.uint64(32)).astype(np.int64)]
+    b_i = inv[(got["key"][pp] & np.uint64(0xFFFFFFFF)).astype(np.int64)]
+    np.testing.assert_allclose(got["delta"][pp], S[a_i, b_i] - D[a_i, b_i], rtol=1e-9, atol=1e-15)
+
+
 @pytest.mark.parametrize("case", ["cloud8x", "jammed_bands", "coincident", "sparse"])
 def test_binning_mode_equals_brute_force(oracle_mod, case):
     """SURVEY §8(c) binning mode: the cell-list pair enumeration returns the brute force's
