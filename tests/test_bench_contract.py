@@ -22,3 +22,24 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("config4-geom")
+
+
+def test_workload_iteration_counts():
+    """N_it of every bench workload from Eqs. 8 + 10: bands sum thickness / d; the
+    Eq. 1 profile integrates dz / d(z) (numerically here, against the closed form in bench.py);
+    config 4 and config 2 reproduce SURVEY §8(d)'s 226 and 186."""
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2501_05300_b200 import dem
+    w2 = bench.WORKLOADS["config2-geom"]
+    d_min, gamma, d_max = w2["profile"]
+    z = np.linspace(0.0, w2["dims"][2], 200001)
+    d = np.minimum(d_max, d_min + gamma * z)
+    f = 1.0 / d
+    num = float(np.sum(0.5 * (f[1:] + f[:-1]) * np.diff(z)))
+    assert abs(bench.workload_network_length(w2) - num) < 1e-6 * num
+    assert dem.plan_iterations(bench.workload_network_length(bench.WORKLOADS["config4-geom"]), 0.02) == 226
+    assert dem.plan_iterations(bench.workload_network_length(w2), 0.02) == 186
+    assert dem.plan_iterations(bench.workload_network_length(bench.WORKLOADS["config3-count"]), 0.02) == 375
+    assert bench.workload_levels(w2) == 3 and bench.workload_levels(bench.WORKLOADS["config4-geom"]) == 3
