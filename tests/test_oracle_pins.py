@@ -715,3 +715,121 @@ def test_monolithic_plate_coupling(oracle_mod):
         mom = 0.02 * np.array(W.plates[0].vel[:]) + mp * W.v[0]
         assert np.abs(mom - mom0).max() <= 1e-12 * 0.02 * 0.3
     assert hit and W.v[0, 0] < -0.05                                 # the sphere was struck
+
+
+# ---------------------------------------------------------------- outputs of the step (O6, O9, R19)
+
+def test_forces_torques_k_stack(oracle_mod):
+    """O6 per-particle outputs F = (1/h) sum +-(P_n n + P_t), T = (1/h) sum +-(l x P_t + P_r)
+    (Eq. 2: the contact forces are G^T lambda).  A settled column of k spheres is in
+    equilibrium: every sphere's net contact force balances its weight, F = +m g z (a sign error on
+    either body, a dropped 1/h or a missing floor contact fails), and no torque acts (the column
+    is symmetric: P_t = 0)."""
+    k, r, h = 4, 4.25e-3, 1e-4
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    x = np.array([[0, 0, r + 2 * r * i] for i in range(k)])
+    W = oracle_mod.OracleWorld(x, np.zeros((k, 3)), np.zeros((k, 3)), [r] * k, np.arange(k), walls=floor)
+    p = oracle_mod.make_params(h=h, n_it=200, E=1e9, nu=0.15, rho=2200.0)
+    for _ in range(400):
+        W.step(p)
+    _, F, T = W.step(p, want_forces=True)
+    m, _ = oracle_mod.mass_inertia(2 * r, 2200.0)
+    for i in range(k):
+        np.testing.assert_allclose(F[i], [0.0, 0.0, m * 9.81], rtol=0, atol=0.01 * m * 9.81)
+    assert np.all(T == 0.0)
+
+
+def test_forces_torques_static_incline(oracle_mod):
+    """A sphere held static on a plane under gravity tilted by theta with tan(theta) <= mu_r
+    (reading R7: rolling bound mu_r R* P_n, R* = r for a wall).  Equilibrium of the
+    free body: the contact force balances gravity, F = -m g; the contact torque vanishes, T = 0;
+    so the rolling-resistance moment balances the friction moment about the centre,
+    |P_r|/h = |l| m g sin(theta) with the lever arm |l| = r - delta/2 (reading R10, the midpoint of
+    the overlap lens).  A soft material makes delta/2r ~ 3 %, so a lever arm of r (or a flipped
+    torque sign, or a dropped rolling term) fails."""
+    mu_t, mu_r, r, h = 0.4, 0.1, 3e-3, 1e-4
+    E, nu = 1e5, 0.3
+    th = math.atan(0.08)
+    g = 9.81
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4, mu_t=mu_t, mu_r=mu_r)
+    m, _ = oracle_mod.mass_inertia(2 * r, RHO)
+    kn = (E / (2 * (1 - nu * nu))) * math.sqrt(2 * r) / 3
+    d0 = (m * g * math.cos(th) / kn) ** (2 / 3)
+    assert d0 / (2 * r) > 0.02
+    W = oracle_mod.OracleWorld([[0, 0, r - d0]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], walls=floor)
+    gv = np.array([g * math.sin(th), 0.0, -g * math.cos(th)])
+    p = oracle_mod.make_params(h=h, n_it=100, E=E, nu=nu, mu_t=mu_t, mu_r=mu_r, g=tuple(gv))
+    for _ in range(4000):
+        W.step(p)
+    c, F, T = W.step(p, want_forces=True)
+    assert abs(W.v[0]).max() < 1e-7 and abs(W.w[0]).max() < 1e-4
+    np.testing.assert_allclose(F[0], -m * gv, rtol=0, atol=1e-4 * m * g)
+    lever = r - c["delta"][0] / 2
+    M = lever * m * g * math.sin(th)
+    assert np.abs(T[0]).max() < 1e-4 * M
+    assert np.linalg.norm(c["P"][0, 4:7]) / h == pytest.approx(M, rel=2e-4)
+    assert abs(np.linalg.norm(c["P"][0, 4:7]) / h - r * m * g * math.sin(th)) > 0.01 * M   # not r
+
+
+def test_residual_report_closed_forms(oracle_mod):
+    """O9 report: max |min(P_n, u_n + Sigma P_n - b)| at the final velocities.
+    (a) One normal row is solved exactly by one Jacobi sweep (c = 1: the split diagonal is the
+    true one), so its residual is 0.  (b) Two spheres stacked on a floor, frictionless, one sweep
+    from P = 0: with mass splitting the lower sphere has c = 2, so D_1 = 2/m, D_2 = 3/m; writing
+    u_c - b_c = -(D_c + S_c) P_c and the velocity changes (P_1 - P_2)/m, P_2/m, both rows end at
+    u' + S P - b = -(P_1 + P_2)/m: the residual is (P_1 + P_2)/m (no mass splitting would give
+    max(P_1, P_2)/m)."""
+    r, h = 4.25e-3, 1e-4
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    p = oracle_mod.make_params(h=h, n_it=1, E=1e9, nu=0.15, rho=2200.0, mu_t=0.0, mu_r=0.0, g=(0, 0, 0),
+                               v_imp=1e30)
+    m, _ = oracle_mod.mass_inertia(2 * r, 2200.0)
+    # (a) one sphere pressed 1 um into the floor, approaching at 1 mm/s
+    W = oracle_mod.OracleWorld([[0, 0, r - 1e-6]], [[0, 0, -1e-3]], np.zeros((1, 3)), [r], [0], walls=floor)
+    c, _, _ = W.step(p)
+    assert len(c) == 1 and c["P"][0, 0] > 0
+    assert W.last_report.max_normal_residual <= 1e-12 * (1e-3 + c["P"][0, 0] / m)
+    # (b) two-sphere stack, both contacts compressed
+    x = np.array([[0, 0, r - 1e-6], [0, 0, 3 * r - 3e-6]])
+    W = oracle_mod.OracleWorld(x, np.zeros((2, 3)), np.zeros((2, 3)), [r, r], [0, 1], walls=floor)
+    c, _, _ = W.step(p)
+    assert len(c) == 2 and np.all(c["P"][:, 0] > 0)
+    P1, P2 = c["P"][:, 0]
+    res = W.last_report.max_normal_residual
+    assert res == pytest.approx((P1 + P2) / m, rel=1e-9)
+    assert abs(res - max(P1, P2) / m) > 0.1 * res
+
+
+def test_centre_inside_plate_box_dense_directions(oracle_mod):
+    """Reading R19 (PAPER silent): a sphere whose centre lies inside a grouser box is pushed out
+    along the shortest way.  Brute force: over a dense set of directions d, the smallest
+    translation t(d) after which the sphere no longer touches the box (distance from the box
+    >= r, found by bisection) is the overlap delta, and the minimising d is -n (n points from the
+    particle into the box)."""
+    lo, hi = np.array([0.0, 0.0, 0.0]), np.array([0.0255, 0.05, 0.043])
+    P = oracle_mod.make_plate([lo], [hi], pos=(0, 0, 0), mass=1.0)
+    r = 3e-3
+    ng = 40000
+    i = np.arange(ng) + 0.5
+    phi = np.arccos(1 - 2 * i / ng)
+    th = np.pi * (1 + 5 ** 0.5) * i
+    D = np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], 1)
+
+    def box_dist(Y):
+        q = np.clip(Y, lo, hi)
+        return np.linalg.norm(Y - q, axis=-1)
+
+    for X in [np.array([0.004, 0.03, 0.02]), np.array([0.02, 0.0475, 0.01]), np.array([0.012, 0.02, 0.0415])]:
+        c, _ = _world(oracle_mod, [X], [r], plates=[P]).detect()
+        assert len(c) == 1
+        a, b = np.zeros(ng), np.full(ng, 0.2)
+        for _ in range(60):
+            mid = 0.5 * (a + b)
+            out = box_dist(X + mid[:, None] * D) >= r
+            b = np.where(out, mid, b)
+            a = np.where(out, a, mid)
+        k = np.argmin(b)
+        assert c["delta"][0] == pytest.approx(b[k], rel=1e-3)
+        np.testing.assert_allclose(c["n"][0], -D[k], atol=0.02)
+        depth = min((X - lo).min(), (hi - X).min())
+        assert c["delta"][0] > r + 0.9 * depth
