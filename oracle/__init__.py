@@ -31,7 +31,7 @@ def build(force: bool = False) -> str:
         os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "oracle.h"))
     ):
         subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+            ["gcc", "-O2", "-std=c11", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
              "-o", LIB, SRC, "-lm"]
         )
     return LIB
@@ -133,6 +133,8 @@ def lib():
         L.or_splitmix64.restype = C.c_uint64
         L.or_set_binning.argtypes = [i32]
         L.or_set_binning.restype = None
+        L.or_set_threads.argtypes = [i32]
+        L.or_set_threads.restype = i32
         _lib = L
     return _lib
 
@@ -141,6 +143,12 @@ def set_binning(on: bool) -> None:
     """SURVEY §8(c) binning mode: particle pairs from a uniform cell list (identical contact set
     and order as the brute force, pinned in tests/test_oracle_pins.py); for big-bed timing."""
     lib().or_set_binning(1 if on else 0)
+
+
+def set_threads(n: int) -> int:
+    """OpenMP threads of the oracle's sweeps (n <= 0: query); returns the count in effect.  The
+    results are bit-identical for any count (pinned in tests/test_oracle_pins.py)."""
+    return int(lib().or_set_threads(int(n)))
 
 
 # ----------------------------------------------------------------------------- pure helpers

@@ -151,6 +151,22 @@ static int cmp_raw(const void *x, const void *y)
 static int g_binning = 0;
 void or_set_binning(int32_t on) { g_binning = on != 0; }
 
+/* OpenMP threads of the sweeps (Jacobi is order-free).  Results do not depend on
+ * the count: each contact is solved alone, each body sums its increments in contact order. */
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+int32_t or_set_threads(int32_t n)
+{
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+    return omp_get_max_threads();
+#else
+    (void)n;
+    return 1;
+#endif
+}
+
 /* one particle pair (i, j): contact iff (dx^2+dy^2)+dz^2 < (r_a+r_b)^2 (reading R14) */
 static int pair_test(const or_world *w, int64_t i, int64_t j, raw_list *L, int64_t *n_degen)
 {
@@ -392,6 +408,7 @@ typedef struct {
     double S, bias;     /* SPOOK row: Sigma-hat and b (P-units) */
     double P[7];
     double dP[7];
+    double inc[9];      /* this sweep's increments: dL = dPn n + dPt, l_a x dPt + dPr, l_b x dPt + dPr */
     double un_minus;    /* n.(v_b - v_a) at the start of the step */
     int impacting;
 } row;
@@ -425,12 +442,12 @@ static void body_b_vel(const or_world *w, const row *R, const double *v, const d
  */
 static void sweep(const or_world *w, const or_params *p, row *R, int64_t nc,
                   const int32_t *cnt, const double *minv, const double *Iinv,
-                  double *v, double *om, double *accL, double *accA, double *accP)
+                  double *v, double *om, const int64_t *inc_s, const int64_t *inc_l, double *accP)
 {
     if (accP) memset(accP, 0, sizeof(double) * 3 * (size_t)w->n_plates);
     const int64_t N = w->n;
-    memset(accL, 0, sizeof(double) * 3 * (size_t)N);
-    memset(accA, 0, sizeof(double) * 3 * (size_t)N);
+    /* every contact from the sweep-start velocities (order-free: OpenMP over contacts) */
+#pragma omp parallel for schedule(static)
     for (int64_t c = 0; c < nc; c++) {
         row *r = &R[c];
         const int64_t a = r->g.a;
@@ -491,30 +508,33 @@ static void sweep(const or_world *w, const or_params *p, row *R, int64_t nc,
         double dPr[3];
         for (int k = 0; k < 3; k++) dPr[k] = Pr[k] - r->P[4 + k];
 
-        /* 4. contributions: a gets -(dPn n + dPt), -(l_a x dPt + dPr); b the opposite sign
-         *    with its own lever arm */
+        /* 4. increments: a gets -(dPn n + dPt), -(l_a x dPt + dPr); b the opposite sign with
+         *    its own lever arm (summed per body below) */
         for (int k = 0; k < 3; k++) {
-            accL[3 * a + k] -= dPn * n[k] + dPt[k];
-            accA[3 * a + k] -= ta[k] + dPr[k];
-        }
-        if (r->g.kind == 0) {
-            const int64_t b = r->g.b;
-            for (int k = 0; k < 3; k++) {
-                accL[3 * b + k] += dPn * n[k] + dPt[k];
-                accA[3 * b + k] += tb[k] + dPr[k];
-            }
-        } else if (r->g.kind == 2 && accP) {
-            /* monolithic plate (R18b): the plate receives +(dPn n + dPt) */
-            for (int k = 0; k < 3; k++) accP[3 * r->g.idx + k] += dPn * n[k] + dPt[k];
+            r->inc[k] = dPn * n[k] + dPt[k];
+            r->inc[3 + k] = ta[k] + dPr[k];
+            r->inc[6 + k] = tb[k] + dPr[k];
         }
         r->P[0] = Pn;
         for (int k = 0; k < 3; k++) { r->P[1 + k] = Pt[k]; r->P[4 + k] = Pr[k]; }
     }
-    /* 5. body update with the real masses (= mass-splitting average) */
+    /* monolithic plate (R18b): the plate receives +(dPn n + dPt) */
+    if (accP)
+        for (int64_t c = 0; c < nc; c++)
+            if (R[c].g.kind == 2) for (int k = 0; k < 3; k++) accP[3 * R[c].g.idx + k] += R[c].inc[k];
+    /* 5. body update with the real masses (= mass-splitting average): per body, its contacts'
+     *    increments in contact order (inc_s/inc_l lists them by increasing contact index) */
+#pragma omp parallel for schedule(static)
     for (int64_t i = 0; i < N; i++) {
+        double aL[3] = {0.0, 0.0, 0.0}, aA[3] = {0.0, 0.0, 0.0};
+        for (int64_t t = inc_s[i]; t < inc_s[i + 1]; t++) {
+            const row *r = &R[inc_l[t] >> 1];
+            if (inc_l[t] & 1) for (int k = 0; k < 3; k++) { aL[k] += r->inc[k]; aA[k] += r->inc[6 + k]; }
+            else for (int k = 0; k < 3; k++) { aL[k] -= r->inc[k]; aA[k] -= r->inc[3 + k]; }
+        }
         for (int k = 0; k < 3; k++) {
-            v[3 * i + k] += minv[i] * accL[3 * i + k];
-            om[3 * i + k] += Iinv[i] * accA[3 * i + k];
+            v[3 * i + k] += minv[i] * aL[k];
+            om[3 * i + k] += Iinv[i] * aA[k];
         }
     }
 }
@@ -728,8 +748,8 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
     double *minv = (double *)malloc(sizeof(double) * (size_t)(N ? N : 1));
     double *Iinv = (double *)malloc(sizeof(double) * (size_t)(N ? N : 1));
     int32_t *cnt = (int32_t *)calloc((size_t)(N ? N : 1), sizeof(int32_t));
-    double *accL = (double *)malloc(sizeof(double) * 3 * (size_t)(N ? N : 1));
-    double *accA = (double *)malloc(sizeof(double) * 3 * (size_t)(N ? N : 1));
+    int64_t *inc_s = (int64_t *)calloc((size_t)N + 2, sizeof(int64_t));
+    int64_t *inc_l = (int64_t *)malloc(sizeof(int64_t) * (2 * (size_t)nc + 1));
     row *R = (row *)calloc((size_t)(nc ? nc : 1), sizeof(row));
     or_contact *H = NULL;
     for (int64_t i = 0; i < N; i++) {
@@ -767,12 +787,24 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
     }
     rep->n_contacts = nc;
     rep->n_degenerate = n_degen;
+    /* per body, its contacts in increasing contact index (entry = c << 1 | is-body-b): the order
+     * in which the sweep adds a body's increments */
+    for (int64_t i = 0; i < N; i++) inc_s[i + 1] = inc_s[i] + cnt[i];
+    {
+        int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N ? N : 1));
+        for (int64_t i = 0; i < N; i++) fill[i] = inc_s[i];
+        for (int64_t c = 0; c < nc; c++) {
+            inc_l[fill[R[c].g.a]++] = c << 1;
+            if (R[c].g.kind == 0) inc_l[fill[R[c].g.b]++] = (c << 1) | 1;
+        }
+        free(fill);
+    }
     const int gs = p->ordering == 1;
     int64_t *order = NULL;
     if (gs) {
         order = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nc ? nc : 1));
         if (gs_order(R, nc, N, order) < 0) {                    /* more than 256 colours */
-            free(L.v); free(minv); free(Iinv); free(cnt); free(accL); free(accA); free(R); free(order);
+            free(L.v); free(minv); free(Iinv); free(cnt); free(inc_s); free(inc_l); free(R); free(order);
             return -3;
         }
     }
@@ -803,7 +835,7 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
         double *accPi = mono_i ? (double *)calloc(3 * (size_t)w->n_plates, sizeof(double)) : NULL;
         for (int32_t s = 0; s < n_imp; s++) {
             if (gs) sweep_gs(w, p, R, nc, order, minv, Iinv, w->v, w->w);
-            else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA, accPi);
+            else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, inc_s, inc_l, accPi);
             if (mono_i)
                 for (int32_t q = 0; q < w->n_plates; q++) {
                     or_plate *P = &w->plates[q];
@@ -873,7 +905,7 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
     /* 7. N_it sweeps: Jacobi, or coloured Gauss-Seidel */
     for (int32_t s = 0; s < p->n_it; s++) {
         if (gs) sweep_gs(w, p, R, nc, order, minv, Iinv, w->v, w->w);
-        else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, accL, accA, accP);
+        else sweep(w, p, R, nc, cnt, minv, Iinv, w->v, w->w, inc_s, inc_l, accP);
         if (mono)
             for (int32_t q = 0; q < w->n_plates; q++) {
                 or_plate *P = &w->plates[q];
@@ -977,6 +1009,6 @@ int32_t or_step(or_world *w, const or_params *p, const or_contact *hist, int64_t
         for (int k = 0; k < 7; k++) if (!isfinite(R[c].P[k])) bad = 1;
     }
     if (bad) rc = -2;
-    free(L.v); free(minv); free(Iinv); free(cnt); free(accL); free(accA); free(R); free(H); free(order);
+    free(L.v); free(minv); free(Iinv); free(cnt); free(inc_s); free(inc_l); free(R); free(H); free(order);
     return rc;
 }

@@ -833,3 +833,25 @@ def test_centre_inside_plate_box_dense_directions(oracle_mod):
         np.testing.assert_allclose(c["n"][0], -D[k], atol=0.02)
         depth = min((X - lo).min(), (hi - X).min())
         assert c["delta"][0] > r + 0.9 * depth
+
+
+def test_openmp_sweeps_bit_identical(oracle_mod):
+    """SURVEY §8(c): OpenMP over contacts and particles is allowed because Jacobi is order-free;
+    the oracle solves each contact alone and sums each body's increments in contact order, so
+    any thread count gives the same bits (5 steps of an 8x polydisperse cloud with walls)."""
+    import synth
+    b = synth.random_cloud(1500, (0, 0, 0), (0.06, 0.06, 0.06), 1e-3, 5e-3, 3, v_scale=0.05, w_scale=2.0,
+                           loguniform=True)
+    out = []
+    n0 = oracle_mod.set_threads(0)
+    try:
+        for nt in (1, 4):
+            oracle_mod.set_threads(nt)
+            W = oracle_mod.OracleWorld(b.x, b.v, b.w, b.r, b.gid,
+                                       walls=oracle_mod.box_walls(b.box_lo, b.box_hi, mu_t=0.2, mu_r=0.05))
+            c, F, T = W.step(oracle_mod.make_params(h=1e-5, n_it=40), 5, want_forces=True)
+            out.append((W.x.copy(), W.v.copy(), W.w.copy(), c["P"].copy(), F, T))
+    finally:
+        oracle_mod.set_threads(n0)
+    for u, v in zip(*out):
+        assert np.array_equal(u, v)
