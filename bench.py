@@ -42,7 +42,10 @@ import synth  # noqa: E402
 # SURVEY §8(d); bands = (depth_top, depth_bottom, r_nom)
 WORKLOADS = {
     "config4-geom": dict(dims=(8.0, 1.0, 0.6), bands=[(0.0, 0.08, 2e-3), (0.08, 0.25, 6e-3), (0.25, 0.6, 16e-3)],
-                         dt=5e-6, seed=1004),
+                         dt=5e-6, seed=1004, plates=8),
+    # configs[4]'s stated count (~40 M) on one GPU: the same bands, lengthened along x (reading R27)
+    "config4-count": dict(dims=(21.9, 1.0, 0.6), bands=[(0.0, 0.08, 2e-3), (0.08, 0.25, 6e-3), (0.25, 0.6, 16e-3)],
+                          dt=5e-6, seed=1004, plates=8),
     "config1": dict(dims=(0.4, 0.4, 0.3), bands=[(0.0, 0.06, 2e-3), (0.06, 0.3, 4e-3)], dt=5e-6, seed=1001),
     "config3-geom": dict(dims=(1.0, 0.5, 0.3), bands=[(0.0, 0.3, 2e-3)], dt=5e-6, seed=1003),
     "config3-count": dict(dims=(4.3, 0.5, 0.3), bands=[(0.0, 0.3, 2e-3)], dt=5e-6, seed=1003),
@@ -158,28 +161,40 @@ class ClockSampler:
                 "samples": len(rows), "power_w": float(np.median(pw)) if pw else None}
 
 
-def cpu_baseline(wl, n_it, dt, budget_s=15.0):
-    """The fp64 oracle as it stands, single thread, on a bounded sample of the workload: a
-    full-depth column of the bed (all bands), stepped once with the workload's N_it."""
+def cpu_baseline(wl, n_it, dt, budget_s=12.0):
+    """The fp64 oracle as it stands (OpenMP over contacts and bodies, bit-identical to its serial
+    sweep) on a bounded sample of the workload: a full-depth column of the bed (all bands), stepped
+    with the workload's N_it, on all host cores and on one core."""
     import oracle as O
     w = WORKLOADS[wl]
     dims = w["dims"]
     col = (0.06, 0.06, dims[2])
     b = make_bed(wl, seed_offset=77, dims=col)
     O.set_binning(True)                 # SURVEY §8(c): the oracle's cell-list mode for timing
-    Wd = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi))
-    p = O.make_params(h=dt, n_it=n_it)
-    t0 = time.perf_counter()
-    steps = 0
-    while True:
-        c, _, _ = Wd.step(p)
-        steps += 1
-        if time.perf_counter() - t0 > budget_s or steps >= 3:
-            break
-    dt_s = time.perf_counter() - t0
-    return {"value": b.n * steps / dt_s, "unit": "particle-steps/s", "cores": 1, "kind": "oracle",
+    nproc = os.cpu_count() or 1
+    legs = {}
+    n0 = O.set_threads(0)
+    try:
+        for cores in (nproc, 1):
+            O.set_threads(cores)
+            Wd = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi))
+            p = O.make_params(h=dt, n_it=n_it)
+            t0 = time.perf_counter()
+            steps = 0
+            while True:
+                c, _, _ = Wd.step(p)
+                steps += 1
+                if time.perf_counter() - t0 > budget_s / 2 or steps >= 3:
+                    break
+            legs[cores] = (b.n * steps / (time.perf_counter() - t0), steps, len(c))
+    finally:
+        O.set_threads(n0)
+    v, steps, nc = legs[nproc]
+    return {"value": v, "unit": "particle-steps/s", "cores": nproc, "nproc": nproc, "kind": "oracle",
+            "value_1core": legs[1][0],
             "sample": f"{b.n}-particle full-depth column (0.06 x 0.06 x {dims[2]} m, all bands) of {wl}, "
-                      f"{steps} step(s), N_it={n_it}, cell-list (binning) detection, {len(c)} contacts"}
+                      f"{steps} step(s), N_it={n_it}, cell-list (binning) detection, {nc} contacts; OpenMP on "
+                      f"{nproc} cores (value) and 1 core (value_1core)"}
 
 
 def run_reference(args, rank, world):
@@ -192,6 +207,8 @@ def run_reference(args, rank, world):
     dims = w["dims"]
     b = make_bed(wl, seed_offset=99, dims=(0.05, 0.05, dims[2]))
     O.set_binning(True)                 # the oracle's cell-list mode for timing
+    nproc = os.cpu_count() or 1
+    O.set_threads(nproc)                # the oracle's OpenMP sweeps on every host core
     Wd = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi))
     p = O.make_params(h=w["dt"], n_it=n_it)
     for _ in range(args.warmup):
@@ -202,15 +219,53 @@ def run_reference(args, rank, world):
     T = time.perf_counter() - t0
     val = b.n * args.steps / T
     sample = (f"{b.n}-particle full-depth column (0.05 x 0.05 x {dims[2]} m) of {wl}; each step is one full "
-              f"oracle step (cell-list detection, N_it={n_it} Jacobi sweeps)")
+              f"oracle step (cell-list detection, N_it={n_it} Jacobi sweeps), OpenMP on {nproc} cores")
     print(json.dumps({
         "impl": "reference", "metric": "particle-steps/s", "value": val, "unit": "particle-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl + " (oracle sample)", "n_particles": b.n, "n_it": n_it, "dt": w["dt"]},
-        "cpu_baseline": {"value": val, "unit": "particle-steps/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": "particle-steps/s", "cores": nproc, "nproc": nproc, "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": val, "unit": "particle-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
+
+
+def torchrun_argv(gpus, argv, port):
+    """argv that re-executes this bench under torchrun with one rank per GPU (the contract's own
+    launch line), or None when no relaunch is needed (gpus == 1 or already under torchrun)."""
+    if gpus <= 1:
+        return None
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + list(argv)
+
+
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+# SURVEY C20/C21: the paper's grouser plate, 0.3 m long (x) across the bed width, 4 teeth 43 mm
+# deep x 25.5 mm long at a 75 mm pitch, a 10 mm base; steel density for its mass
+def c21_plate_boxes(width):
+    hy = 0.5 * width - 0.01
+    lo, hi = [(-0.15, -hy, 0.0)], [(0.15, hy, 0.01)]
+    for k in range(4):
+        xc = -0.1125 + 0.075 * k
+        lo.append((xc - 0.01275, -hy, -0.043))
+        hi.append((xc + 0.01275, hy, 0.0))
+    vol = sum((b[0] - a[0]) * (b[1] - a[1]) * (b[2] - a[2]) for a, b in zip(lo, hi))
+    return lo, hi, 7850.0 * vol
+
+
+def add_plates(bed, n_plates, L_total, width, z_top):
+    """n_plates C21 plates evenly along the whole bed, grouser tips 0.1 mm above the bed top
+    (every rank adds all of them: plates are global bodies)."""
+    lo, hi, mass = c21_plate_boxes(width)
+    return [bed.add_plate(lo, hi, ((i + 0.5) * L_total / n_plates, 0.5 * width, z_top + 0.043 + 1e-4), mass)
+            for i in range(n_plates)]
 
 
 def main():
@@ -228,17 +283,23 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e, no baseline, no clocks")
-    ap.add_argument("--reduction", default="canonical", choices=["canonical", "contiguous"],
-                    help="per-particle sum of the Jacobi sweep: canonical (default; bit-identical for any number of "
-                         "GPUs) or contiguous (slightly faster; rounding depends on the decomposition)")
     ap.add_argument("--ordering", default="jacobi", choices=["jacobi", "gs"],
                     help="contact-solve ordering: Jacobi with mass splitting (default) or coloured Gauss-Seidel")
     ap.add_argument("--decompose", action="store_true",
                     help="run the x-slab decomposition (NCCL transport) even at N = 1 (code-path check)")
+    ap.add_argument("--plates", default="c21", choices=["c21", "none"],
+                    help="c21 (default for config 4): 8 grouser plates pressed (-z) and sheared (+x) at 0.05 m/s in "
+                         "the timed window; none: the bed alone")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ:
+        relaunch = torchrun_argv(args.gpus, sys.argv[1:], free_port())
+        if relaunch:                      # --gpus N without torchrun: one rank per GPU, as the contract launches
+            os.execvp(relaunch[0], relaunch)
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -270,8 +331,27 @@ def main():
     N_total = dem.generator_count(gen, box)
     if args.settle > 0:
         bed.step(args.settle)             # coarse relaxation of the jammed packing (not timed)
-    bed.set_solver(dt=w["dt"], n_iter=n_it, ordering=1 if args.ordering == "gs" else 0,
-                   reduction=0 if args.reduction == "canonical" else 1)
+    n_plates = w.get("plates", 0) if args.plates == "c21" else 0
+    pids = []
+    if n_plates:
+        # plates start 0.1 mm above the bed; an untimed press at the coarse step brings
+        # the grousers ~1.4 mm into the surface, then the window presses (-z) and shears (+x) at 0.05 m/s
+        st = bed.get_state()
+        z_top = float(np.max(st["pos"][:, 2] + st["radius"])) if len(st["radius"]) else w["dims"][2]
+        if dist:
+            import torch.distributed as tdist
+            zt = torch.tensor([z_top], dtype=torch.float64, device="cuda")
+            tdist.all_reduce(zt, op=tdist.ReduceOp.MAX)
+            z_top = float(zt.item())
+        del st
+        pids = add_plates(bed, n_plates, L_total, w["dims"][1], z_top)
+        for p in pids:
+            bed.drive_plate(p, 2, 1, -0.5)
+        bed.step(30)
+        for p in pids:
+            bed.drive_plate(p, 2, 1, -0.05)
+            bed.drive_plate(p, 0, 1, 0.05)
+    bed.set_solver(dt=w["dt"], n_iter=n_it, ordering=1 if args.ordering == "gs" else 0)
     wrep = None
     for _ in range(args.warmup):
         wrep = bed.step(1)
@@ -330,6 +410,9 @@ def main():
     imp_rate = float(np.mean([r["impact_fired"] for r in reps]))
     rebuild_rate = float(np.mean([r["rebuilt"] for r in reps]))
     value = world * N * args.steps / (ms / 1e3)
+    n_imp_sweeps = imp_rate * n_it                 # impact-stage sweeps per step (N_imp = N_it)
+    ms_main = ms / args.steps - n_imp_sweeps * (tm["ms_sweeps"] / max(tm["n_sweep_launches"], 1))
+    value_main = world * N / (ms_main / 1e3) if ms_main > 0 else None
     # reports are global with the decomposition (each contact counted once over the ranks)
     contacts_per_s = (nc_mean if world > 1 else world * nc_mean) * args.steps / (ms / 1e3)
     nc_rank = nc_mean / world if world > 1 else nc_mean
@@ -359,12 +442,19 @@ def main():
                    "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)"
                    if (world > 1 or args.decompose) else "single GPU",
                    "l2": l2_note,
-                   "precision": "fp64 state and row math; fp64 normals/rows, fp32 impulses",
+                   "precision": "fp64 state and row math; fp64 normal/overlap/bias records, fp32 impulses",
                    "ordering": "coloured Gauss-Seidel" if args.ordering == "gs" else "Jacobi (mass splitting)",
-                   "reduction": args.reduction},
+                   "reduction": "exact int64 fixed point per particle (order-free: bit-identical for any decomposition)",
+                   "plates": n_plates, "plate_contacts_per_step": {"min": min(r["n_plate"] for r in reps),
+                                                                   "mean": float(np.mean([r["n_plate"] for r in reps]))},
+                   "plate_motion": "kinematic -z 0.05 m/s and +x 0.05 m/s (SURVEY C21: pressed and sheared)"
+                   if n_plates else None},
+        "value_main_stage_only": value_main,
+        "main_stage_only_note": "particle-steps/s with the impact-stage sweeps' time removed (a settled bed fires it "
+                                "rarely); the timed steps themselves all include it when it fires",
         "contacts_per_s": contacts_per_s,
         "contact_sweeps_per_s": tm["contact_sweeps"] / (ms / 1e3) * world,   # rank-local contacts (incl. ghost copies)
-        "roofline": {"bound": "hbm", "kernel": "k_gs_color (all colours of a sweep)" if args.ordering == "gs" else "k_sweep_t2", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "roofline": {"bound": "hbm", "kernel": "k_gs_color (all colours of a sweep)" if args.ordering == "gs" else "k_sweep", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
                      "traffic_unit": "GB per launch (ncu dram read+write)",
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": sweep_ms,
@@ -377,33 +467,35 @@ def main():
     }
     if ck:
         out["clocks"] = ck
-    # e2e through the public API: per step H2D the drive inputs (wall velocities) and D2H the
-    # whole particle state (a trajectory frame) into pinned host memory.
+    # e2e through the public API (the C-ABI with HOST buffers): per step the drive inputs go H2D
+    # (dem_drive_wall / dem_drive_plate upload the boundary state) and dem_get_state copies the
+    # whole particle state (a trajectory frame) into pinned host memory
     if not args.no_e2e and not args.profile:
         cap = int(1.2 * N) + 1024        # owned count drifts by migration across the slab faces
         pin = {k: torch.empty((cap, 3), dtype=torch.float64, pin_memory=True) for k in ("pos", "vel", "angvel")}
-        dev = {k: torch.empty((cap, 3), dtype=torch.float64, device="cuda") for k in ("pos", "vel", "angvel")}
+        n_drive = 4 + 2 * len(pids)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
+        n_own = 0
         for _ in range(args.steps):
             for wall in (0, 1, 2, 3):
                 bed.drive_wall(wall, 0.0)            # H2D: boundary drive inputs
+            for p in pids:
+                bed.drive_plate(p, 2, 1, -0.05)
+                bed.drive_plate(p, 0, 1, 0.05)
             bed.step(1)
-            n_own = bed.get_state_device(dev)
-            with torch.cuda.stream(stream):
-                for k in pin:
-                    pin[k][:n_own].copy_(dev[k][:n_own], non_blocking=True)
-            stream.synchronize()
+            n_own = bed.get_state_into(pin)           # D2H through dem_get_state into pinned host buffers
         T = time.perf_counter() - t0
         if dist:
             t = torch.tensor([T], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             T = float(t.item())
         out["e2e"] = {"value": world * N * args.steps / T, "unit": "particle-steps/s",
-                      "h2d_bytes_per_step": 4 * 5336, "d2h_bytes_per_step": int(72 * N),
-                      "what": "per step: wall-drive inputs H2D, full particle state (pos, vel, angvel) D2H to pinned host"}
+                      "h2d_bytes_per_step": n_drive * dem.boundary_upload_bytes(), "d2h_bytes_per_step": int(72 * n_own),
+                      "what": "per step: wall and plate drive inputs H2D, the full owned particle state (pos, vel, "
+                              "angvel; fp64) D2H by dem_get_state into pinned host buffers"}
     if rank == 0 and not args.no_cpu_baseline and not args.profile:
         out["cpu_baseline"] = cpu_baseline(wl, n_it, w["dt"])
     if rank == 0:

@@ -74,12 +74,11 @@ typedef struct {
                                   contacts coloured greedily in SplitMix64(key) priority, swept colour
                                   by colour with the real masses (single undecomposed context only) */
     double skin;               /* Verlet skin [m] of the candidate list; <= 0 -> 0.1 r_min */
-    int32_t reduction;         /* per-particle sum of the Jacobi sweep: 0 (default) canonical -- each
-                                  particle's contributions, ordered by partner gid, summed by a tree
-                                  that depends only on its own list, so trajectories are bit-identical
-                                  for any number of GPUs/slabs; 1 contiguous -- ~4 %
-                                  faster sweep (no packing holes), bit-reproducible run to run, but the
-                                  rounding of the sums depends on the decomposition */
+    int32_t reduction;         /* kept for the ABI; 0 and 1 are identical.  The Jacobi sweep sums each
+                                  particle's contact increments exactly (int64 fixed point at a scale
+                                  chosen from the particle's own weights, sweep.cu), so trajectories
+                                  are bit-identical for any number of GPUs/slabs and
+                                  run to run; values other than 0/1 -> DEM_ERR_INVALID */
     int32_t plate_coupling;    /* force-driven plate axes: 0 staggered after the solve (reading R18,
                                   default); 1 monolithic -- the axis is a body of the impact and
                                   main-stage solves (reading R18b): V += (h F + sum of
@@ -332,16 +331,17 @@ dem_status dem_set_timing(dem_ctx *ctx, int32_t enable);
 dem_status dem_get_timing(dem_ctx *ctx, dem_timing *out);
 dem_status dem_reset_timing(dem_ctx *ctx);
 
-/* Diagnostic (not on the stepping path): time n >= 1 Jacobi sweeps of sweep-kernel `variant`
- * (0 shipped k_sweep_t2 with the context's reduction, 7 contiguous k_sweep_t2, 8 packed with
- * contact-indexed rows, 1 cp.async pipeline, 2 particle-per-thread, 3 tile with L1 prefetch, 4
- * first tile kernel; 10/11/12 the geometry-recomputing kernels of sweep5.cu; 41-43 timing
- * experiments; 60-64 layout experiments; 20-39 and 50-59 retired: DEM_ERR_INVALID) on the
- * last step's contacts, from the current velocities and the last step's final impulses.
- * Outputs: device ms per sweep, and max |v - v_ref| / max |v_ref| after n sweeps against
- * variant 0.  The particle state and contact getters are unchanged.  DEM_ERR_STATE before any
- * step; DEM_ERR_INVALID for n < 1. */
+/* Diagnostic (not on the stepping path): time n >= 1 Jacobi sweeps of the shipped sweep kernel
+ * (variant must be 0; sweep.cu) on the last step's contacts, from the current
+ * velocities and the last step's final impulses with the main-stage rows.  Output: device ms per
+ * sweep (CUDA events on the context's stream); *max_dv_rel is set to 0.  The particle state and
+ * contact getters are unchanged.  DEM_ERR_STATE before any step; DEM_ERR_INVALID for n < 1, a
+ * variant other than 0, a decomposed context or the Gauss-Seidel ordering. */
 dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms_per_sweep, double *max_dv_rel);
+
+/* Bytes one drive call (dem_drive_wall, dem_drive_plate) copies host -> device: the boundary
+ * state is uploaded whole (accounting of end-to-end benchmarks).  Pure, never fails. */
+int64_t dem_drive_upload_bytes(void);
 
 /* Owned particles of this rank (all particles with world_size 1), and owned + ghost copies. */
 int64_t dem_num_particles(const dem_ctx *ctx);

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "lib", "libdem.so")
-SOURCES = ["ctx.cu", "detect.cu", "solve.cu", "sweep5.cu", "sweep_t2.cu", "dist.cu", "generate.cu", "gs.cu", "scan.cu", "radix_sort.cu", "planner.cpp"]
+SOURCES = ["ctx.cu", "detect.cu", "solve.cu", "sweep.cu", "dist.cu", "generate.cu", "gs.cu", "scan.cu", "radix_sort.cu", "planner.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3", "--expt-relaxed-constexpr"]

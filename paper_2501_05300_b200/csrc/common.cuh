@@ -26,23 +26,6 @@
 #define INC_CMASK 0x7FFFFFFFu            // incidence entry: contact index bits
 #define CCAND_FLIP 0x80000000u           // ccand entry: the contact's (a, b) is its candidate (j, i)
 
-// both impulse records of a contact in one 32-byte slot: (P_n, P_t) and (P_r, 0)
-struct __align__(32) P8 { float4 a, b; };
-__device__ __forceinline__ P8 ldP8(const P8 *p)
-{
-    P8 r;
-    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y), "=f"(r.b.z), "=f"(r.b.w)
-        : "l"(p));
-    return r;
-}
-__device__ __forceinline__ void stP8(P8 *p, const float4 a, const float4 b)
-{
-    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(a.x), "f"(a.y), "f"(a.z),
-                 "f"(a.w), "f"(b.x), "f"(b.y), "f"(b.z), "f"(b.w)
-                 : "memory");
-}
-
 // Canonical orientation of a particle pair: body a = the smaller gid, so every
 // decomposition evaluates a contact with the same operands in the same order.
 __device__ __forceinline__ bool cand_flip(uint2 ij, const uint32_t *__restrict__ gid)
@@ -64,10 +47,9 @@ __device__ __forceinline__ uint64_t partner_key(uint32_t p, const uint32_t *__re
 // store impulses / normals / row constants as fp64 instead of fp32 (all row arithmetic is fp64).
 // The shipped build uses G64 + R64 (fp32 impulses), chosen by measured parity.
 #ifdef DEM_P64
-typedef double4 P4;
-#else
-typedef float4 P4;
+#error "DEM_P64 was retired: contact-array impulses are float4 (the sweep's item records choose their own precision)"
 #endif
+typedef float4 P4;
 #ifdef DEM_G64
 typedef double4 G4;
 #else

@@ -76,17 +76,18 @@ struct dem_ctx {
     P4 *Pfa = nullptr, *Pfb = nullptr;            // final impulses of the last step
     uint32_t *ccand = nullptr;
     // incidence
-    uint32_t *inc_cnt = nullptr, *inc_start = nullptr, *order = nullptr;
-    // packed incidence of the canonical reduction (solver.reduction == 0; sweep_t2.cu)
-    uint32_t *pk_off = nullptr, *pk_start = nullptr, *pk_wsize = nullptr, *pk_wbase = nullptr;
-    uint2 *pk_inc = nullptr;
-    G4 *pk_geo = nullptr;
-    R4 *pk_row = nullptr, *pk_rowi = nullptr;
-    P8 *p8[2] = {nullptr, nullptr};
-    int64_t pk_cap = 0, pk_n = 0;
-    PackedInc pkv{};
-    // CUDA graphs of the packed sweep loops (single context): re-captured when a pointer, the
-    // particle count, the sweep count, the start parity or the solver parameters change
+    uint32_t *inc_cnt = nullptr, *inc_start = nullptr;
+    // contact-once tile plan of the Jacobi sweep (sweep.cu), rebuilt every step
+    SweepPlan pl{};
+    uint32_t *pl_nitem = nullptr, *pl_nin = nullptr;
+    unsigned int *pl_full = nullptr;
+    int64_t n_items = 0, cap_items = 0;
+    CRec *it_rec = nullptr;
+    PRec *it_P[2] = {nullptr, nullptr};
+    uint32_t *it_flag = nullptr, *it_scan = nullptr, *it_plist = nullptr;   // monolithic plates: plate items
+    int64_t n_it_plist = 0;
+    // CUDA graphs of the sweep loops (single context): re-captured when a pointer, the particle
+    // count, the sweep count, the start parity or the solver parameters change
     struct SweepGraph { cudaGraphExec_t exec = nullptr; std::vector<unsigned char> key; };
     SweepGraph g_imp[4], g_main[4];   // small LRU caches (start parity, ping-pong pointer sets)
     int64_t g_tick = 0;
@@ -142,7 +143,6 @@ struct dem_ctx {
 };
 
 // ------------------------------------------------------------------ helpers
-#define PKV(ctx) ((ctx)->sol.reduction == 0 && (ctx)->pk_n ? &(ctx)->pkv : nullptr)
 #define OWN(ctx) ((ctx)->tp ? (const uint8_t *)(ctx)->own : (const uint8_t *)nullptr)
 #define CK(call)                                                                      \
     do {                                                                              \
@@ -321,8 +321,8 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
     double4 **d4[] = {&ctx->pos, &ctx->pos2, &ctx->vel[0], &ctx->vel[1], &ctx->ang[0], &ctx->ang[1], &ctx->vel2,
                       &ctx->ang2, &ctx->xref, &ctx->pos_prev, &ctx->vel_prev, &ctx->ang_prev};
     uint32_t **u4[] = {&ctx->gid, &ctx->gid2, &ctx->gid_sorted, &ctx->co_start, &ctx->ct_cnt, &ctx->ct_start,
-                       &ctx->ct_cursor, &ctx->inc_cnt, &ctx->inc_start, &ctx->order, &ctx->pk_off, &ctx->pk_start,
-                       &ctx->pk_wsize, &ctx->pk_wbase};
+                       &ctx->ct_cursor, &ctx->inc_cnt, &ctx->inc_start, &ctx->pl.istart, &ctx->pl.pin,
+                       &ctx->pl_nitem, &ctx->pl_nin};
     const size_t N = (size_t)cap + 1;
     for (auto q : d4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N)); }
     for (auto q : u4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N + 1)); }
@@ -332,6 +332,12 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
     ctx->own = nullptr;
     TRY(A(ctx, &ctx->own, N));
     TRY(A(ctx, &ctx->ke_part, N / 256 + 2));
+    dfree(ctx, ctx->pl.noint);
+    dfree(ctx, ctx->pl.rad);
+    ctx->pl.noint = nullptr;
+    ctx->pl.rad = nullptr;
+    TRY(A(ctx, &ctx->pl.noint, N / SWEEP_TILE + 2));
+    TRY(A(ctx, &ctx->pl.rad, N));
     if (!ctx->lvbox) {
         TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
         TRY(A(ctx, &ctx->db, 1));
@@ -340,6 +346,7 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
         TRY(A(ctx, &ctx->hub_acc, 3 * DEM_MAX_PLATES));
         CK(cudaMemsetAsync(ctx->hub_acc, 0, 3 * DEM_MAX_PLATES * sizeof(unsigned long long), ctx->s));
         TRY(A(ctx, &ctx->dsc, 1));
+        TRY(A(ctx, &ctx->pl_full, 1));
     }
     ctx->capN = cap;
     // the key/scan scratch is not reset: it also serves the candidate and history sorts
@@ -372,7 +379,7 @@ static dem_status ensure_cand(dem_ctx *ctx, int64_t n)
     TRY(regrow(ctx, &ctx->row_imp, cap)); TRY(regrow(ctx, &ctx->Pwa, cap)); TRY(regrow(ctx, &ctx->Pwb, cap));
     for (int k = 0; k < 2; k++) { TRY(regrow(ctx, &ctx->Pa[k], cap)); TRY(regrow(ctx, &ctx->Pb[k], cap)); }
     TRY(regrow(ctx, &ctx->ccand, cap));
-    TRY(regrow(ctx, &ctx->p8[0], cap)); TRY(regrow(ctx, &ctx->p8[1], cap));
+    TRY(regrow(ctx, &ctx->pl.slot_of, cap));
     TRY(regrow(ctx, &ctx->plist, cap + 1));
     TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
     if (ctx->sol.ordering == 1 || ctx->gs_cij) {
@@ -877,37 +884,50 @@ static dem_status rebuild(dem_ctx *ctx)
 }
 
 // ------------------------------------------------------------------ one step
-// canonical reduction: pack each warp's half-contact lists into 32-lane chunks (sweep_t2.cu)
-static dem_status pack_incidence(dem_ctx *ctx, int64_t N)
+// the Jacobi sweep's tile plan of this step (sweep.cu): items per tile, slots, radii
+static dem_status build_plan(dem_ctx *ctx, int64_t N)
 {
     cudaStream_t s = ctx->s;
-    const int64_t nw = (N + 31) / 32;
-    pack_plan(N, ctx->inc_start, ctx->pk_off, ctx->pk_wsize, ctx->pk_wbase, ctx->scan_tmp, s, &ctx->launches);
-    uint32_t np = 0;
-    CK(cudaMemcpyAsync(&np, ctx->pk_wbase + nw, 4, cudaMemcpyDeviceToHost, s));
+    if (N > (int64_t)IT_IDX) { ctx->err = "more than 2^29 local particles on one rank"; return DEM_ERR_INVALID; }
+    plan_counts(N, ctx->inc_start, ctx->inc, ctx->pl, ctx->pl_nitem, ctx->pl_nin, ctx->pl_full, ctx->scan_tmp, s,
+                &ctx->launches);
+    uint32_t ni = 0;
+    CK(cudaMemcpyAsync(&ni, ctx->pl.istart + N, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if ((int64_t)np > ctx->pk_cap) {
-        const int64_t cap = std::max<int64_t>((int64_t)np + np / 4, 1024);
-        TRY(regrow(ctx, &ctx->pk_inc, cap));
-        TRY(regrow(ctx, &ctx->pk_geo, cap)); TRY(regrow(ctx, &ctx->pk_row, cap)); TRY(regrow(ctx, &ctx->pk_rowi, cap));
-        ctx->pk_cap = cap;
+    if ((int64_t)ni > ctx->cap_items) {
+        const int64_t cap = std::max<int64_t>((int64_t)ni + ni / 4, 1024);
+        TRY(regrow(ctx, &ctx->pl.item_c, cap)); TRY(regrow(ctx, &ctx->pl.item_meta, cap));
+        TRY(regrow(ctx, &ctx->it_rec, cap)); TRY(regrow(ctx, &ctx->it_P[0], cap * PREC_UNITS));
+        TRY(regrow(ctx, &ctx->it_P[1], cap * PREC_UNITS));
+        TRY(regrow(ctx, &ctx->it_flag, cap + 1)); TRY(regrow(ctx, &ctx->it_scan, cap + 1));
+        TRY(regrow(ctx, &ctx->it_plist, cap + 1));
+        ctx->cap_items = cap;
+        TRY(ensure_keys(ctx, cap + 1));   // scan scratch of the plate-item list
     }
-    ctx->pk_n = np;
-    if (getenv("DEM_DEBUG"))
-        fprintf(stderr, "[dem] packed incidence: %u lanes for %llu half-contacts (%.2f %% holes)\n", np,
-                (unsigned long long)(2 * ctx->nc), np ? 100.0 * (np - 2.0 * ctx->nc) / np : 0.0);
-    pack_fill(N, ctx->inc_start, ctx->inc, ctx->pk_off, ctx->pk_wbase, ctx->pk_start, ctx->pk_inc, np, s, &ctx->launches);
-    ctx->pkv = PackedInc{ctx->pk_inc, ctx->pk_start, ctx->pk_wbase, ctx->pk_geo, ctx->pk_row, ctx->p8[0], ctx->p8[1]};
+    ctx->n_items = ni;
+    plan_fill(N, ctx->inc_start, ctx->inc, ctx->pos, ctx->pl, s, &ctx->launches);
+    if (getenv("DEM_DEBUG")) {
+        unsigned full = 0;
+        CK(cudaMemcpyAsync(&full, ctx->pl_full, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        fprintf(stderr, "[dem] sweep plan: %u items for %lld contacts (%.3f per contact)%s\n", ni, (long long)ctx->nc,
+                ctx->nc ? (double)ni / ctx->nc : 0.0, full ? ", some tiles over the slot capacity" : "");
+    }
     return DEM_OK;
 }
 
 // monolithic plates (R18b): the impulse the force-driven plate axes received between pin and pout
-// (pin == nullptr: all of pout; first: plus the external impulse h F), summed over the ranks
+// (pin == nullptr: all of pout; first: plus the external impulse h F), summed over the ranks.
+// items: pin/pout are item impulse records (sweeps), else contact-indexed P4 (warm start).
 static bool mono_active(const dem_ctx *ctx) { return ctx->hb.mono && ctx->hb.n_plates > 0 && ctx->sol.ordering == 0; }
-static dem_status plate_hub(dem_ctx *ctx, bool p8, const void *pin, const void *pout, int first)
+static dem_status plate_hub(dem_ctx *ctx, bool items, const void *pin, const void *pout, int first)
 {
     cudaStream_t s = ctx->s;
-    launch_plate_hub(p8, ctx->n_plist, ctx->plist, ctx->cij, ctx->geo, pin, pout, ctx->hub_acc, s);
+    if (items)
+        launch_plate_hub_items(ctx->n_it_plist, ctx->it_plist, ctx->pl, ctx->geo, ctx->it_rec, (const PRec *)pin,
+                               (const PRec *)pout, ctx->hub_acc, s);
+    else
+        launch_plate_hub(ctx->n_plist, ctx->plist, ctx->cij, ctx->geo, pin, pout, ctx->hub_acc, s);
     if (ctx->tp) {
         long long v[3 * DEM_MAX_PLATES];
         CK(cudaMemcpyAsync(v, ctx->hub_acc, sizeof(v), cudaMemcpyDeviceToHost, s));
@@ -920,51 +940,36 @@ static dem_status plate_hub(dem_ctx *ctx, bool p8, const void *pin, const void *
     return DEM_OK;
 }
 
-// Runs n packed sweeps (impulses ping-pong in p8[0/1] from p8[0]; velocities from vel[cur]),
-// replaying a captured CUDA graph when the launch configuration is unchanged (single context:
-// the sweep loop has no host step between launches).  ctx->cur ends n sweeps later.
-static dem_status packed_sweeps(dem_ctx *ctx, int stage, int n, const R4 *rows, const SolveParams &sp)
+// Runs n Jacobi sweeps of the stage (impulses ping-pong in it_P[0/1] from it_P[0]; velocities
+// from vel[cur]), replaying a captured CUDA graph when the launch configuration is unchanged
+// (single context: the sweep loop has no host step between launches).  ctx->cur ends n sweeps
+// later.
+static dem_status item_sweeps(dem_ctx *ctx, int stage, int n, const SolveParams &sp)
 {
     cudaStream_t s = ctx->s;
     const int64_t N = ctx->N;
     const int c0 = ctx->cur;
     const bool hub = mono_active(ctx);
-    auto body = [&]() {
-        for (int it = 0; it < n; it++) {
-            const int a = c0 ^ (it & 1);
-            ctx->pkv.row = rows;
-            ctx->pkv.p8in = ctx->p8[it & 1];
-            ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
-            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[a], ctx->ang[a], ctx->vel[a ^ 1], ctx->ang[a ^ 1],
-                         ctx->inc_start, ctx->inc, &ctx->pkv, ctx->geo, nullptr, nullptr, nullptr, nullptr, nullptr,
-                         ctx->db, sp, s);
-            if (hub) {
-                launch_plate_hub(true, ctx->n_plist, ctx->plist, ctx->cij, ctx->geo, ctx->p8[it & 1],
-                                 ctx->p8[(it & 1) ^ 1], ctx->hub_acc, s);
-                launch_plate_kick(ctx->db, ctx->hub_acc, sp.h, 0, s);
-            }
-        }
+    const bool impact = stage == 0;
+    auto one = [&](int it, int a) {
+        launch_sweep_items(impact, N, ctx->vel[a], ctx->ang[a], ctx->pl.rad, ctx->vel[a ^ 1], ctx->ang[a ^ 1], ctx->pl,
+                           ctx->it_rec, ctx->it_P[it & 1], ctx->it_P[(it & 1) ^ 1], ctx->db, sp, s);
     };
+    ctx->launches += n;
     if (ctx->tp || n < 2 || getenv("DEM_NO_GRAPHS")) {
         for (int it = 0; it < n; it++) {
-            const int a = ctx->cur;
-            ctx->pkv.row = rows;
-            ctx->pkv.p8in = ctx->p8[it & 1];
-            ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
-            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[a], ctx->ang[a], ctx->vel[a ^ 1], ctx->ang[a ^ 1],
-                         ctx->inc_start, ctx->inc, &ctx->pkv, ctx->geo, nullptr, nullptr, nullptr, nullptr, nullptr,
-                         ctx->db, sp, s);
-            if (hub) TRY(plate_hub(ctx, true, ctx->p8[it & 1], ctx->p8[(it & 1) ^ 1], 0));
+            one(it, ctx->cur);
+            if (hub) TRY(plate_hub(ctx, true, ctx->it_P[it & 1], ctx->it_P[(it & 1) ^ 1], 0));
             ctx->cur ^= 1;
             TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
         }
         return DEM_OK;
     }
     // key: everything the captured launches bake in
-    const void *ptrs[] = {ctx->vel[0], ctx->vel[1], ctx->ang[0], ctx->ang[1], ctx->inc_start, ctx->pk_inc, ctx->pk_start,
-                          ctx->pk_wbase, ctx->pk_geo, rows, ctx->p8[0], ctx->p8[1], ctx->db, ctx->plist, ctx->cij,
-                          ctx->geo, ctx->hub_acc};
-    const int64_t ints[] = {N, n, c0, hub ? ctx->n_plist : -1};
+    const void *ptrs[] = {ctx->vel[0], ctx->vel[1], ctx->ang[0], ctx->ang[1], ctx->pl.rad, ctx->pl.istart, ctx->pl.pin,
+                          ctx->it_rec, ctx->it_P[0], ctx->it_P[1], ctx->db, ctx->it_plist, ctx->pl.item_c, ctx->geo,
+                          ctx->hub_acc};
+    const int64_t ints[] = {N, n, c0, hub ? ctx->n_it_plist : -1};
     std::vector<unsigned char> key(sizeof(ptrs) + sizeof(ints) + sizeof(SolveParams));
     std::memcpy(key.data(), ptrs, sizeof(ptrs));
     std::memcpy(key.data() + sizeof(ptrs), ints, sizeof(ints));
@@ -983,7 +988,14 @@ static dem_status packed_sweeps(dem_ctx *ctx, int stage, int n, const R4 *rows, 
         if (g.exec) { cudaGraphExecDestroy(g.exec); g.exec = nullptr; }
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        body();
+        for (int it = 0; it < n; it++) {
+            one(it, c0 ^ (it & 1));
+            if (hub) {
+                launch_plate_hub_items(ctx->n_it_plist, ctx->it_plist, ctx->pl, ctx->geo, ctx->it_rec, ctx->it_P[it & 1],
+                                       ctx->it_P[(it & 1) ^ 1], ctx->hub_acc, s);
+                launch_plate_kick(ctx->db, ctx->hub_acc, sp.h, 0, s);
+            }
+        }
         CK(cudaStreamEndCapture(s, &graph));
         CK(cudaGraphInstantiate(&g.exec, graph, 0));
         cudaGraphDestroy(graph);
@@ -1028,8 +1040,9 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     launch_count_kinds(nc, OWN(ctx), ctx->cij, ctx->gid, ctx->dsc, s);
     launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->gid, ctx->inc_cnt,
                ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
-    if (ctx->sol.reduction == 0 && ctx->sol.ordering == 0) TRY(pack_incidence(ctx, N));
+    if (ctx->sol.ordering == 0) TRY(build_plan(ctx, N));
     ctx->n_plist = 0;
+    ctx->n_it_plist = 0;
     if (mono_active(ctx) && nc) {
         // monolithic plates: this step's owned plate contacts (cflag/cscan are free again)
         launch_plate_list_flags(nc, OWN(ctx), ctx->cij, ctx->cflag, s);
@@ -1039,11 +1052,19 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         CK(cudaStreamSynchronize(s));
         launch_compact_idx(nc, ctx->cflag, ctx->cscan, ctx->plist, s);
         ctx->n_plist = np;
-        ctx->launches += 2;
+        // ... and their items (the per-sweep increments come from the item impulses)
+        const int64_t ni = ctx->n_items;
+        launch_plate_items_flag(ni, OWN(ctx), ctx->pl, ctx->cij, ctx->it_flag, s);
+        scan_u32(ctx->it_flag, ctx->it_scan, ni, ctx->scan_tmp, s, &ctx->launches);
+        uint32_t npi = 0;
+        CK(cudaMemcpyAsync(&npi, ctx->it_scan + ni, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        launch_compact_idx(ni, ctx->it_flag, ctx->it_scan, ctx->it_plist, s);
+        ctx->n_it_plist = npi;
+        ctx->launches += 4;
     }
     launch_prepare(N, ctx->inc_start, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], sp.rho, s);
     TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));      // ghosts' weights c/m, c/I from their owners
-    if (sweep_uses_order()) launch_tile_order(N, ctx->inc_start, ctx->order, s);
     // impact trigger
     launch_rows(nc, 0, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
     ctx->launches += 6;
@@ -1085,35 +1106,17 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         ctx->tm.particle_sweeps += (int64_t)n_imp * N;
     } else if (impact) {
         // Newton impact stage from P = 0 with Sigma = 0 (reading R13); impulses discarded
-        CK(cudaMemsetAsync(ctx->Pa[0], 0, nc * sizeof(P4), s));
-        CK(cudaMemsetAsync(ctx->Pb[0], 0, nc * sizeof(P4), s));
-        if (PKV(ctx)) {   // canonical reduction: packed rows, impulses in 32-byte slots
-            pack_rows(ctx->pk_n, ctx->pk_inc, ctx->geo, ctx->row_imp, ctx->pk_geo, ctx->pk_rowi, s);
-            CK(cudaMemsetAsync(ctx->p8[0], 0, nc * sizeof(P8), s));
-            ctx->launches += 1;
-            TRY(packed_sweeps(ctx, 0, n_imp, ctx->pk_rowi, sp));
-        }
-        for (int it = 0; it < (PKV(ctx) ? 0 : n_imp); it++) {
-            const int pi = it & 1;
-            ctx->pkv.p8in = ctx->p8[pi];
-            ctx->pkv.p8out = ctx->p8[pi ^ 1];
-            launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
-                         ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row_imp, ctx->Pa[pi],
-                         ctx->Pb[pi], ctx->Pa[pi ^ 1], ctx->Pb[pi ^ 1], ctx->db, sp, s);
-            if (mono_active(ctx)) TRY(plate_hub(ctx, false, ctx->Pa[pi], ctx->Pa[pi ^ 1], 0));
-            ctx->cur ^= 1;
-            TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
-        }
-        ctx->launches += n_imp;
+        item_pack(ctx->n_items, ctx->pl, ctx->geo, ctx->cdel, ctx->row_imp, nullptr, nullptr, ctx->it_rec, ctx->it_P[0], s);
+        ctx->launches += 1;
+        TRY(item_sweeps(ctx, 0, n_imp, sp));
         ctx->tm.n_sweep_launches += n_imp;
         ctx->tm.contact_sweeps += (int64_t)n_imp * nc;
         ctx->tm.particle_sweeps += (int64_t)n_imp * N;
     }
     // main stage: SPOOK rows, gravity + warm start, N_it Jacobi sweeps
     launch_rows(nc, 1, ctx->cij, ctx->geo, ctx->cdel, ctx->row, ctx->row_imp, ctx->vel[ctx->cur], ctx->pos, ctx->db, sp, ctx->dsc, s);
-    launch_sweep(SWEEP_MODE_APPLY, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
-                 ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, nullptr,
-                 nullptr, ctx->db, sp, s);
+    launch_apply(SWEEP_MODE_APPLY, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
+                 ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, sp, s);
     ctx->cur ^= 1;
     ctx->launches += 2;
     TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
@@ -1122,13 +1125,6 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     tstart(ctx, 3);
     const int n_it = ctx->sol.n_iter;
     const P4 *pin_a = ctx->Pwa, *pin_b = ctx->Pwb;
-    const bool pk = !gs && PKV(ctx) != nullptr;
-    if (pk) {
-        pack_rows(ctx->pk_n, ctx->pk_inc, ctx->geo, ctx->row, ctx->pk_geo, ctx->pk_row, s);
-        p8_pack(nc, ctx->Pwa, ctx->Pwb, ctx->p8[0], s);
-        ctx->pkv.row = ctx->pk_row;
-        ctx->launches += 2;
-    }
     if (gs) {
         // N_it coloured Gauss-Seidel sweeps, impulses and velocities updated in place
         gs_gather(nc, ctx->gs_ord, ctx->cij, ctx->geo, ctx->row, ctx->Pwa, ctx->Pwb, nullptr, nullptr, ctx->gs_row,
@@ -1140,29 +1136,15 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
         ctx->launches += 3;
         pin_a = ctx->Pa[0];
         pin_b = ctx->Pb[0];
-    }
-    if (pk) TRY(packed_sweeps(ctx, 1, n_it, ctx->pk_row, sp));
-    for (int it = 0; it < ((gs || pk) ? 0 : n_it); it++) {
-        P4 *oa = ctx->Pa[it & 1], *ob = ctx->Pb[it & 1];
-        ctx->pkv.p8in = ctx->p8[it & 1];
-        ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
-        launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel[ctx->cur ^ 1],
-                     ctx->ang[ctx->cur ^ 1], ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row, pin_a, pin_b, oa, ob,
-                     ctx->db, sp, s);
-        if (mono_active(ctx)) TRY(plate_hub(ctx, false, pin_a, oa, 0));
-        ctx->cur ^= 1;
-        TRY(halo(ctx, ctx->vel[ctx->cur], ctx->ang[ctx->cur]));
-        pin_a = oa;
-        pin_b = ob;
-    }
-    if (pk && n_it > 0) {
-        // the final impulses back into the per-array layout the rest of the step reads
-        p8_unpack(nc, ctx->p8[n_it & 1], ctx->Pa[0], ctx->Pb[0], s);
+    } else if (n_it > 0) {
+        // N_it Jacobi sweeps from the warm start, then the final impulses back to the contacts
+        item_pack(ctx->n_items, ctx->pl, ctx->geo, ctx->cdel, ctx->row, ctx->Pwa, ctx->Pwb, ctx->it_rec, ctx->it_P[0], s);
+        TRY(item_sweeps(ctx, 1, n_it, sp));
+        item_unpack(ctx->n_items, ctx->pl, ctx->it_rec, ctx->it_P[n_it & 1], ctx->Pa[0], ctx->Pb[0], s);
+        ctx->launches += 2;
         pin_a = ctx->Pa[0];
         pin_b = ctx->Pb[0];
-        ctx->launches += 1;
     }
-    if (!gs) ctx->launches += n_it;
     ctx->tm.n_sweep_launches += n_it;
     ctx->tm.contact_sweeps += (int64_t)n_it * nc;
     ctx->tm.particle_sweeps += (int64_t)n_it * N;
@@ -1613,8 +1595,8 @@ dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device)
     const int64_t N = ctx->N, Nown = ctx->N_own;
     if (!N) return DEM_OK;
     cudaStream_t s = ctx->s;
-    launch_sweep(SWEEP_MODE_FORCES, N, ctx->order, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
-                 ctx->inc, PKV(ctx), ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, nullptr, nullptr, ctx->db, ctx->sp, s);
+    launch_apply(SWEEP_MODE_FORCES, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
+                 ctx->inc, ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, ctx->sp, s);
     double *d = nullptr;
     TRY(A(ctx, &d, 6 * N));
     launch_to_gid_order(N, Nown, OWN(ctx), ctx->gid, ctx->gid_sorted, ctx->vel2, ctx->ang2, nullptr, d, d + 3 * Nown, nullptr, nullptr,
@@ -1744,130 +1726,42 @@ dem_status dem_reset_timing(dem_ctx *ctx)
     return DEM_OK;
 }
 
-// Diagnostic: time n Jacobi sweeps of one sweep-kernel variant on the last step's contact set
-// (inputs: the current velocities, the last step's final impulses, main-stage rows) and report
-// the max velocity difference after n sweeps against the shipped kernel (variant 0).
-// Leaves the particle state and the last step's contact getters untouched.
+// Diagnostic: time n Jacobi sweeps of the shipped sweep kernel (variant 0, the only one) on the
+// last step's contact set: inputs are the current velocities and the last step's final
+// impulses with the main-stage rows.  Leaves the particle state and the contact getters
+// untouched (the sweeps write scratch buffers).  *max_dv_rel is 0 (kept for the ABI).
 dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms_per_sweep, double *max_dv_rel)
 {
     if (!ctx || n < 1) return DEM_ERR_INVALID;
     if (!ctx->have_step) { ctx->err = "no step taken yet"; return DEM_ERR_STATE; }
     if (ctx->tp) { ctx->err = "dem_bench_sweeps needs world_size 1"; return DEM_ERR_INVALID; }
-    if ((variant >= 20 && variant < 40) || (variant >= 50 && variant < 60)) {
-        // tile-paired / slot / staged experiments assume contacts oriented as their candidates
-        // (body a = the scanning particle); retired with the gid-canonical orientation
-        ctx->err = "sweep variants 20-39 and 50-59 were retired (they need candidate-oriented contacts)";
-        return DEM_ERR_INVALID;
-    }
-    const int64_t N = ctx->N, nc = ctx->nc;
+    if (variant != 0) { ctx->err = "dem_bench_sweeps: only variant 0 (the shipped sweep) exists"; return DEM_ERR_INVALID; }
+    if (ctx->sol.ordering != 0) { ctx->err = "dem_bench_sweeps times the Jacobi sweep (ordering 0)"; return DEM_ERR_INVALID; }
+    const int64_t N = ctx->N;
     cudaStream_t s = ctx->s;
-    double *cb = nullptr;
-    double4 *ref = nullptr;
-    unsigned long long *md = nullptr;
-    TRY(A(ctx, &cb, nc + 1));
-    TRY(A(ctx, &ref, N + 1));
-    TRY(A(ctx, &md, 2));
-    launch_row_bias(nc, ctx->row, cb, s);
-    launch_tile_order(N, ctx->inc_start, ctx->order, s);
-    P4 *spa = ctx->Pfa == ctx->Pa[0] ? ctx->Pa[1] : ctx->Pa[0];
-    P4 *spb = ctx->Pfb == ctx->Pb[0] ? ctx->Pb[1] : ctx->Pb[0];
-    double4 *vbuf[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel2}, *wbuf[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang2};
-    float ms = 0.f;
-    double4 *vres = nullptr;
-    G4 *plg = nullptr;
-    R4 *plr = nullptr;
-    for (int pass = 0; pass < 2; pass++) {
-        const int var = pass == 0 ? 0 : variant;
-        CK(cudaMemcpyAsync(ctx->Pwa, ctx->Pfa, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(ctx->Pwb, ctx->Pfb, nc * sizeof(P4), cudaMemcpyDeviceToDevice, s));
-        if (var >= 60) {
-            // layout experiment: P8 / VW interleaved records (sweep_t2.cu, run_sweep_t3)
-            void *scr = nullptr;
-            double4 *r3 = nullptr;
-            TRY(dalloc(ctx, &scr, (size_t)nc * 64 + (size_t)N * 128 + 1024));
-            TRY(A(ctx, &r3, N + 1));
-            P4 *pa2[2] = {ctx->Pwa, spa}, *pb2[2] = {ctx->Pwb, spb};
-            run_sweep_t3(var - 60, n, N, nc, ctx->vel[ctx->cur], ctx->ang[ctx->cur], vbuf, wbuf, ctx->inc_start, ctx->inc,
-                         ctx->geo, ctx->row, pa2, pb2, scr, ctx->db, ctx->sp, s, r3, ctx->ev[6], ctx->ev[7]);
-            CK(cudaGetLastError());
-            CK(cudaStreamSynchronize(s));
-            cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
-            vres = r3;
-            launch_maxdiff(N, vres, ref, md, s);
-            unsigned long long h3[2] = {0, 0};
-            CK(cudaMemcpyAsync(h3, md, sizeof(h3), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            double d3v, m3;
-            std::memcpy(&d3v, &h3[0], 8);
-            std::memcpy(&m3, &h3[1], 8);
-            if (ms_per_sweep) *ms_per_sweep = ms / n;
-            if (max_dv_rel) *max_dv_rel = m3 > 0 ? d3v / m3 : d3v;
-            dfree(ctx, scr);
-            dfree(ctx, r3);
-            dfree(ctx, cb); dfree(ctx, ref); dfree(ctx, md);
-            return DEM_OK;
-        }
-        const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
-        P4 *pai = ctx->Pwa, *pbi = ctx->Pwb, *pao = spa, *pbo = spb;
-        if ((var == 0 || var == 8 || var == 9 || var == 44 || var == 45) && PKV(ctx)) {
-            p8_pack(nc, ctx->Pwa, ctx->Pwb, ctx->p8[0], s);
-            ctx->pkv.geo = var == 8 ? ctx->geo : ctx->pk_geo;
-            ctx->pkv.row = var == 8 ? ctx->row : ctx->pk_row;
-            if (var == 9) {   // the staged kernel reads chunk-plane records
-                if (!plg) { TRY(A(ctx, &plg, ctx->pk_n)); TRY(A(ctx, &plr, ctx->pk_n)); }
-                to_planes(ctx->pk_n, ctx->pk_geo, plg, s);
-                to_planes(ctx->pk_n, ctx->pk_row, plr, s);
-                ctx->pkv.geo = plg;
-                ctx->pkv.row = plr;
-            }
-        }
-        cudaEventRecord(ctx->ev[6], s);
-        for (int it = 0; it < n; it++) {
-            double4 *vo = vbuf[it & 1], *wo = wbuf[it & 1];
-            ctx->pkv.p8in = ctx->p8[it & 1];
-            ctx->pkv.p8out = ctx->p8[(it & 1) ^ 1];
-            if (var < 10 || (var >= 40 && var < 50)) {
-                set_sweep_variant(var);
-                launch_sweep(SWEEP_MODE_SWEEP, N, ctx->order, vi, wi, vo, wo, ctx->inc_start, ctx->inc, PKV(ctx), ctx->geo, ctx->row,
-                             pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
-            } else {
-                // geometry from the positions the step's sweeps saw (before integration)
-                launch_sweep5(var - 10, false, N, ctx->order, ctx->pos_prev, vi, wi, vo, wo, ctx->inc_start, ctx->inc, cb,
-                              pai, pbi, pao, pbo, ctx->db, ctx->sp, s);
-            }
-            vi = vo; wi = wo;
-            std::swap(pai, pao);
-            std::swap(pbi, pbo);
-            vres = vo;
-        }
-        cudaEventRecord(ctx->ev[7], s);
-        set_sweep_variant(0);
-        ctx->pkv.geo = ctx->pk_geo;
-        ctx->pkv.row = ctx->pk_row;
-        CK(cudaGetLastError());
-        if (pass == 0) CK(cudaMemcpyAsync(ref, vres, N * sizeof(double4), cudaMemcpyDeviceToDevice, s));
-        CK(cudaStreamSynchronize(s));
-        cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
+    item_pack(ctx->n_items, ctx->pl, ctx->geo, ctx->cdel, ctx->row, ctx->Pfa, ctx->Pfb, ctx->it_rec, ctx->it_P[0], s);
+    double4 *vb[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel2}, *wb[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang2};
+    const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
+    cudaEventRecord(ctx->ev[6], s);
+    for (int it = 0; it < n; it++) {
+        launch_sweep_items(false, N, vi, wi, ctx->pl.rad, vb[it & 1], wb[it & 1], ctx->pl, ctx->it_rec,
+                           ctx->it_P[it & 1], ctx->it_P[(it & 1) ^ 1], ctx->db, ctx->sp, s);
+        vi = vb[it & 1];
+        wi = wb[it & 1];
     }
-    launch_maxdiff(N, vres, ref, md, s);
-    unsigned long long h[2] = {0, 0};
-    CK(cudaMemcpyAsync(h, md, sizeof(h), cudaMemcpyDeviceToHost, s));
+    cudaEventRecord(ctx->ev[7], s);
+    CK(cudaGetLastError());
     CK(cudaStreamSynchronize(s));
-    double d, m;
-    std::memcpy(&d, &h[0], 8);
-    std::memcpy(&m, &h[1], 8);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ctx->ev[6], ctx->ev[7]);
     if (ms_per_sweep) *ms_per_sweep = ms / n;
-    if (max_dv_rel) *max_dv_rel = m > 0 ? d / m : d;
-    dfree(ctx, cb);
-    dfree(ctx, ref);
-    dfree(ctx, md);
-    dfree(ctx, plg);
-    dfree(ctx, plr);
-
+    if (max_dv_rel) *max_dv_rel = 0.0;
     return DEM_OK;
 }
 
 void *dem_stream(dem_ctx *ctx) { return ctx ? (void *)ctx->s : nullptr; }
+
+int64_t dem_drive_upload_bytes(void) { return (int64_t)sizeof(DevBoundary); }
 
 int64_t dem_num_particles(const dem_ctx *ctx) { return ctx ? ctx->N_own : -1; }
 

@@ -44,35 +44,9 @@ void launch_prepare(int64_t N, const uint32_t *inc_start, const double4 *pos, do
 void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const double *cdel, R4 *row, R4 *row_imp,
                  const double4 *vel, const double4 *pos, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
                  cudaStream_t s);
-// packed incidence of the canonical reduction (sweep_t2.cu): entries in 32-lane chunks, start[i]
-// = packed position of particle i's list, wbase[g] = first packed entry of warp g's particles
-extern thread_local bool g_t2_rows_by_contact;
-extern thread_local bool g_t2_stage;
-void to_planes(int64_t np, const double4 *in, double4 *out, cudaStream_t s);
-extern thread_local int g_t2_exp;
-struct PackedInc {
-    const uint2 *inc;
-    const uint32_t *start;
-    const uint32_t *wbase;
-    const G4 *geo;        // normals, rows of the stage: one copy per half-contact, packed order
-    const R4 *row;
-    const P8 *p8in;       // impulses of the sweep, one 32-byte slot per contact
-    P8 *p8out;
-};
-void pack_rows(int64_t np, const uint2 *pinc, const G4 *geo, const R4 *row, G4 *gpk, R4 *rpk, cudaStream_t s);
-void p8_pack(int64_t nc, const P4 *a, const P4 *b, P8 *o, cudaStream_t s);
-void p8_unpack(int64_t nc, const P8 *q, P4 *a, P4 *b, cudaStream_t s);
-void pack_plan(int64_t N, const uint32_t *inc_start, uint32_t *off_local, uint32_t *wsize, uint32_t *wbase,
-               void *scan_tmp, cudaStream_t s, long long *launches);
-void pack_fill(int64_t N, const uint32_t *inc_start, const uint2 *inc, const uint32_t *off_local, const uint32_t *wbase,
-               uint32_t *pstart, uint2 *pinc, int64_t npacked, cudaStream_t s, long long *launches);
-void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin, const double4 *win, double4 *vout,
-                  double4 *wout, const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo,
-                  const R4 *row,
-                  const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
-                  const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
-bool sweep_uses_order();
-void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s);
+void launch_apply(int mode, int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
+                  const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row, const P4 *Pa,
+                  const P4 *Pb, const SolveParams &sp, cudaStream_t s);
 void launch_integrate(int64_t N, const uint8_t *own, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
                       double rho, double *ke_part, StepScalars *sc, cudaStream_t s);
 void launch_plate_sum(int64_t nc, const uint8_t *own, const uint2 *cij, const G4 *geo, const P4 *Pa, unsigned long long *acc,
@@ -99,7 +73,7 @@ void launch_first_bad(int64_t nc, int64_t N, const uint8_t *own, const uint2 *ci
                       const P4 *Pb, const double4 *pos, const double4 *vel, const double4 *ang,
                       unsigned long long *out, cudaStream_t s);
 void launch_plate_list_flags(int64_t nc, const uint8_t *own, const uint2 *cij, uint32_t *flag, cudaStream_t s);
-void launch_plate_hub(bool p8, int64_t n, const uint32_t *list, const uint2 *cij, const G4 *geo, const void *pin,
+void launch_plate_hub(int64_t n, const uint32_t *list, const uint2 *cij, const G4 *geo, const void *pin,
                       const void *pout, unsigned long long *acc, cudaStream_t s);
 void launch_plate_kick(DevBoundary *bnd, unsigned long long *acc, double h, int first, cudaStream_t s);
 void launch_keep(int64_t n, const double *x, int axis, double lo, double hi, uint32_t *flag, cudaStream_t s);
@@ -116,26 +90,55 @@ void launch_to_gid_order(int64_t N, int64_t n_sorted, const uint8_t *own, const 
                          uint32_t *ogid, cudaStream_t s);
 void launch_load_state(int64_t N, const double *x, const double *r, const double *v, const double *w,
                        const uint32_t *gid_in, double4 *pos, double4 *vel, double4 *ang, uint32_t *gid, cudaStream_t s);
-void set_sweep_variant(int v);      // 0 k_sweep_tile, 1 k_sweep_pipe, 2 k_sweep_ppt (bench/diagnostics)
-
-// sweep5.cu: sweeps re-evaluating the contact geometry from positions (cb = SPOOK bias per contact)
-enum { SWEEP5_PPT = 0, SWEEP5_PPT_PF = 1, SWEEP5_TILE = 2 };
-void launch_sweep5(int kind, bool impact, int64_t N, const uint32_t *order, const double4 *pos, const double4 *vin,
-                   const double4 *win, double4 *vout, double4 *wout, const uint32_t *inc_start, const uint2 *inc,
-                   const double *cb, const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
-                   const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
-void launch_row_bias(int64_t nc, const R4 *row, double *cb, cudaStream_t s);
-void launch_maxdiff(int64_t N, const double4 *a, const double4 *b, unsigned long long *out, cudaStream_t s);
-
-// sweep_t2.cu: tile sweep with 256-bit records and conflict-free shared staging
-void launch_sweep_t2(int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
-                     const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo, const R4 *row,
-                     const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out, const DevBoundary *bnd,
-                     const SolveParams &sp, cudaStream_t s);
-void run_sweep_t3(int variant, int n, int64_t N, int64_t nc, const double4 *vin, const double4 *win, double4 *vbuf[2],
-                  double4 *wbuf[2], const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row,
-                  P4 *Pa[2], P4 *Pb[2], void *scratch, const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s,
-                  double4 *vres, cudaEvent_t e0, cudaEvent_t e1);
+// sweep.cu: the contact-once tile sweep.  Tiles of SWEEP_TILE particles; items =
+// contacts owned by a tile (intra-tile pairs once, cross-tile pairs once per side, boundary
+// contacts once); item meta word: flags + partner (see IT_*).
+#ifndef SWEEP_TILE
+#define SWEEP_TILE 256
+#endif
+#ifndef SWEEP_SLOT_CAP
+#define SWEEP_SLOT_CAP 768
+#endif
+#ifndef SWEEP_MINB
+#define SWEEP_MINB 3
+#endif
+#define IT_INTRA 0x80000000u     // partner in the tile, body b's share goes to slot (bits 9..20)
+#define IT_B 0x40000000u         // cross pair: the owner is the canonical body b
+#define IT_EXT 0x20000000u       // wall / plate box: bits 0..28 = boundary code (PARTNER_* codes)
+#define IT_IDX 0x1FFFFFFFu       // cross pair: partner's local index (< 2^29)
+#define IT_LOC 0x1FFu            // intra pair: partner's index in the tile
+#define IT_SLOT_SHIFT 9
+#define IT_SLOT_MASK 0xFFFu
+#ifndef SWEEP_PMODE
+#define SWEEP_PMODE 0        // impulse storage of the sweep's items: 0 f32; 1 P_n f64, P_t/P_r f32; 2 f64
+#endif
+#define PREC_UNITS (SWEEP_PMODE == 2 ? 2 : 1)   // 32-byte PRec units per item
+struct __align__(32) CRec { double nu, nv, delta, b; };  // per item, per stage: n (2 of 3 comps, sweep.cu), delta, bias
+struct __align__(32) PRec { uint32_t w[8]; };             // per item, ping-pong: impulses + meta (sweep.cu)
+static_assert(sizeof(CRec) == 32 && sizeof(PRec) == 32, "32-byte item records");
+struct SweepPlan {
+    uint32_t *istart = nullptr;   // [N+1] first item of each particle (tile-contiguous)
+    uint32_t *pin = nullptr;      // [N] slot range in the tile: start | count << 16
+    uint8_t *noint = nullptr;     // [tiles] 1: the tile's intra pairs are evaluated as cross pairs
+    uint32_t *slot_of = nullptr;  // [nc] slot of an intra contact at body b
+    uint32_t *item_c = nullptr;   // [items] contact index
+    uint32_t *item_meta = nullptr;// [items] meta word
+    double *rad = nullptr;        // [N] radius
+};
+void plan_counts(int64_t N, const uint32_t *inc_start, const uint2 *inc, const SweepPlan &pl, uint32_t *nitem,
+                 uint32_t *nin, unsigned int *any_full, void *scan_tmp, cudaStream_t s, long long *launches);
+void plan_fill(int64_t N, const uint32_t *inc_start, const uint2 *inc, const double4 *pos, const SweepPlan &pl,
+               cudaStream_t s, long long *launches);
+void item_pack(int64_t n, const SweepPlan &pl, const G4 *geo, const double *cdel, const R4 *row, const P4 *Pa,
+               const P4 *Pb, CRec *rec, PRec *P, cudaStream_t s);
+void item_unpack(int64_t n, const SweepPlan &pl, const CRec *rec, const PRec *P, P4 *Pa, P4 *Pb, cudaStream_t s);
+void launch_sweep_items(bool impact, int64_t N, const double4 *vin, const double4 *win, const double *rad, double4 *vout,
+                        double4 *wout, const SweepPlan &pl, const CRec *rec, const PRec *Pin, PRec *Pout,
+                        const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s);
+void launch_plate_items_flag(int64_t n, const uint8_t *own, const SweepPlan &pl, const uint2 *cij, uint32_t *flag,
+                             cudaStream_t s);
+void launch_plate_hub_items(int64_t n, const uint32_t *list, const SweepPlan &pl, const G4 *geo, const CRec *rec,
+                            const PRec *pin, const PRec *pout, unsigned long long *acc, cudaStream_t s);
 // generate.cu: on-device bed generator (include/dem.h dem_generator)
 bool generate_bed(const dem_generator &g, const dem_box &box, double slab_lo, double slab_hi,
                   void *(*alloc)(size_t, void *), void *actx, cudaStream_t s, double **x, double **r, uint32_t **gid,

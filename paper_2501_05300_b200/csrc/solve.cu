@@ -3,14 +3,7 @@
 //  k_prepare    mass-splitting weights c/m, c/I per particle (c = contact count)
 //  k_rows       impact trigger and Newton impact rows, SPOOK rows of the Hertz-mapped
 //               normal constraint (reading R4)
-//  k_sweep_tile one Jacobi projected-impulse sweep (P:134 solver run as Jacobi, reading R2).
-//               A block owns a tile of TP consecutive (Morton-ordered) particles; its threads
-//               walk the tile's half-contacts in chunks of TP (one half-contact per thread, all
-//               lanes busy whatever the contact counts), recompute each incident contact from the
-//               sweep-start velocities in the canonical (a, b) orientation -- bit-identical from
-//               both ends -- and the owning particle sums its chunk contributions from shared
-//               memory in CSR order: a deterministic segmented reduction, no float atomics.
-//               Body a of a contact writes the new impulse (ping-pong buffers).
+//  (the Jacobi sweep itself is sweep.cu)
 //  k_apply      gravity + warm-start impulses (MODE_APPLY) and per-particle force/torque
 //               evaluation (MODE_FORCES), one thread per particle
 //  k_integrate  x += h v, displacement since rebuild, KE / max|v| / NaN flags
@@ -69,439 +62,6 @@ __global__ void k_rows(int64_t nc, int mode, const uint2 *__restrict__ cij, cons
     const double S = spook_sigma(sp, ext ? ra : rstar(ra, pos[ij.y].w), delta);
     row[c] = mkR4(S, 4.0 * sp.Ups / sp.h * (delta / sp.e_H) + sp.Ups * un, rw.z, rw.w);
 }
-
-// ------------------------------------------------------------------ the Jacobi sweep
-
-constexpr int TP = 128;
-constexpr int NW = TP / 32;
-#ifndef SWEEP_MINB
-#define SWEEP_MINB 5
-#endif
-#ifndef SWEEP_MINB_PIPE
-#define SWEEP_MINB_PIPE 3
-#endif
-#ifndef SWEEP_MINB_PPT
-#define SWEEP_MINB_PPT 4
-#endif
-#ifndef SWEEP_KERNEL
-#define SWEEP_KERNEL 0      // 0: k_sweep_t2 (default, fastest measured), 1: k_sweep_pipe, 2: k_sweep_ppt, 4: k_sweep_tile
-#endif
-
-// Tile sweep: the block stages the tile's states and CSR offsets in shared memory once; each
-// warp then owns 32 consecutive particles and walks their half-contacts 32 at a time, with no
-// block barrier inside the loop.  Per chunk, owners come from a warp-wide bitmask of segment
-// starts; the lanes' contributions are reduced per owner by a segmented shuffle scan whose
-// depth is the longest segment of the chunk, and each segment's last lane adds the sum to the
-// owner's warp-private shared accumulator (one writer per particle per chunk): a fixed
-// summation order, hence deterministic, and no float atomics.
-__device__ __forceinline__ void pf_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-
-// EXP (timing experiments only): 1 no contact math, 2 no contact-record loads, 3 neither
-// contact-record nor partner global loads (math on shared memory only)
-__device__ __forceinline__ HalfOut fake_half(const double4 VA, const double4 WA, const double4 VB, const double4 WB,
-                                             const G4 g, const R4 rw, const P4 pa, const P4 pb)
-{
-    HalfOut o;
-    o.dL = mk(1e-30 * (VA.x + VB.x + g.x + rw.x + pa.x), 1e-30 * (VA.y + WB.y + g.y + rw.y + pb.x),
-              1e-30 * (WA.z + VB.z + g.z + rw.z + pa.y));
-    o.dA = mk(1e-30 * (WA.x + g.w + rw.w + pa.z), 1e-30 * (WB.x + pa.w + pb.y), 1e-30 * pb.z);
-    o.Pa = pa;
-    o.Pb = pb;
-    return o;
-}
-
-template <bool PF, int EXP = 0>
-__global__ void __launch_bounds__(TP, SWEEP_MINB) k_sweep_tile(int64_t N, const double4 *__restrict__ vin,
-                                                      const double4 *__restrict__ win, double4 *__restrict__ vout,
-                                                      double4 *__restrict__ wout, const uint32_t *__restrict__ inc_start,
-                                                      const uint2 *__restrict__ inc, const G4 *__restrict__ geo,
-                                                      const R4 *__restrict__ row, const P4 *__restrict__ Pa_in,
-                                                      const P4 *__restrict__ Pb_in, P4 *__restrict__ Pa_out,
-                                                      P4 *__restrict__ Pb_out, const DevBoundary *__restrict__ bnd,
-                                                      SolveParams sp)
-{
-    __shared__ double4 sV[TP], sW[TP];
-    __shared__ double4 sExt[TP];                     // per lane: boundary-body velocity
-    __shared__ double sAcc[NW][6][32];               // per warp: per-particle accumulators
-    __shared__ uint8_t sOwn[NW][32];                 // per warp: owner of each segment start
-    __shared__ uint32_t sI[TP + 1];
-    __shared__ double4 sZero;
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int64_t p0 = (int64_t)blockIdx.x * TP;
-    const int np = (int)min((int64_t)TP, N - p0);
-    if (t < np) {
-        sV[t] = vin[p0 + t];
-        sW[t] = win[p0 + t];
-    }
-    for (int q = t; q <= np; q += TP) sI[q] = inc_start[p0 + q];
-    if (t == 0) sZero = make_double4(0, 0, 0, 0);
-#pragma unroll
-    for (int f = 0; f < 6; f++) sAcc[w][f][lane] = 0.0;
-    __syncthreads();
-    const int lo_p = 32 * w, hi_p = min(32 * w + 32, np);
-    const int me = lo_p + lane;                      // this lane's particle (if me < hi_p)
-    const uint32_t s_me = me < hi_p ? sI[me] : 0u, e_me = me < hi_p ? sI[me + 1] : 0u;
-    if (lo_p < np) {
-        const uint32_t k0 = sI[lo_p], k1 = sI[hi_p];
-        uint2 ent_next = make_uint2(0, 0), ent_nn = make_uint2(0, 0);
-        if (k0 + lane < k1) ent_next = inc[k0 + lane];
-        if (PF && k0 + 32 + lane < k1) ent_nn = inc[k0 + 32 + lane];
-        int carry = 0;                               // owner (warp-local) of the chunk's lane 0
-        for (uint32_t kb = k0; kb < k1; kb += 32) {
-            const uint32_t k = kb + lane;
-            const bool valid = k < k1;
-            const uint2 ent = ent_next;
-            if (PF) {
-                // L1 prefetch of the next chunk's contact records and partner states while this
-                // chunk computes; incidence two chunks ahead in registers
-                ent_next = ent_nn;
-                if (kb + 32 + lane < k1) {
-                    const uint32_t c2 = ent_next.x & INC_CMASK, p2 = ent_next.y;
-                    pf_l1(&geo[c2]); pf_l1(&row[c2]); pf_l1(&Pa_in[c2]); pf_l1(&Pb_in[c2]);
-                    if (!(p2 & PARTNER_EXT)) {
-                        const int64_t pl = (int64_t)p2 - p0;
-                        if (pl < 0 || pl >= np) { pf_l1(&vin[p2]); pf_l1(&win[p2]); }
-                    }
-                }
-                if (kb + 64 + lane < k1) ent_nn = inc[kb + 64 + lane];
-            } else if (kb + 32 + lane < k1) ent_next = inc[kb + 32 + lane];     // prefetch the next chunk
-            // segment starts of this chunk (nonempty particles whose CSR range starts here)
-            const bool starts = e_me > s_me && s_me >= kb && s_me < kb + 32;
-            const unsigned smask = __reduce_or_sync(0xffffffffu, starts ? (1u << (s_me - kb)) : 0u);
-            if (starts) sOwn[w][s_me - kb] = (uint8_t)lane;
-            __syncwarp();
-            const unsigned le = smask & (0xffffffffu >> (31 - lane));
-            const int sstart = le ? 31 - __clz(le) : 0;
-            const int owner = le ? (int)sOwn[w][sstart] : carry;
-            double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
-            if (valid) {
-                const int o = lo_p + owner;
-                const uint32_t c = ent.x & INC_CMASK;
-                const bool isB = (ent.x & B_SIDE) != 0;
-                const uint32_t p = ent.y;
-                const double4 *pPV, *pPW;
-                double mt;
-                if (!(p & PARTNER_EXT)) {
-                    const int64_t pl = EXP == 3 ? (int64_t)(p & (TP - 1)) : (int64_t)p - p0;
-                    if (pl >= 0 && pl < np) { pPV = &sV[pl]; pPW = &sW[pl]; }
-                    else { pPV = &vin[p]; pPW = &win[p]; }
-                    mt = sp.mu_t;
-                } else {
-                    d3 bv;
-                    boundary_vel(p, bnd, bv, mt);
-                    sExt[t] = make_double4(bv.x, bv.y, bv.z, 0.0);
-                    pPV = &sExt[t];
-                    pPW = &sZero;
-                }
-                const double4 *pSV = &sV[o], *pSW = &sW[o];
-                G4 gc;
-                R4 rc;
-                P4 pac, pbc;
-                if (EXP >= 2) {
-                    gc = mkG4(0.6, 0.0, 0.8, 1e-4 + 1e-12 * c);
-                    rc = mkR4(1e5, 1e-3, 1e-3, 1e-3);
-                    pac = mkP4(1e-6, 0, 0, 0);
-                    pbc = mkP4(0, 0, 0, 0);
-                } else {
-                    gc = geo[c]; rc = row[c]; pac = Pa_in[c]; pbc = Pb_in[c];
-                }
-                const HalfOut r = EXP == 1 ? fake_half(*(isB ? pPV : pSV), *(isB ? pPW : pSW), *(isB ? pSV : pPV),
-                                                       *(isB ? pSW : pPW), gc, rc, pac, pbc)
-                                           : half_contact(*(isB ? pPV : pSV), *(isB ? pPW : pSW), *(isB ? pSV : pPV),
-                                               *(isB ? pSW : pPW), isB, mt, gc, rc, pac, pbc,
-                                               sp.rolling_dims);
-                if (!isB) {
-                    Pa_out[c] = r.Pa;
-                    Pb_out[c] = r.Pb;
-                }
-                v0 = r.dL.x; v1 = r.dL.y; v2 = r.dL.z; v3 = r.dA.x; v4 = r.dA.y; v5 = r.dA.z;
-            }
-            // segmented inclusive scan, depth = longest segment of this chunk
-            const int dist = valid ? lane - sstart : 0;
-            const int maxd = __reduce_max_sync(0xffffffffu, dist);
-            for (int d = 1; d <= maxd; d <<= 1) {
-                const double u0 = __shfl_up_sync(0xffffffffu, v0, d), u1 = __shfl_up_sync(0xffffffffu, v1, d);
-                const double u2 = __shfl_up_sync(0xffffffffu, v2, d), u3 = __shfl_up_sync(0xffffffffu, v3, d);
-                const double u4 = __shfl_up_sync(0xffffffffu, v4, d), u5 = __shfl_up_sync(0xffffffffu, v5, d);
-                if (lane - d >= sstart) { v0 += u0; v1 += u1; v2 += u2; v3 += u3; v4 += u4; v5 += u5; }
-            }
-            const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1);
-            if (seg_end) {
-                sAcc[w][0][owner] += v0; sAcc[w][1][owner] += v1; sAcc[w][2][owner] += v2;
-                sAcc[w][3][owner] += v3; sAcc[w][4][owner] += v4; sAcc[w][5][owner] += v5;
-            }
-            carry = __shfl_sync(0xffffffffu, owner, 31);
-            __syncwarp();
-        }
-    }
-    if (me < hi_p) {
-        // body update with the real masses (1/m = (c/m)/c): the mass-splitting average
-        double4 V = sV[me], W = sW[me];
-        const uint32_t cnt = e_me - s_me;
-        if (cnt) {
-            const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
-            V.x += im * sAcc[w][0][lane]; V.y += im * sAcc[w][1][lane]; V.z += im * sAcc[w][2][lane];
-            W.x += iI * sAcc[w][3][lane]; W.y += iI * sAcc[w][4][lane]; W.z += iI * sAcc[w][5][lane];
-        }
-        vout[p0 + me] = V;
-        wout[p0 + me] = W;
-    }
-}
-
-// ------------------------------------------------------------------ pipelined tile sweep
-// Same work split and reduction as k_sweep_tile, plus a 2-stage cp.async pipeline: while a
-// warp computes chunk i it has chunk i+1's contact records (geo, row, P) and partner states in
-// flight into a warp-private shared-memory stage (LDGSTS, L2-only), and chunk i+2's incidence
-// entries in registers.  Load latency is then hidden by the warp's own computation instead of
-// by occupancy.
-__device__ __forceinline__ void cp16(void *smem, const void *gmem)
-{
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
-template <class T>
-__device__ __forceinline__ void cpT(T *smem, const T *gmem)
-{
-    static_assert(sizeof(T) % 16 == 0, "16-byte granules");
-#pragma unroll
-    for (int q = 0; q < (int)(sizeof(T) / 16); q++) cp16((char *)smem + 16 * q, (const char *)gmem + 16 * q);
-}
-
-struct Stage {                      // one chunk of one warp (SoA: conflict-free per-lane access)
-    G4 geo[32];
-    R4 row[32];
-    P4 pa[32], pb[32];
-    double4 vp[32], wp[32];
-};
-constexpr int TPP = 128;
-constexpr int NWP = TPP / 32;
-struct PipeSmem {
-    Stage st[NWP][2];
-    double4 sV[TPP], sW[TPP];
-    double sAcc[NWP][6][32];
-    uint32_t sI[TPP + 1];
-    uint8_t sOwn[NWP][32];
-};
-size_t sweep_pipe_smem() { return sizeof(PipeSmem); }
-
-__device__ __forceinline__ void issue_stage(Stage &S, int lane, bool valid, uint2 ent, const G4 *__restrict__ geo,
-                                            const R4 *__restrict__ row, const P4 *__restrict__ Pa,
-                                            const P4 *__restrict__ Pb, const double4 *__restrict__ vin,
-                                            const double4 *__restrict__ win)
-{
-    if (!valid) return;
-    const uint32_t c = ent.x & INC_CMASK, p = ent.y;
-    cpT(&S.geo[lane], &geo[c]);
-    cpT(&S.row[lane], &row[c]);
-    cpT(&S.pa[lane], &Pa[c]);
-    cpT(&S.pb[lane], &Pb[c]);
-    if (!(p & PARTNER_EXT)) {
-        cpT(&S.vp[lane], &vin[p]);
-        cpT(&S.wp[lane], &win[p]);
-    }
-}
-
-__global__ void __launch_bounds__(TPP, SWEEP_MINB_PIPE) k_sweep_pipe(int64_t N, const double4 *__restrict__ vin,
-                                                      const double4 *__restrict__ win, double4 *__restrict__ vout,
-                                                      double4 *__restrict__ wout, const uint32_t *__restrict__ inc_start,
-                                                      const uint2 *__restrict__ inc, const G4 *__restrict__ geo,
-                                                      const R4 *__restrict__ row, const P4 *__restrict__ Pa_in,
-                                                      const P4 *__restrict__ Pb_in, P4 *__restrict__ Pa_out,
-                                                      P4 *__restrict__ Pb_out, const DevBoundary *__restrict__ bnd,
-                                                      SolveParams sp)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    PipeSmem &sm = *reinterpret_cast<PipeSmem *>(smem_raw);
-    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    const int64_t p0 = (int64_t)blockIdx.x * TPP;
-    const int np = (int)min((int64_t)TPP, N - p0);
-    if (t < np) {
-        sm.sV[t] = vin[p0 + t];
-        sm.sW[t] = win[p0 + t];
-    }
-    for (int q = t; q <= np; q += TPP) sm.sI[q] = inc_start[p0 + q];
-#pragma unroll
-    for (int f = 0; f < 6; f++) sm.sAcc[w][f][lane] = 0.0;
-    __syncthreads();
-    const int lo_p = 32 * w, hi_p = min(32 * w + 32, np);
-    const int me = lo_p + lane;
-    const uint32_t s_me = me < hi_p ? sm.sI[me] : 0u, e_me = me < hi_p ? sm.sI[me + 1] : 0u;
-    if (lo_p < np) {
-        const uint32_t k0 = sm.sI[lo_p], k1 = sm.sI[hi_p];
-        uint2 entA = make_uint2(0, 0), entB = make_uint2(0, 0);
-        if (k0 + lane < k1) entA = inc[k0 + lane];
-        if (k0 + 32 + lane < k1) entB = inc[k0 + 32 + lane];
-        issue_stage(sm.st[w][0], lane, k0 + lane < k1, entA, geo, row, Pa_in, Pb_in, vin, win);
-        cp_commit();
-        int carry = 0;
-        int sidx = 0;
-        for (uint32_t kb = k0; kb < k1; kb += 32) {
-            const uint32_t k = kb + lane;
-            const bool valid = k < k1;
-            // stage chunk i+1, prefetch the incidence of chunk i+2
-            issue_stage(sm.st[w][sidx ^ 1], lane, kb + 32 + lane < k1, entB, geo, row, Pa_in, Pb_in, vin, win);
-            cp_commit();
-            uint2 entC = make_uint2(0, 0);
-            if (kb + 64 + lane < k1) entC = inc[kb + 64 + lane];
-            // owners of this chunk's lanes from the segment-start bitmask
-            const bool starts = e_me > s_me && s_me >= kb && s_me < kb + 32;
-            const unsigned smask = __reduce_or_sync(0xffffffffu, starts ? (1u << (s_me - kb)) : 0u);
-            if (starts) sm.sOwn[w][s_me - kb] = (uint8_t)lane;
-            cp_wait1();
-            __syncwarp();
-            const unsigned le = smask & (0xffffffffu >> (31 - lane));
-            const int sstart = le ? 31 - __clz(le) : 0;
-            const int owner = le ? (int)sm.sOwn[w][sstart] : carry;
-            double v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
-            if (valid) {
-                Stage &S = sm.st[w][sidx];
-                const int o = lo_p + owner;
-                const bool isB = (entA.x & B_SIDE) != 0;
-                const uint32_t p = entA.y;
-                double mt;
-                double4 VP, WP;
-                if (!(p & PARTNER_EXT)) {
-                    VP = S.vp[lane];
-                    WP = S.wp[lane];
-                    mt = sp.mu_t;
-                } else {
-                    d3 bv;
-                    boundary_vel(p, bnd, bv, mt);
-                    VP = make_double4(bv.x, bv.y, bv.z, 0.0);
-                    WP = make_double4(0.0, 0.0, 0.0, 0.0);
-                }
-                const double4 VS = sm.sV[o], WS = sm.sW[o];
-                const HalfOut r = half_contact(isB ? VP : VS, isB ? WP : WS, isB ? VS : VP, isB ? WS : WP, isB, mt,
-                                               S.geo[lane], S.row[lane], S.pa[lane], S.pb[lane], sp.rolling_dims);
-                if (!isB) {
-                    const uint32_t c = entA.x & INC_CMASK;
-                    Pa_out[c] = r.Pa;
-                    Pb_out[c] = r.Pb;
-                }
-                v0 = r.dL.x; v1 = r.dL.y; v2 = r.dL.z; v3 = r.dA.x; v4 = r.dA.y; v5 = r.dA.z;
-            }
-            const int dist = valid ? lane - sstart : 0;
-            const int maxd = __reduce_max_sync(0xffffffffu, dist);
-            for (int d = 1; d <= maxd; d <<= 1) {
-                const double u0 = __shfl_up_sync(0xffffffffu, v0, d), u1 = __shfl_up_sync(0xffffffffu, v1, d);
-                const double u2 = __shfl_up_sync(0xffffffffu, v2, d), u3 = __shfl_up_sync(0xffffffffu, v3, d);
-                const double u4 = __shfl_up_sync(0xffffffffu, v4, d), u5 = __shfl_up_sync(0xffffffffu, v5, d);
-                if (lane - d >= sstart) { v0 += u0; v1 += u1; v2 += u2; v3 += u3; v4 += u4; v5 += u5; }
-            }
-            const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1);
-            if (seg_end) {
-                sm.sAcc[w][0][owner] += v0; sm.sAcc[w][1][owner] += v1; sm.sAcc[w][2][owner] += v2;
-                sm.sAcc[w][3][owner] += v3; sm.sAcc[w][4][owner] += v4; sm.sAcc[w][5][owner] += v5;
-            }
-            carry = __shfl_sync(0xffffffffu, owner, 31);
-            entA = entB;
-            entB = entC;
-            sidx ^= 1;
-            __syncwarp();
-        }
-    }
-    if (me < hi_p) {
-        double4 V = sm.sV[me], W = sm.sW[me];
-        const uint32_t cnt = e_me - s_me;
-        if (cnt) {
-            const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
-            V.x += im * sm.sAcc[w][0][lane]; V.y += im * sm.sAcc[w][1][lane]; V.z += im * sm.sAcc[w][2][lane];
-            W.x += iI * sm.sAcc[w][3][lane]; W.y += iI * sm.sAcc[w][4][lane]; W.z += iI * sm.sAcc[w][5][lane];
-        }
-        vout[p0 + me] = V;
-        wout[p0 + me] = W;
-    }
-}
-
-// ------------------------------------------------------------------ particle-per-thread sweep
-// One thread per particle walks its own CSR list: contributions accumulate in registers in CSR
-// order (deterministic, no reduction step, no owner search).  Divergence from unequal contact
-// counts is removed by k_tile_order, which sorts the particles of every 128-tile by count once
-// per step, so a warp's lanes have (nearly) equal trip counts.
-constexpr int TPT = 128;
-
-__global__ void k_tile_order(int64_t N, const uint32_t *__restrict__ inc_start, uint32_t *__restrict__ order)
-{
-    __shared__ uint32_t key[TPT];
-    const int t = threadIdx.x;
-    const int64_t p0 = (int64_t)blockIdx.x * TPT;
-    const int np = (int)min((int64_t)TPT, N - p0);
-    // key = (count << 8) | local index, descending count; padding sorts last
-    key[t] = t < np ? (((inc_start[p0 + t + 1] - inc_start[p0 + t]) << 8) | (uint32_t)t) : 0u;
-    __syncthreads();
-    for (int k = 2; k <= TPT; k <<= 1)           // bitonic sort, descending
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            const int ix = t ^ j;
-            if (ix > t) {
-                const uint32_t a = key[t], b = key[ix];
-                const bool desc = (t & k) == 0;
-                if (desc ? (a < b) : (a > b)) { key[t] = b; key[ix] = a; }
-            }
-            __syncthreads();
-        }
-    if (t < np) order[p0 + t] = (uint32_t)(p0 + (key[t] & 0xFF));
-}
-
-__global__ void __launch_bounds__(TPT, SWEEP_MINB_PPT) k_sweep_ppt(int64_t N, const uint32_t *__restrict__ order,
-                                                      const double4 *__restrict__ vin, const double4 *__restrict__ win,
-                                                      double4 *__restrict__ vout, double4 *__restrict__ wout,
-                                                      const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
-                                                      const G4 *__restrict__ geo, const R4 *__restrict__ row,
-                                                      const P4 *__restrict__ Pa_in, const P4 *__restrict__ Pb_in,
-                                                      P4 *__restrict__ Pa_out, P4 *__restrict__ Pb_out,
-                                                      const DevBoundary *__restrict__ bnd, SolveParams sp)
-{
-    const int64_t tid = (int64_t)blockIdx.x * TPT + threadIdx.x;
-    if (tid >= N) return;
-    const uint32_t i = order[tid];
-    const uint32_t s = inc_start[i], e = inc_start[i + 1];
-    const double4 V = vin[i], W = win[i];
-    double a0 = 0, a1 = 0, a2 = 0, a3 = 0, a4 = 0, a5 = 0;
-    uint2 ent_next = s < e ? inc[s] : make_uint2(0, 0);
-    for (uint32_t k = s; k < e; k++) {
-        const uint2 ent = ent_next;
-        if (k + 1 < e) ent_next = inc[k + 1];
-        const uint32_t c = ent.x & INC_CMASK;
-        const bool isB = (ent.x & B_SIDE) != 0;
-        const uint32_t p = ent.y;
-        double4 VP, WP;
-        double mt;
-        if (!(p & PARTNER_EXT)) {
-            VP = vin[p];
-            WP = win[p];
-            mt = sp.mu_t;
-        } else {
-            d3 bv;
-            boundary_vel(p, bnd, bv, mt);
-            VP = make_double4(bv.x, bv.y, bv.z, 0.0);
-            WP = make_double4(0.0, 0.0, 0.0, 0.0);
-        }
-        const HalfOut r = half_contact(isB ? VP : V, isB ? WP : W, isB ? V : VP, isB ? W : WP, isB, mt, geo[c], row[c],
-                                       Pa_in[c], Pb_in[c], sp.rolling_dims);
-        if (!isB) {
-            Pa_out[c] = r.Pa;
-            Pb_out[c] = r.Pb;
-        }
-        a0 += r.dL.x; a1 += r.dL.y; a2 += r.dL.z; a3 += r.dA.x; a4 += r.dA.y; a5 += r.dA.z;
-    }
-    double4 Vn = V, Wn = W;
-    const uint32_t cnt = e - s;
-    if (cnt) {
-        const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
-        Vn.x += im * a0; Vn.y += im * a1; Vn.z += im * a2;
-        Wn.x += iI * a3; Wn.y += iI * a4; Wn.z += iI * a5;
-    }
-    vout[i] = Vn;
-    wout[i] = Wn;
-}
-
-static thread_local int g_sweep_variant = SWEEP_KERNEL;   // per host thread: contexts may step concurrently
-void set_sweep_variant(int v) { g_sweep_variant = v; }
-bool sweep_uses_order() { return g_sweep_variant == 2; }
-void launch_tile_order(int64_t N, const uint32_t *inc_start, uint32_t *order, cudaStream_t s)
-{ if (N) k_tile_order<<<(unsigned)((N + TPT - 1) / TPT), TPT, 0, s>>>(N, inc_start, order); }
 
 // gravity + warm start (MODE_APPLY) or force/torque (MODE_FORCES, O6)
 template <int MODE>
@@ -710,7 +270,6 @@ __global__ void k_plate_flag(int64_t nc, const uint8_t *__restrict__ own, const 
 }
 // the impulse the plate received over a sweep: sum of (P_n n + P_t)(out) - (...)(in), int64 fixed
 // point (exact, order-free); in == nullptr: the whole impulse of `out` (the warm start)
-template <bool P8L>
 __global__ void k_plate_hub(int64_t n, const uint32_t *__restrict__ list, const uint2 *__restrict__ cij,
                             const G4 *__restrict__ geo, const void *__restrict__ pin, const void *__restrict__ pout,
                             unsigned long long *__restrict__ acc)
@@ -720,9 +279,9 @@ __global__ void k_plate_hub(int64_t n, const uint32_t *__restrict__ list, const 
     const uint32_t c = list[t];
     const int q = (cij[c].y >> 4) & 0xF;
     const G4 g = geo[c];
-    const P4 o = P8L ? ((const P8 *)pout)[c].a : ((const P4 *)pout)[c];
+    const P4 o = ((const P4 *)pout)[c];
     P4 i = mkP4(0, 0, 0, 0);
-    if (pin) i = P8L ? ((const P8 *)pin)[c].a : ((const P4 *)pin)[c];
+    if (pin) i = ((const P4 *)pin)[c];
     const double dPn = (double)o.x - (double)i.x;
     const double d[3] = {dPn * g.x + ((double)o.y - (double)i.y), dPn * g.y + ((double)o.z - (double)i.z),
                          dPn * g.z + ((double)o.w - (double)i.w)};
@@ -743,12 +302,11 @@ __global__ void k_plate_kick(DevBoundary *bnd, unsigned long long *acc, double h
 #define PGRID(n) (unsigned)(((n) + 255) / 256), 256, 0, s
 void launch_plate_list_flags(int64_t nc, const uint8_t *own, const uint2 *cij, uint32_t *flag, cudaStream_t s)
 { if (nc) k_plate_flag<<<PGRID(nc)>>>(nc, own, cij, flag); }
-void launch_plate_hub(bool p8, int64_t n, const uint32_t *list, const uint2 *cij, const G4 *geo, const void *pin,
+void launch_plate_hub(int64_t n, const uint32_t *list, const uint2 *cij, const G4 *geo, const void *pin,
                       const void *pout, unsigned long long *acc, cudaStream_t s)
 {
     if (!n) return;
-    if (p8) k_plate_hub<true><<<PGRID(n)>>>(n, list, cij, geo, pin, pout, acc);
-    else k_plate_hub<false><<<PGRID(n)>>>(n, list, cij, geo, pin, pout, acc);
+    k_plate_hub<<<PGRID(n)>>>(n, list, cij, geo, pin, pout, acc);
 }
 void launch_plate_kick(DevBoundary *bnd, unsigned long long *acc, double h, int first, cudaStream_t s)
 { k_plate_kick<<<1, 32, 0, s>>>(bnd, acc, h, first); }
@@ -885,45 +443,16 @@ void launch_rows(int64_t nc, int mode, const uint2 *cij, const G4 *geo, const do
                  const double4 *vel, const double4 *pos, const DevBoundary *bnd, const SolveParams &sp, StepScalars *sc,
                  cudaStream_t s)
 { if (nc) k_rows<<<GRID(nc)>>>(nc, mode, cij, geo, cdel, row, row_imp, vel, pos, bnd, sp, sc); }
-void launch_sweep(int mode, int64_t N, const uint32_t *order, const double4 *vin, const double4 *win, double4 *vout,
-                  double4 *wout, const uint32_t *inc_start, const uint2 *inc, const PackedInc *pk, const G4 *geo,
-                  const R4 *row,
-                  const P4 *Pa_in, const P4 *Pb_in, P4 *Pa_out, P4 *Pb_out,
-                  const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s)
+// gravity + warm start (MODE_APPLY) or per-particle contact force/torque (MODE_FORCES)
+void launch_apply(int mode, int64_t N, const double4 *vin, const double4 *win, double4 *vout, double4 *wout,
+                  const uint32_t *inc_start, const uint2 *inc, const G4 *geo, const R4 *row, const P4 *Pa,
+                  const P4 *Pb, const SolveParams &sp, cudaStream_t s)
 {
     if (!N) return;
-    if (mode == SWEEP_MODE_SWEEP && g_sweep_variant == 2) {
-        k_sweep_ppt<<<(unsigned)((N + TPT - 1) / TPT), TPT, 0, s>>>(N, order, vin, win, vout, wout, inc_start, inc, geo,
-                                                                    row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
-    } else if (mode == SWEEP_MODE_SWEEP && g_sweep_variant == 1) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_sweep_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PipeSmem));
-            attr = true;
-        }
-        k_sweep_pipe<<<(unsigned)((N + TPP - 1) / TPP), TPP, sizeof(PipeSmem), s>>>(
-            N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
-    } else if (mode == SWEEP_MODE_SWEEP && (g_sweep_variant == 0 || g_sweep_variant == 7 || g_sweep_variant == 8 ||
-                                            g_sweep_variant == 9 || g_sweep_variant == 44 || g_sweep_variant == 45)) {
-        // 0: the context's reduction (packed canonical if pk, else contiguous); 7: contiguous;
-        // 8: packed with contact-indexed normals/rows (diagnostic; pk->geo/row set by the caller)
-        g_t2_rows_by_contact = g_sweep_variant == 8;
-        g_t2_stage = g_sweep_variant == 9;
-        g_t2_exp = g_sweep_variant == 44 ? 1 : (g_sweep_variant == 45 ? 2 : 0);
-        launch_sweep_t2(N, vin, win, vout, wout, inc_start, inc, g_sweep_variant == 7 ? nullptr : pk, geo, row, Pa_in,
-                        Pb_in, Pa_out, Pb_out, bnd, sp, s);
-        g_t2_rows_by_contact = false;
-        g_t2_stage = false;
-        g_t2_exp = 0;
-    }
-    else if (mode == SWEEP_MODE_SWEEP)
-        (g_sweep_variant == 3 ? k_sweep_tile<true> : g_sweep_variant == 41 ? k_sweep_tile<false, 1> :
-         g_sweep_variant == 42 ? k_sweep_tile<false, 2> : g_sweep_variant == 43 ? k_sweep_tile<false, 3> : k_sweep_tile<false>)<<<(unsigned)((N + TP - 1) / TP), TP, 0, s>>>(N, vin, win, vout, wout, inc_start, inc, geo, row,
-                                                                  Pa_in, Pb_in, Pa_out, Pb_out, bnd, sp);
-    else if (mode == SWEEP_MODE_APPLY)
-        k_apply<SWEEP_MODE_APPLY><<<GRID(N)>>>(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, sp);
+    if (mode == SWEEP_MODE_APPLY)
+        k_apply<SWEEP_MODE_APPLY><<<GRID(N)>>>(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa, Pb, sp);
     else
-        k_apply<SWEEP_MODE_FORCES><<<GRID(N)>>>(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa_in, Pb_in, sp);
+        k_apply<SWEEP_MODE_FORCES><<<GRID(N)>>>(N, vin, win, vout, wout, inc_start, inc, geo, row, Pa, Pb, sp);
 }
 void launch_integrate(int64_t N, const uint8_t *own, double4 *pos, const double4 *vel, const double4 *ang, const double4 *xref, double h,
                       double rho, double *ke_part, StepScalars *sc, cudaStream_t s)

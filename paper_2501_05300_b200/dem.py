@@ -127,7 +127,7 @@ CONTACT_DTYPE = np.dtype([("key", "<u8"), ("n", "<f8", (3,)), ("delta", "<f8"), 
 EXPORTS = ["dem_create_bed", "dem_step", "dem_set_solver", "dem_get_state", "dem_set_state", "dem_get_contacts", "dem_get_forces",
            "dem_add_plate", "dem_drive_plate", "dem_get_plate", "dem_drive_wall", "dem_get_wall", "dem_set_timing",
            "dem_get_timing", "dem_rebalance", "dem_add_particles", "dem_remove_particles",
-           "dem_reset_timing", "dem_bench_sweeps", "dem_num_particles", "dem_num_local", "dem_nccl_unique_id",
+           "dem_reset_timing", "dem_bench_sweeps", "dem_drive_upload_bytes", "dem_num_particles", "dem_num_local", "dem_nccl_unique_id",
            "dem_loopback_create", "dem_loopback_destroy", "dem_generator_count", "dem_stream", "dem_destroy", "dem_last_error", "dem_profile_diameter",
            "dem_contact_network_length", "dem_plan_iterations", "dem_plan_timestep"]
 
@@ -164,6 +164,9 @@ def lib():
         L.dem_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.dem_reset_timing.argtypes = [vp]
         L.dem_bench_sweeps.argtypes = [vp, i32, i32, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        if hasattr(L, "dem_drive_upload_bytes"):      # (diagnostic builds of older libraries lack it)
+            L.dem_drive_upload_bytes.argtypes = []
+            L.dem_drive_upload_bytes.restype = C.c_int64
         L.dem_num_particles.argtypes = [vp]
         L.dem_num_particles.restype = C.c_int64
         L.dem_num_local.argtypes = [vp]
@@ -215,6 +218,11 @@ def plan_timestep(d, eps, rho, sigma):
 
 
 # ---------------------------------------------------------------- x-slab decomposition plumbing
+def boundary_upload_bytes():
+    """bytes one dem_drive_wall / dem_drive_plate call copies host -> device (dem_drive_upload_bytes)"""
+    return int(lib().dem_drive_upload_bytes())
+
+
 def nccl_unique_id():
     """A fresh ncclUniqueId (128 bytes) for rank 0 to broadcast (torch.distributed)."""
     buf = (C.c_ubyte * 128)()
@@ -452,6 +460,17 @@ class Bed:
         int32 with cap >= n_owned; fills the first n_owned rows (gid order) and returns n_owned."""
         cap = min(int(t.shape[0]) for t in out.values())
         v = StateView(cap, *(out[k].data_ptr() if k in out else None for k in ("pos", "vel", "angvel", "radius", "gid")), 1, 0)
+        self._check(lib().dem_get_state(self._h, C.byref(v)))
+        return int(v.n)
+
+    def get_state_into(self, out):
+        """Host variant of get_state_device: out = dict of caller-owned HOST arrays (numpy, or torch
+        CPU tensors, e.g. pinned) pos/vel/angvel (cap,3) f64 and optionally radius (cap,) f64, gid
+        (cap,) u32 with cap >= n_owned; dem_get_state copies into them.  Returns n_owned."""
+        def addr(t):
+            return t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+        cap = min(int(t.shape[0]) for t in out.values())
+        v = StateView(cap, *(addr(out[k]) if k in out else None for k in ("pos", "vel", "angvel", "radius", "gid")), 0, 0)
         self._check(lib().dem_get_state(self._h, C.byref(v)))
         return int(v.n)
 

@@ -43,3 +43,30 @@ def test_workload_iteration_counts():
     assert dem.plan_iterations(bench.workload_network_length(w2), 0.02) == 186
     assert dem.plan_iterations(bench.workload_network_length(bench.WORKLOADS["config3-count"]), 0.02) == 375
     assert bench.workload_levels(w2) == 3 and bench.workload_levels(bench.WORKLOADS["config4-geom"]) == 3
+
+
+def test_gpus_flag_relaunches_one_rank_per_gpu():
+    """VERDICT r1 / ADVICE: `bench.py --gpus N` without torchrun re-executes itself under
+    torch.distributed.run with N ranks (127.0.0.1 rendezvous); a WORLD_SIZE that disagrees with
+    --gpus is refused.  Exercised on CPU through the reference arm (rank 0 alone prints)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.torchrun_argv(1, ["--gpus", "1"], 29500) is None
+    argv = bench.torchrun_argv(4, ["--gpus", "4", "--steps", "2"], 29511)
+    assert argv[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in argv and "--master-port=29511" in argv
+    assert argv[argv.index("--master-addr") + 1] == "127.0.0.1"
+    assert argv[-4:] == ["--gpus", "4", "--steps", "2"] and argv[-5].endswith("bench.py")
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                          "--steps", "1", "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT,
+                         env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    assert json.loads(lines[0])["n_gpus"] == 2
+    env["WORLD_SIZE"] = "2"
+    bad = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "1"], capture_output=True,
+                         text=True, timeout=120, cwd=ROOT, env=env)
+    assert bad.returncode != 0 and "WORLD_SIZE=2" in (bad.stderr + bad.stdout)
