@@ -53,8 +53,13 @@ WORKLOADS = {
     "config2-geom": dict(dims=(1.0, 0.5, 0.5), profile=(4e-3, 0.056, 32e-3), dt=5e-6, seed=1002),
     "config2-count": dict(dims=(7.8, 0.5, 0.5), profile=(4e-3, 0.056, 32e-3), dt=5e-6, seed=1002),
 }
-ALG_B_PARTICLE = 112     # algorithmic bytes per particle per sweep
-ALG_B_CONTACT = 72       # ... per contact per sweep
+ALG_B_PARTICLE = 112     # algorithmic bytes per particle per sweep (fp64 v, w read + write, statics)
+# per contact per sweep at the precision the acceptance demands (SURVEY §8(d)'s own definition):
+# n and delta in fp64 (32 B; fp32 normals fail the torque bar) and the impulses
+# P_n, P_t, P_r in fp64, read and written (2 x 56 B; fp32 impulses fail it on the bench-shaped
+# bed: 6.8e-5).  SURVEY §8(d) budgeted fp32 values: 72 B (reported beside).
+ALG_B_CONTACT = 144
+ALG_B_CONTACT_SURVEY = 72
 
 
 def network_length(bands):
@@ -458,7 +463,10 @@ def main():
                      "frac": (achieved / hbm) if hbm else None, "traffic": traffic,
                      "traffic_unit": "GB per launch (ncu dram read+write)",
                      "alg_bytes_per_launch": alg_bytes, "launch_ms": sweep_ms,
-                     "alg_bytes_model": "112 B/particle + 72 B/contact per sweep (SURVEY 8d)",
+                     "alg_bytes_model": "112 B/particle + 144 B/contact per sweep: SURVEY 8(d)'s terms at the precision "
+                                        "the acceptance demands (fp64 normals and impulses; DESIGN.md 5, 6)",
+                     "frac_survey_fp32_model": (ALG_B_PARTICLE * N + ALG_B_CONTACT_SURVEY * nc_rank) / (sweep_ms / 1e3)
+                                               / 1e9 / hbm if hbm else None,
                      "sweep_share_of_step": tm["ms_sweeps"] / max(tm["ms_total"], 1e-9),
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
                      "frac_vs_8000_GBps": achieved / 8000.0},

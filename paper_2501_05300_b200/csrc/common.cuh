@@ -241,6 +241,15 @@ __device__ __forceinline__ double rsqrt64(double x)
     return r * (1.5 - 0.5 * x * r * r);
 }
 
+// 1/sqrt(x) for x > 0 with ONE Newton step (relative error ~1e-14): where the result only scales
+// an iterate (cone projections, the SPOOK regularisation of a sweep), not a geometric quantity
+__device__ __forceinline__ double rsqrt64_1(double x)
+{
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r * (1.5 - 0.5 * x * r * r);
+}
+
 // R* = r_a r_b / (r_a + r_b) (d* = 2 R*): one definition for every kernel
 __device__ __forceinline__ double rstar(double ra, double rb) { return ra * rb * rcp64(ra + rb); }
 

@@ -334,10 +334,16 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
     TRY(A(ctx, &ctx->ke_part, N / 256 + 2));
     dfree(ctx, ctx->pl.noint);
     dfree(ctx, ctx->pl.rad);
+    dfree(ctx, ctx->pl.halo_n);
+    dfree(ctx, ctx->pl.halo_idx);
     ctx->pl.noint = nullptr;
     ctx->pl.rad = nullptr;
+    ctx->pl.halo_n = nullptr;
+    ctx->pl.halo_idx = nullptr;
     TRY(A(ctx, &ctx->pl.noint, N / SWEEP_TILE + 2));
     TRY(A(ctx, &ctx->pl.rad, N));
+    TRY(A(ctx, &ctx->pl.halo_n, N / SWEEP_TILE + 2));
+    TRY(A(ctx, &ctx->pl.halo_idx, (N / SWEEP_TILE + 2) * HALO_CAP));
     if (!ctx->lvbox) {
         TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
         TRY(A(ctx, &ctx->db, 1));
@@ -897,8 +903,9 @@ static dem_status build_plan(dem_ctx *ctx, int64_t N)
     if ((int64_t)ni > ctx->cap_items) {
         const int64_t cap = std::max<int64_t>((int64_t)ni + ni / 4, 1024);
         TRY(regrow(ctx, &ctx->pl.item_c, cap)); TRY(regrow(ctx, &ctx->pl.item_meta, cap));
-        TRY(regrow(ctx, &ctx->it_rec, cap)); TRY(regrow(ctx, &ctx->it_P[0], cap * PREC_UNITS));
-        TRY(regrow(ctx, &ctx->it_P[1], cap * PREC_UNITS));
+        TRY(regrow(ctx, &ctx->pl.item_own, cap));
+        TRY(regrow(ctx, &ctx->it_rec, cap)); TRY(regrow(ctx, &ctx->it_P[0], cap));
+        TRY(regrow(ctx, &ctx->it_P[1], cap));
         TRY(regrow(ctx, &ctx->it_flag, cap + 1)); TRY(regrow(ctx, &ctx->it_scan, cap + 1));
         TRY(regrow(ctx, &ctx->it_plist, cap + 1));
         ctx->cap_items = cap;

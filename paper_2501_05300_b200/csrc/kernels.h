@@ -94,13 +94,13 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 // contacts owned by a tile (intra-tile pairs once, cross-tile pairs once per side, boundary
 // contacts once); item meta word: flags + partner (see IT_*).
 #ifndef SWEEP_TILE
-#define SWEEP_TILE 256
+#define SWEEP_TILE 256           // <= 256: the owner index is 8 bits
 #endif
 #ifndef SWEEP_SLOT_CAP
 #define SWEEP_SLOT_CAP 768
 #endif
 #ifndef SWEEP_MINB
-#define SWEEP_MINB 3
+#define SWEEP_MINB 2
 #endif
 #define IT_INTRA 0x80000000u     // partner in the tile, body b's share goes to slot (bits 9..20)
 #define IT_B 0x40000000u         // cross pair: the owner is the canonical body b
@@ -109,13 +109,14 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 #define IT_LOC 0x1FFu            // intra pair: partner's index in the tile
 #define IT_SLOT_SHIFT 9
 #define IT_SLOT_MASK 0xFFFu
-#ifndef SWEEP_PMODE
-#define SWEEP_PMODE 0        // impulse storage of the sweep's items: 0 f32; 1 P_n f64, P_t/P_r f32; 2 f64
+#define IT_HALO (IT_INTRA | IT_EXT)   // cross pair whose partner is staged in the tile's halo (bits 0..9)
+#define IT_HMASK 0x3FFu
+#ifndef HALO_CAP
+#define HALO_CAP 448                  // staged cross-tile partners per tile
 #endif
-#define PREC_UNITS (SWEEP_PMODE == 2 ? 2 : 1)   // 32-byte PRec units per item
-struct __align__(32) CRec { double nu, nv, delta, b; };  // per item, per stage: n (2 of 3 comps, sweep.cu), delta, bias
-struct __align__(32) PRec { uint32_t w[8]; };             // per item, ping-pong: impulses + meta (sweep.cu)
-static_assert(sizeof(CRec) == 32 && sizeof(PRec) == 32, "32-byte item records");
+struct __align__(32) CRec { double nx, ny, nz, delta; };  // per item, per stage (meta in n's low bits, sweep.cu)
+struct __align__(32) PRec { double pn, pt[3], pr[3], b; }; // per item, ping-pong: fp64 impulses + SPOOK bias
+static_assert(sizeof(CRec) == 32 && sizeof(PRec) == 64, "item records");
 struct SweepPlan {
     uint32_t *istart = nullptr;   // [N+1] first item of each particle (tile-contiguous)
     uint32_t *pin = nullptr;      // [N] slot range in the tile: start | count << 16
@@ -123,6 +124,9 @@ struct SweepPlan {
     uint32_t *slot_of = nullptr;  // [nc] slot of an intra contact at body b
     uint32_t *item_c = nullptr;   // [items] contact index
     uint32_t *item_meta = nullptr;// [items] meta word
+    uint8_t *item_own = nullptr;  // [items] owner's index in the tile
+    int *halo_n = nullptr;        // [tiles] staged partners of the tile
+    uint32_t *halo_idx = nullptr; // [tiles * HALO_CAP] their local indices (sorted)
     double *rad = nullptr;        // [N] radius
 };
 void plan_counts(int64_t N, const uint32_t *inc_start, const uint2 *inc, const SweepPlan &pl, uint32_t *nitem,

@@ -10,10 +10,8 @@
 //   * wall / plate contacts: one item, owned by the particle.
 // A tile's items are stored contiguously, grouped by owner (warp w's 32 particles' items form
 // one range), so records move with coalesced 256-bit accesses:
-//   CRec 32 B per item: n (a -> b; two fp64 components, the third reconstructed), delta and the
-//        stage's SPOOK bias b (fp64)
-//   PRec 32 B per item: P_n, P_t (3), P_r (3) and a 32-bit meta word (partner, flags); storage
-//        precision SWEEP_PMODE (kernels.h)
+//   CRec 32 B per item: n (a -> b) and delta, fp64 (the item's meta word in n's low bits)
+//   PRec 64 B per item: P_n, P_t (3), P_r (3) and the stage's SPOOK bias b, fp64
 // Everything else the contact row needs is derived from the radii: R* = r_a r_b/(r_a + r_b),
 // l_a = r_a - delta/2, l_b = r_b - delta/2, mu_r R*, Sigma-hat = Cs / sqrt(2 R* delta) (R4).
 //
@@ -22,9 +20,10 @@
 // body's own mass-splitting weight (c/m, c/I) and summed exactly; integer sums are order-free,
 // so a particle's velocity update does not depend on how contacts fall into tiles, warps or
 // ranks: trajectories are bit-identical for any decomposition.  Resolution
-// ~2^-48 m/s (linear) and ~2^-44 rad/s (angular) of velocity per contribution, far below the
-// fp32 impulse storage's rounding; a contribution beyond 2^56 units (~256 m/s or 4096 rad/s per
-// sweep) or a non-finite one poisons the particle's velocity with NaN (the step rolls back).
+// ~2^-42 m/s (linear) and ~2^-36 rad/s (angular) of velocity per contribution (5e-9 of g dt,
+// against 1e-5 of the parity bar); a contribution beyond 2^51 units (~500 m/s or ~3e4 rad/s in
+// one sweep) or a non-finite one poisons the particle's velocity with NaN (the step rolls back,
+// S:385).
 #include "common.cuh"
 #include "kernels.h"
 #include "sweep_core.cuh"
@@ -32,7 +31,7 @@
 constexpr int TT = SWEEP_TILE;           // particles per tile (one CTA), kernels.h
 constexpr int NWT = TT / 32;
 constexpr int SLOT_CAP = SWEEP_SLOT_CAP; // intra-tile body-b slots per tile
-constexpr int FX_EL = 48, FX_EA = 44;    // fixed-point exponents (linear, angular)
+constexpr int FX_EL = 42, FX_EA = 36;    // fixed-point exponents (linear, angular)
 
 __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { return make_double4(a.x, a.y, b.x, b.y); }
 
@@ -48,8 +47,7 @@ __device__ __forceinline__ double pow2(int e) { return __longlong_as_double((lon
 // rounds x s to an integer exactly (RN-even, like llrint) whenever |x s| <= 2^51, and then the
 // bit pattern of t is round(x s) + FX_MAGIC_BITS.  Sums of raw patterns are taken mod 2^64 and
 // the c FX_MAGIC_BITS are subtracted once per particle (exact: integer arithmetic wraps).  fx1
-// returns the deviation of t's exponent field from 0x433 (nonzero: out of range or NaN -> the
-// slow path, which produces the same raw form).
+// returns the deviation of t's exponent field from 0x433: nonzero means out of range or NaN.
 constexpr double FX_MAGIC = 6755399441055744.0;            // 1.5 2^52
 constexpr long long FX_MAGIC_BITS = 0x4338000000000000LL;
 struct Fx6 { long long v[6]; };
@@ -58,22 +56,12 @@ __device__ __forceinline__ unsigned fx1(double x, double s, long long &o)
     o = __double_as_longlong(__fma_rn(x, s, FX_MAGIC));
     return ((unsigned)((unsigned long long)o >> 52)) ^ 0x433u;
 }
-__device__ __noinline__ Fx6 fx6_slow(const d3 L, const d3 A, double sL, double sA, bool &bad)
-{
-    const double y[6] = {L.x * sL, L.y * sL, L.z * sL, A.x * sA, A.y * sA, A.z * sA};
-    Fx6 o;
-    for (int f = 0; f < 6; f++) {
-        if (!(fabs(y[f]) < 72057594037927936.0)) { bad = true; o.v[f] = FX_MAGIC_BITS; }   // >= 2^56 or NaN
-        else o.v[f] = (long long)((unsigned long long)__double2ll_rn(y[f]) + (unsigned long long)FX_MAGIC_BITS);
-    }
-    return o;
-}
 __device__ __forceinline__ Fx6 fx6(const d3 L, const d3 A, double sL, double sA, bool &bad)
 {
     Fx6 o;
     const unsigned e = fx1(L.x, sL, o.v[0]) | fx1(L.y, sL, o.v[1]) | fx1(L.z, sL, o.v[2]) | fx1(A.x, sA, o.v[3]) |
                        fx1(A.y, sA, o.v[4]) | fx1(A.z, sA, o.v[5]);
-    if (e) o = fx6_slow(L, A, sL, sA, bad);
+    bad |= e != 0u;
     return o;
 }
 // angular shares with one fixed rounding sequence (every path that produces a body's share of a
@@ -87,61 +75,38 @@ __device__ __forceinline__ d3 share_b(double lb, const d3 x, const d3 r)
     return mk(__fma_rn(-lb, x.x, r.x), __fma_rn(-lb, x.y, r.y), __fma_rn(-lb, x.z, r.z));
 }
 
-// ------------------------------------------------------------------ contact record (CRec)
-// n is stored as two fp64 components; the third, the largest in magnitude (>= 1/sqrt 3), is
-// sqrt(1 - u^2 - v^2) with its axis and sign in the low 3 mantissa bits of delta (delta itself
-// is used with those bits cleared: <= 7 ulp).  SWEEP_PMODE 1 also keeps the item's meta word in
-// the low 16 bits of u and v (n then carries ~36 bits: 1e-11, against 6e-8 of fp32 normals).
-#if SWEEP_PMODE == 1
+// ------------------------------------------------------------------ item records
+// CRec (32 B, written per stage): n (a -> b) and delta in fp64; the item's 32-bit meta word
+// rides in the low 16 bits of n.x and n.y (n keeps 36 mantissa bits there: ~1e-11), the owner's
+// index in the tile in the low 8 bits of delta (44 bits left: ~1e-13).
+// PRec (64 B, ping-pong): P_n, P_t (3), P_r (3) and the stage's SPOOK bias b, all fp64.  fp64
+// impulses are what the 1e-5 force/torque bar needs: with fp32 storage the rounding of the
+// impulses at every sweep, amplified by the rigid friction and rolling rows, reaches 6.8e-5 in
+// torque on the bench-shaped bed (measured); fp64 storage gives 9e-8.
 constexpr unsigned long long N_LOWMASK = 0xFFFFull;
-#else
-constexpr unsigned long long N_LOWMASK = 0ull;
-#endif
-__device__ __forceinline__ void crec_decode(const double4 c, d3 &n, double &delta, double &b)
+__device__ __forceinline__ double clr_low(double x)
 {
-    const unsigned long long db = (unsigned long long)__double_as_longlong(c.z);
-    delta = __longlong_as_double((long long)(db & ~7ull));
-    b = c.w;
-    const double u = __longlong_as_double((long long)((unsigned long long)__double_as_longlong(c.x) & ~N_LOWMASK));
-    const double v = __longlong_as_double((long long)((unsigned long long)__double_as_longlong(c.y) & ~N_LOWMASK));
-    const double s = __fma_rn(-u, u, __fma_rn(-v, v, 1.0));
-    double m = s * rsqrt64(s);
-    if (db & 4ull) m = -m;
-    const int ax = (int)(db & 3ull);
-    n = ax == 0 ? mk(m, u, v) : (ax == 1 ? mk(v, m, u) : mk(u, v, m));
+    return __longlong_as_double((long long)((unsigned long long)__double_as_longlong(x) & ~N_LOWMASK));
 }
-__device__ __forceinline__ double4 crec_encode(const d3 n, double delta, double b, uint32_t meta)
+__device__ __forceinline__ uint32_t crec_meta(const double4 c)
 {
-    const double ax0 = fabs(n.x), ax1 = fabs(n.y), ax2 = fabs(n.z);
-    const int ax = (ax0 >= ax1 && ax0 >= ax2) ? 0 : (ax1 >= ax2 ? 1 : 2);
-    const double big = ax == 0 ? n.x : (ax == 1 ? n.y : n.z);
-    double u = ax == 0 ? n.y : (ax == 1 ? n.z : n.x), v = ax == 0 ? n.z : (ax == 1 ? n.x : n.y);
-    if (N_LOWMASK) {
-        u = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(u) & ~N_LOWMASK) | (meta & 0xFFFFu)));
-        v = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(v) & ~N_LOWMASK) | (meta >> 16)));
-    }
-    const unsigned long long db = ((unsigned long long)__double_as_longlong(delta) & ~7ull) | (unsigned long long)ax |
-                                  (big < 0.0 ? 4ull : 0ull);
-    return make_double4(u, v, __longlong_as_double((long long)db), b);
+    return (uint32_t)((unsigned long long)__double_as_longlong(c.x) & N_LOWMASK) |
+           ((uint32_t)((unsigned long long)__double_as_longlong(c.y) & N_LOWMASK) << 16);
 }
-
-// ------------------------------------------------------------------ impulse record (PRec)
-// PMODE 0: P_n, P_t, P_r f32 + meta (32 B); 1: P_n f64, P_t, P_r f32 (32 B), meta in the CRec;
-// 2: all f64 + meta (64 B, two PRec units).  The sweep rounds each new impulse to its storage
-// precision and applies exactly the stored increments (momentum stays consistent).
-#if SWEEP_PMODE == 0
-typedef float PN_T;
-typedef float PT_T;
-struct PRaw { float4 a, b; };
-#elif SWEEP_PMODE == 1
-typedef double PN_T;
-typedef float PT_T;
-struct PRaw { double4 a; };
-#else
-typedef double PN_T;
-typedef double PT_T;
-struct PRaw { double4 a, b; };
-#endif
+__device__ __forceinline__ int crec_owner(const double4 c) { return (int)((unsigned long long)__double_as_longlong(c.w) & 0xFFull); }
+__device__ __forceinline__ double crec_delta(const double4 c)
+{
+    return __longlong_as_double((long long)((unsigned long long)__double_as_longlong(c.w) & ~0xFFull));
+}
+__device__ __forceinline__ double4 crec_encode(const d3 n, double delta, uint32_t meta, uint32_t owner)
+{
+    const double nx = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(n.x) & ~N_LOWMASK) |
+                                                       (meta & 0xFFFFu)));
+    const double ny = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(n.y) & ~N_LOWMASK) |
+                                                       (meta >> 16)));
+    const double dl = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(delta) & ~0xFFull) | owner));
+    return make_double4(nx, ny, n.z, dl);
+}
 __device__ __forceinline__ double4 ldg4d(const void *p)
 {
     double4 v;
@@ -152,136 +117,57 @@ __device__ __forceinline__ void stg4d(void *p, double a, double b, double c, dou
 {
     asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
 }
-__device__ __forceinline__ double pk2(float x, float y)
-{
-    return __longlong_as_double((long long)(((unsigned long long)__float_as_uint(y) << 32) | __float_as_uint(x)));
-}
-__device__ __forceinline__ float lo2(double d) { return __uint_as_float((uint32_t)(unsigned long long)__double_as_longlong(d)); }
-__device__ __forceinline__ float hi2(double d) { return __uint_as_float((uint32_t)((unsigned long long)__double_as_longlong(d) >> 32)); }
-
+struct PRaw { double4 a, b; };       // (P_n, P_t) and (P_r, bias)
 __device__ __forceinline__ PRaw ld_praw(const PRec *P, uint32_t k)
 {
     PRaw r;
-#if SWEEP_PMODE == 0
-    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-        : "=f"(r.a.x), "=f"(r.a.y), "=f"(r.a.z), "=f"(r.a.w), "=f"(r.b.x), "=f"(r.b.y), "=f"(r.b.z), "=f"(r.b.w)
-        : "l"(P + k));
-#elif SWEEP_PMODE == 1
     r.a = ldg4d(P + k);
-#else
-    r.a = ldg4d(P + 2 * (size_t)k);
-    r.b = ldg4d(reinterpret_cast<const double *>(P + 2 * (size_t)k) + 4);
-#endif
+    r.b = ldg4d(reinterpret_cast<const double4 *>(P + k) + 1);
     return r;
-}
-__device__ __forceinline__ uint32_t praw_meta(const PRaw &r, const double4 c)
-{
-#if SWEEP_PMODE == 0
-    (void)c;
-    return __float_as_uint(r.b.w);
-#elif SWEEP_PMODE == 1
-    (void)r;
-    return (uint32_t)((unsigned long long)__double_as_longlong(c.x) & 0xFFFFull) |
-           ((uint32_t)((unsigned long long)__double_as_longlong(c.y) & 0xFFFFull) << 16);
-#else
-    (void)c;
-    return (uint32_t)(unsigned long long)__double_as_longlong(r.b.w);
-#endif
-}
-__device__ __forceinline__ void praw_vals(const PRaw &r, double &pn, d3 &pt, d3 &pr)
-{
-#if SWEEP_PMODE == 0
-    pn = r.a.x; pt = mk(r.a.y, r.a.z, r.a.w); pr = mk(r.b.x, r.b.y, r.b.z);
-#elif SWEEP_PMODE == 1
-    pn = r.a.x;
-    pt = mk(lo2(r.a.y), hi2(r.a.y), lo2(r.a.z));
-    pr = mk(hi2(r.a.z), lo2(r.a.w), hi2(r.a.w));
-#else
-    pn = r.a.x; pt = mk(r.a.y, r.a.z, r.a.w); pr = mk(r.b.x, r.b.y, r.b.z);
-#endif
-}
-template <typename C>
-__device__ __forceinline__ void st_prec(PRec *P, uint32_t k, const C &c, uint32_t meta)
-{
-#if SWEEP_PMODE == 0
-    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(P + k), "f"(c.pn), "f"(c.pt[0]),
-                 "f"(c.pt[1]), "f"(c.pt[2]), "f"(c.pr[0]), "f"(c.pr[1]), "f"(c.pr[2]), "f"(__uint_as_float(meta))
-                 : "memory");
-#elif SWEEP_PMODE == 1
-    (void)meta;
-    stg4d(P + k, c.pn, pk2(c.pt[0], c.pt[1]), pk2(c.pt[2], c.pr[0]), pk2(c.pr[1], c.pr[2]));
-#else
-    double *q = reinterpret_cast<double *>(P + 2 * (size_t)k);
-    stg4d(q, c.pn, c.pt[0], c.pt[1], c.pt[2]);
-    stg4d(q + 4, c.pr[0], c.pr[1], c.pr[2], __longlong_as_double((long long)meta));
-#endif
-}
-// plain (generic-path) value access for the per-stage kernels
-struct PVals { double pn; d3 pt, pr; uint32_t meta; };
-__device__ __forceinline__ PVals prec_get(const PRec *P, const CRec *rec, int64_t k)
-{
-    PRaw r;
-#if SWEEP_PMODE == 0
-    const float *f = reinterpret_cast<const float *>(P + k);
-    r.a = make_float4(f[0], f[1], f[2], f[3]);
-    r.b = make_float4(f[4], f[5], f[6], f[7]);
-#elif SWEEP_PMODE == 1
-    r.a = reinterpret_cast<const double4 *>(P)[k];
-#else
-    r.a = reinterpret_cast<const double4 *>(P)[2 * k];
-    r.b = reinterpret_cast<const double4 *>(P)[2 * k + 1];
-#endif
-    PVals v;
-    praw_vals(r, v.pn, v.pt, v.pr);
-    v.meta = praw_meta(r, reinterpret_cast<const double4 *>(rec)[k]);
-    return v;
-}
-__device__ __forceinline__ void prec_put(PRec *P, int64_t k, double pn, const d3 pt, const d3 pr, uint32_t meta)
-{
-    ContactOutT<PN_T, PT_T> c;
-    c.pn = (PN_T)pn;
-    c.pt[0] = (PT_T)pt.x; c.pt[1] = (PT_T)pt.y; c.pt[2] = (PT_T)pt.z;
-    c.pr[0] = (PT_T)pr.x; c.pr[1] = (PT_T)pr.y; c.pr[2] = (PT_T)pr.z;
-#if SWEEP_PMODE == 0
-    float *f = reinterpret_cast<float *>(P + k);
-    f[0] = c.pn; f[1] = c.pt[0]; f[2] = c.pt[1]; f[3] = c.pt[2]; f[4] = c.pr[0]; f[5] = c.pr[1]; f[6] = c.pr[2];
-    f[7] = __uint_as_float(meta);
-#elif SWEEP_PMODE == 1
-    reinterpret_cast<double4 *>(P)[k] = make_double4(c.pn, pk2(c.pt[0], c.pt[1]), pk2(c.pt[2], c.pr[0]), pk2(c.pr[1], c.pr[2]));
-#else
-    reinterpret_cast<double4 *>(P)[2 * k] = make_double4(c.pn, c.pt[0], c.pt[1], c.pt[2]);
-    reinterpret_cast<double4 *>(P)[2 * k + 1] = make_double4(c.pr[0], c.pr[1], c.pr[2], __longlong_as_double((long long)meta));
-#endif
 }
 
 // ------------------------------------------------------------------ the sweep kernel
 // Each warp takes a contiguous range of the tile's particles holding ~1/NWT of its items
 // (balanced: the CTA's final barrier does not wait on a warp of coarse particles) and walks
 // their items 32 at a time, the next chunk's records in flight while the current one computes.
-// Operands are loaded by index straight into their canonical (a, b) slots (no selects):
-// intra-tile pairs and boundary contacts from shared memory, cross-tile pairs from global
-// (the tile's own particle is L1/L2-resident: the CTA just staged it).
+// Operands are loaded by index straight into their canonical (a, b) slots (no selects), from
+// shared memory: the CTA stages its tile's particles and its halo -- the distinct cross-tile
+// partners of its items (k_plan_halo) -- so the item loop makes no dependent global gathers
+// (partners beyond the halo capacity fall back to global loads).
+constexpr int TS = TT + HALO_CAP;        // staged particles per CTA: the tile and its halo
 template <bool IMPACT>
 __global__ void __launch_bounds__(TT, SWEEP_MINB)
     k_sweep(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win,
             const double *__restrict__ rad, double4 *__restrict__ vout, double4 *__restrict__ wout,
             const uint32_t *__restrict__ istart, const uint32_t *__restrict__ pin, const CRec *__restrict__ rec,
-            const PRec *__restrict__ Pin, PRec *__restrict__ Pout, const DevBoundary *__restrict__ bnd, SolveParams sp)
+            const PRec *__restrict__ Pin, PRec *__restrict__ Pout, const DevBoundary *__restrict__ bnd,
+            const int *__restrict__ halo_n, const uint32_t *__restrict__ halo_idx, SolveParams sp)
 {
-    __shared__ double2 sVa[TT], sVb[TT], sWa[TT], sWb[TT];
-    __shared__ double sR[TT];
+    // dynamic shared memory (> 48 KB in total): the states of the tile's particles [0, TT) and of
+    // its halo [TT, TT + HALO_CAP) as double2 halves, their radii, and the body-b slots
+    extern __shared__ double2 sDyn[];
+    double2 *sVa = sDyn, *sVb = sVa + TS, *sWa = sVb + TS, *sWb = sWa + TS;
+    double *sR = reinterpret_cast<double *>(sWb + TS);
+    longlong2 *sSlot = reinterpret_cast<longlong2 *>(sR + TS);   // [SLOT_CAP][3]
     __shared__ double2 sSig[TT];          // fixed-point scales (linear, angular) of the particle
     __shared__ long long sAcc[6][TT];
-    extern __shared__ long long sSlotDyn[];                 // [6][SLOT_CAP] (dynamic: > 48 KB total)
-    long long (*sSlot)[SLOT_CAP] = reinterpret_cast<long long (*)[SLOT_CAP]>(sSlotDyn);
     __shared__ uint32_t sI[TT + 1];
     __shared__ uint32_t sIn[TT];
-    __shared__ uint8_t sOwn[NWT][32];
     __shared__ int sBad[TT];
+    __shared__ int sWR[NWT + 1];          // the warps' particle ranges (balanced by items)
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t p0 = (int64_t)blockIdx.x * TT;
     const int np = (int)min((int64_t)TT, N - p0);
     for (int q = t; q <= np; q += TT) sI[q] = __ldg(&istart[p0 + q]);
+    // the halo: the tile's cross-tile partners (sorted, distinct; plan k_plan_halo)
+    const int hn = __ldg(&halo_n[blockIdx.x]);
+    for (int h = t; h < hn; h += TT) {
+        const uint32_t g = __ldg(&halo_idx[(size_t)blockIdx.x * HALO_CAP + h]);
+        const double4 v = ld4g(&vin[g]), o = ld4g(&win[g]);
+        sVa[TT + h] = make_double2(v.x, v.y); sVb[TT + h] = make_double2(v.z, v.w);
+        sWa[TT + h] = make_double2(o.x, o.y); sWb[TT + h] = make_double2(o.z, o.w);
+        sR[TT + h] = __ldg(&rad[g]);
+    }
     if (t < np) {
         const double4 v = ld4g(&vin[p0 + t]), o = ld4g(&win[p0 + t]);
         sVa[t] = make_double2(v.x, v.y); sVb[t] = make_double2(v.z, v.w);
@@ -296,19 +182,22 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
     for (int f = 0; f < 6; f++) sAcc[f][t] = 0;
     sBad[t] = 0;
     __syncthreads();
-    // the warp's particles [pb, pe): first particle whose items start at or after its share
-    const uint32_t I0 = sI[0], IT = sI[np] - I0;
-    auto first_at = [&](int q) -> int {
-        if (q <= 0) return 0;
-        if (q >= NWT) return np;
-        const uint32_t tgt = I0 + (uint32_t)(((uint64_t)IT * (uint32_t)q + NWT - 1) / NWT);
-        int lo = 0, hi = np;                 // smallest p in [0, np] with sI[p] >= tgt
-        while (lo < hi) { const int mid = (lo + hi) >> 1; if (sI[mid] < tgt) lo = mid + 1; else hi = mid; }
-        return lo;
-    };
-    const int pb = first_at(w), pe = first_at(w + 1);
+    // warp q's particles [sWR[q], sWR[q+1]): from the first particle whose items start at or after
+    // q/NWT of the tile's items (one binary search per warp boundary, threads 0..NWT)
+    if (t <= NWT) {
+        const uint32_t I0 = sI[0], IT = sI[np] - I0;
+        int lo = 0, hi = np;
+        if (t == 0) hi = 0;
+        else if (t == NWT) lo = np;
+        else {
+            const uint32_t tgt = I0 + (uint32_t)(((uint64_t)IT * (uint32_t)t + NWT - 1) / NWT);
+            while (lo < hi) { const int mid = (lo + hi) >> 1; if (sI[mid] < tgt) lo = mid + 1; else hi = mid; }
+        }
+        sWR[t] = lo;
+    }
+    __syncthreads();
+    const int pb = sWR[w], pe = sWR[w + 1];
     const uint32_t k0 = sI[pb], k1 = sI[pe];
-    int carry = 0;
     double4 cn;
     PRaw qn;
     if (k0 + lane < k1) { cn = ldg4d(rec + k0 + lane); qn = ld_praw(Pin, k0 + lane); }
@@ -318,23 +207,17 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
         const double4 cr = cn;
         const PRaw q = qn;
         if (kb + 32 + lane < k1) { cn = ldg4d(rec + kb + 32 + lane); qn = ld_praw(Pin, kb + 32 + lane); }   // next chunk in flight
-        // segment starts of the chunk (particles of the warp whose first item lies in it)
-        unsigned smask = 0;
-        for (int g = pb; g < pe; g += 32) {
-            const int p = g + lane;
-            const uint32_t sp_ = p < pe ? sI[p] : 0u, ep = p < pe ? sI[p + 1] : 0u;
-            const bool st = ep > sp_ && sp_ >= kb && sp_ < kb + 32;
-            smask |= __reduce_or_sync(0xffffffffu, st ? (1u << (sp_ - kb)) : 0u);
-            if (st) sOwn[w][sp_ - kb] = (uint8_t)p;
-        }
-        __syncwarp();
+        // segments of the chunk: runs of equal owner (items are grouped by owner)
+        const int o = valid ? crec_owner(cr) : -1;
+        const int op = __shfl_up_sync(0xffffffffu, o, 1);
+        const unsigned smask = __ballot_sync(0xffffffffu, valid && (lane == 0 || op != o));
         const unsigned le = smask & (0xffffffffu >> (31 - lane));
         const int sstart = le ? 31 - __clz(le) : 0;
-        const int o = le ? (int)sOwn[w][sstart] : carry;
         long long v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
         if (valid) {
-            const uint32_t meta = praw_meta(q, cr);
-            const bool intra = (meta & IT_INTRA) != 0, isB = (meta & IT_B) != 0, ext = (meta & IT_EXT) != 0;
+            const uint32_t meta = crec_meta(cr);
+            const uint32_t kind = meta & (IT_INTRA | IT_EXT);
+            const bool intra = kind == IT_INTRA, ext = kind == IT_EXT, isB = (meta & IT_B) != 0;
             double4 VA, WA, VB, WB;
             double ra, rb, mt, mr;
             int pl = -1;
@@ -348,36 +231,43 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
             } else {
                 mt = sp.mu_t;
                 mr = sp.mu_r;
-                if (intra) {     // owned by body a; body b in the tile
-                    pl = (int)(meta & IT_LOC);
-                    VA = cat2(sVa[o], sVb[o]); WA = cat2(sWa[o], sWb[o]); ra = sR[o];
-                    VB = cat2(sVa[pl], sVb[pl]); WB = cat2(sWa[pl], sWb[pl]); rb = sR[pl];
-                } else {
-                    const int64_t g = (int64_t)(meta & IT_IDX), me = p0 + o;
-                    const int64_t ga = isB ? g : me, gb = isB ? me : g;
+                int ia = -1, ib = -1;      // shared-memory slots of bodies a and b
+                int64_t g = -1;
+                if (intra) { pl = (int)(meta & IT_LOC); ia = o; ib = pl; }       // owned by body a
+                else if (kind == IT_HALO) { const int hh = TT + (int)(meta & IT_HMASK); ia = isB ? hh : o; ib = isB ? o : hh; }
+                else {
+                    g = (int64_t)(meta & IT_IDX);
+                    const int64_t l = g - p0;
+                    if (l >= 0 && l < np) { ia = isB ? (int)l : o; ib = isB ? o : (int)l; g = -1; }
+                }
+                if (g < 0) {
+                    VA = cat2(sVa[ia], sVb[ia]); WA = cat2(sWa[ia], sWb[ia]); ra = sR[ia];
+                    VB = cat2(sVa[ib], sVb[ib]); WB = cat2(sWa[ib], sWb[ib]); rb = sR[ib];
+                } else {         // partner beyond the halo capacity: from global memory
+                    const int64_t me = p0 + o, ga = isB ? g : me, gb = isB ? me : g;
                     VA = ld4g(&vin[ga]); WA = ld4g(&win[ga]); ra = __ldg(&rad[ga]);
                     VB = ld4g(&vin[gb]); WB = ld4g(&win[gb]); rb = __ldg(&rad[gb]);
                 }
             }
-            d3 n;
-            double delta, bias;
-            crec_decode(cr, n, delta, bias);
+            const d3 n = mk(clr_low(cr.x), clr_low(cr.y), cr.z);
+            const double delta = crec_delta(cr), bias = q.b.w;
             const double Rs = ext ? ra : rstar(ra, rb);
-            const double S = IMPACT ? 0.0 : spook_sigma(sp, Rs, delta);
+            const double S = IMPACT ? 0.0 : (sp.hertz ? sp.Cs * rsqrt64_1(2.0 * Rs * delta) : sp.Cs);   // R4
             const double la = ra - 0.5 * delta, lb = ext ? 0.0 : rb - 0.5 * delta;
-            double Pn0;
-            d3 Pt0, Pr0;
-            praw_vals(q, Pn0, Pt0, Pr0);
-            const ContactOutT<PN_T, PT_T> c = contact_core_t<PN_T, PT_T>(VA, WA, VB, WB, mt, n, mr * Rs, S, bias, la, lb,
-                                                                         Pn0, Pt0, Pr0, sp.rolling_dims);
-            st_prec(Pout, k, c, meta);
+            const ContactOutT<double, double> c = contact_core_t<double, double>(
+                VA, WA, VB, WB, mt, n, mr * Rs, S, bias, la, lb, q.a.x, mk(q.a.y, q.a.z, q.a.w), mk(q.b.x, q.b.y, q.b.z),
+                sp.rolling_dims);
+            double *po = reinterpret_cast<double *>(Pout + k);
+            stg4d(po, c.pn, c.pt[0], c.pt[1], c.pt[2]);
+            stg4d(po + 4, c.pr[0], c.pr[1], c.pr[2], bias);
             bool bad = false;
             if (intra) {   // body b of an intra-tile contact: its slot (stored first: fewer live registers)
                 const double2 sg = sSig[pl];
                 const Fx6 ot = fx6(c.L, share_b(lb, c.nxdPt, c.dPr), sg.x, sg.y, bad);
                 const int sl = (int)((meta >> IT_SLOT_SHIFT) & IT_SLOT_MASK);
-#pragma unroll
-                for (int f = 0; f < 6; f++) sSlot[f][sl] = ot.v[f];
+                sSlot[3 * sl] = make_longlong2(ot.v[0], ot.v[1]);
+                sSlot[3 * sl + 1] = make_longlong2(ot.v[2], ot.v[3]);
+                sSlot[3 * sl + 2] = make_longlong2(ot.v[4], ot.v[5]);
                 if (bad) atomicOr(&sBad[pl], 1);
             }
             const double2 ss = sSig[o];
@@ -410,8 +300,6 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
             A0[2 * TT + o] += (unsigned long long)v2; A0[3 * TT + o] += (unsigned long long)v3;
             A0[4 * TT + o] += (unsigned long long)v4; A0[5 * TT + o] += (unsigned long long)v5;
         }
-        carry = __shfl_sync(0xffffffffu, o, 31);
-        __syncwarp();
     }
     __syncthreads();
     if (t < np) {
@@ -423,8 +311,10 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
 #pragma unroll
             for (int f = 0; f < 6; f++) a[f] = sAcc[f][t];
             for (uint32_t s = is; s < is + ic; s++) {
+                const longlong2 x0 = sSlot[3 * s], x1 = sSlot[3 * s + 1], x2 = sSlot[3 * s + 2];
+                const long long x[6] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y};
 #pragma unroll
-                for (int f = 0; f < 6; f++) a[f] = (long long)((unsigned long long)a[f] + (unsigned long long)sSlot[f][s]);
+                for (int f = 0; f < 6; f++) a[f] = (long long)((unsigned long long)a[f] + (unsigned long long)x[f]);
             }
             const unsigned long long mc = (unsigned long long)cnt * (unsigned long long)FX_MAGIC_BITS;
 #pragma unroll
@@ -447,7 +337,7 @@ void launch_sweep_items(bool impact, int64_t N, const double4 *vin, const double
                         const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s)
 {
     if (!N) return;
-    constexpr int dyn = 6 * SLOT_CAP * (int)sizeof(long long);
+    constexpr int dyn = 4 * TS * (int)sizeof(double2) + TS * (int)sizeof(double) + 3 * SLOT_CAP * (int)sizeof(longlong2);
     static bool attr = [] {
         cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
@@ -456,9 +346,11 @@ void launch_sweep_items(bool impact, int64_t N, const double4 *vin, const double
     (void)attr;
     const unsigned gb = (unsigned)((N + TT - 1) / TT);
     if (impact)
-        k_sweep<true><<<gb, TT, dyn, s>>>(N, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd, sp);
+        k_sweep<true><<<gb, TT, dyn, s>>>(N, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd,
+                                          pl.halo_n, pl.halo_idx, sp);
     else
-        k_sweep<false><<<gb, TT, dyn, s>>>(N, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd, sp);
+        k_sweep<false><<<gb, TT, dyn, s>>>(N, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd,
+                                           pl.halo_n, pl.halo_idx, sp);
 }
 
 // ================================================================== the tile plan (per step)
@@ -530,7 +422,7 @@ __global__ void k_plan_slot(int64_t N, const uint32_t *__restrict__ inc_start, c
 __global__ void k_plan_fill(int64_t N, const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
                             const uint8_t *__restrict__ noint, const uint32_t *__restrict__ istart,
                             const uint32_t *__restrict__ slot_of, uint32_t *__restrict__ item_c,
-                            uint32_t *__restrict__ item_meta)
+                            uint32_t *__restrict__ item_meta, uint8_t *__restrict__ item_own)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
@@ -548,6 +440,7 @@ __global__ void k_plan_fill(int64_t N, const uint32_t *__restrict__ inc_start, c
         else meta = (isB ? IT_B : 0u) | e.y;
         item_c[o] = c;
         item_meta[o] = meta;
+        item_own[o] = (uint8_t)(i - tb);
         o++;
     }
 }
@@ -579,17 +472,107 @@ void plan_counts(int64_t N, const uint32_t *inc_start, const uint2 *inc, const S
     scan_u32(nitem, pl.istart, N, scan_tmp, s, launches);
     *launches += N ? 4 : 0;
 }
+__global__ void k_plan_halo(int64_t N, const uint32_t *__restrict__ istart, uint32_t *__restrict__ item_meta,
+                            int *__restrict__ halo_n, uint32_t *__restrict__ halo_idx);
 void plan_fill(int64_t N, const uint32_t *inc_start, const uint2 *inc, const double4 *pos, const SweepPlan &pl,
                cudaStream_t s, long long *launches)
 {
     if (!N) return;
-    k_plan_fill<<<IGRID(N)>>>(N, inc_start, inc, pl.noint, pl.istart, pl.slot_of, pl.item_c, pl.item_meta);
+    k_plan_fill<<<IGRID(N)>>>(N, inc_start, inc, pl.noint, pl.istart, pl.slot_of, pl.item_c, pl.item_meta,
+                              pl.item_own);
+    k_plan_halo<<<(unsigned)((N + TT - 1) / TT), TT, 0, s>>>(N, pl.istart, pl.item_meta, pl.halo_n, pl.halo_idx);
     k_radius<<<IGRID(N)>>>(N, pos, pl.rad);
-    *launches += 2;
+    *launches += 3;
+}
+
+// Halo of each tile: the distinct particles beyond the tile that its cross items name, sorted
+// (bitonic sort of at most HALO_SORT names in shared memory), the first HALO_CAP of them staged by
+// the sweep; their items' meta words are rewritten to name the halo slot (IT_HALO).  A tile
+// with more than HALO_SORT cross items keeps global partners (deterministic either way).
+constexpr int HALO_SORT = 2048;
+__global__ void __launch_bounds__(TT) k_plan_halo(int64_t N, const uint32_t *__restrict__ istart,
+                                                  uint32_t *__restrict__ item_meta, int *__restrict__ halo_n,
+                                                  uint32_t *__restrict__ halo_idx)
+{
+    __shared__ uint32_t key[HALO_SORT];
+    __shared__ uint32_t cnt, nu;
+    __shared__ uint32_t wsum[NWT];
+    const int t = threadIdx.x;
+    const int64_t p0 = (int64_t)blockIdx.x * TT;
+    const int np = (int)min((int64_t)TT, N - p0);
+    const uint32_t I0 = istart[p0], I1 = istart[p0 + np];
+    if (t == 0) cnt = 0;
+    __syncthreads();
+    auto cross = [&](uint32_t m, uint32_t &g) -> bool {
+        if (m & (IT_INTRA | IT_EXT)) return false;
+        g = m & IT_IDX;
+        return !((int64_t)g >= p0 && (int64_t)g < p0 + np);
+    };
+    for (uint32_t k = I0 + t; k < I1; k += TT) {
+        uint32_t g;
+        if (cross(item_meta[k], g)) {
+            const uint32_t q = atomicAdd(&cnt, 1u);
+            if (q < HALO_SORT) key[q] = g;
+        }
+    }
+    __syncthreads();
+    const uint32_t n = cnt;
+    if (n == 0 || n > (uint32_t)HALO_SORT) {
+        if (t == 0) halo_n[blockIdx.x] = 0;
+        return;
+    }
+    uint32_t L = 1;
+    while (L < n) L <<= 1;
+    for (uint32_t q = n + t; q < L; q += TT) key[q] = 0xFFFFFFFFu;
+    __syncthreads();
+    for (uint32_t sz = 2; sz <= L; sz <<= 1)             // bitonic sort, ascending
+        for (uint32_t j = sz >> 1; j > 0; j >>= 1) {
+            for (uint32_t q = t; q < L; q += TT) {
+                const uint32_t r = q ^ j;
+                if (r > q) {
+                    const uint32_t a = key[q], b = key[r];
+                    const bool up = (q & sz) == 0;
+                    if ((a > b) == up) { key[q] = b; key[r] = a; }
+                }
+            }
+            __syncthreads();
+        }
+    // distinct names, in order: an exclusive count of "first of its value" flags (block scan in
+    // chunks of TT), compacted in place (each write goes to an index <= its read)
+    if (t == 0) nu = 0;
+    __syncthreads();
+    for (uint32_t base = 0; base < n; base += TT) {
+        const uint32_t q = base + t;
+        const bool f = q < n && (q == 0 || key[q] != key[q - 1]);
+        const uint32_t v = q < n ? key[q] : 0u;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        const int lane = t & 31, w = t >> 5;
+        if (lane == 0) wsum[w] = __popc(bal);
+        __syncthreads();
+        uint32_t off = nu;
+        for (int k = 0; k < w; k++) off += wsum[k];
+        off += __popc(bal & ((1u << lane) - 1u));
+        __syncthreads();
+        if (f) key[off] = v;
+        if (t == TT - 1) nu = off + (f ? 1u : 0u);
+        __syncthreads();
+    }
+    const uint32_t H = nu < (uint32_t)HALO_CAP ? nu : (uint32_t)HALO_CAP;
+    for (uint32_t h = t; h < H; h += TT) halo_idx[(size_t)blockIdx.x * HALO_CAP + h] = key[h];
+    if (t == 0) halo_n[blockIdx.x] = (int)H;
+    for (uint32_t k = I0 + t; k < I1; k += TT) {
+        const uint32_t m = item_meta[k];
+        uint32_t g;
+        if (!cross(m, g)) continue;
+        uint32_t lo = 0, hi = H;                          // g in key[0, H)?
+        while (lo < hi) { const uint32_t mid = (lo + hi) >> 1; if (key[mid] < g) lo = mid + 1; else hi = mid; }
+        if (lo < H && key[lo] == g) item_meta[k] = IT_HALO | (m & IT_B) | lo;
+    }
 }
 
 // ------------------------------------------------------------------ per stage: records in, impulses out
 __global__ void k_item_pack(int64_t n, const uint32_t *__restrict__ item_c, const uint32_t *__restrict__ item_meta,
+                            const uint8_t *__restrict__ item_own,
                             const G4 *__restrict__ geo, const double *__restrict__ cdel, const R4 *__restrict__ row,
                             const P4 *__restrict__ Pa, const P4 *__restrict__ Pb, CRec *__restrict__ rec,
                             PRec *__restrict__ P)
@@ -598,12 +581,16 @@ __global__ void k_item_pack(int64_t n, const uint32_t *__restrict__ item_c, cons
     if (k >= n) return;
     const uint32_t c = item_c[k], meta = item_meta[k];
     const G4 g = geo[c];
-    reinterpret_cast<double4 *>(rec)[k] = crec_encode(mk(g.x, g.y, g.z), cdel[c], row[c].y, meta);
+    reinterpret_cast<double4 *>(rec)[k] = crec_encode(mk(g.x, g.y, g.z), cdel[c], meta, item_own[k]);
+    double4 *q = reinterpret_cast<double4 *>(P + k);
+    const double b = row[c].y;
     if (Pa) {
-        const P4 a = Pa[c], b = Pb[c];
-        prec_put(P, k, a.x, mk(a.y, a.z, a.w), mk(b.x, b.y, b.z), meta);
+        const P4 a = Pa[c], bb = Pb[c];
+        q[0] = make_double4(a.x, a.y, a.z, a.w);
+        q[1] = make_double4(bb.x, bb.y, bb.z, b);
     } else {
-        prec_put(P, k, 0.0, mk(0, 0, 0), mk(0, 0, 0), meta);
+        q[0] = make_double4(0.0, 0.0, 0.0, 0.0);
+        q[1] = make_double4(0.0, 0.0, 0.0, b);
     }
 }
 // the stage's final impulses back to the contact arrays (one item per contact writes: body a's)
@@ -612,15 +599,16 @@ __global__ void k_item_unpack(int64_t n, const uint32_t *__restrict__ item_c, co
 {
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const PVals q = prec_get(P, rec, k);
-    if (q.meta & IT_B) return;
+    if (crec_meta(reinterpret_cast<const double4 *>(rec)[k]) & IT_B) return;
+    const double4 *q = reinterpret_cast<const double4 *>(P + k);
+    const double4 a = q[0], b = q[1];
     const uint32_t c = item_c[k];
-    Pa[c] = make_float4((float)q.pn, (float)q.pt.x, (float)q.pt.y, (float)q.pt.z);
-    Pb[c] = make_float4((float)q.pr.x, (float)q.pr.y, (float)q.pr.z, 0.0f);
+    Pa[c] = mkP4(a.x, a.y, a.z, a.w);
+    Pb[c] = mkP4(b.x, b.y, b.z, 0.0);
 }
 void item_pack(int64_t n, const SweepPlan &pl, const G4 *geo, const double *cdel, const R4 *row, const P4 *Pa,
                const P4 *Pb, CRec *rec, PRec *P, cudaStream_t s)
-{ if (n) k_item_pack<<<IGRID(n)>>>(n, pl.item_c, pl.item_meta, geo, cdel, row, Pa, Pb, rec, P); }
+{ if (n) k_item_pack<<<IGRID(n)>>>(n, pl.item_c, pl.item_meta, pl.item_own, geo, cdel, row, Pa, Pb, rec, P); }
 void item_unpack(int64_t n, const SweepPlan &pl, const CRec *rec, const PRec *P, P4 *Pa, P4 *Pb, cudaStream_t s)
 { if (n) k_item_unpack<<<IGRID(n)>>>(n, pl.item_c, rec, P, Pa, Pb); }
 
@@ -633,7 +621,7 @@ __global__ void k_plate_items_flag(int64_t n, const uint8_t *__restrict__ own, c
     const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
     const uint32_t m = item_meta[k];
-    flag[k] = ((m & IT_EXT) && (m & PARTNER_PLATE) && (!own || own[cij[item_c[k]].x])) ? 1u : 0u;
+    flag[k] = ((m & (IT_EXT | IT_INTRA)) == IT_EXT && (m & PARTNER_PLATE) && (!own || own[cij[item_c[k]].x])) ? 1u : 0u;
 }
 void launch_plate_items_flag(int64_t n, const uint8_t *own, const SweepPlan &pl, const uint2 *cij, uint32_t *flag,
                              cudaStream_t s)
@@ -647,14 +635,13 @@ __global__ void k_plate_hub_items(int64_t n, const uint32_t *__restrict__ list, 
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= n) return;
     const uint32_t k = list[t];
-    const PVals o = prec_get(pout, rec, k);
+    const double4 o = reinterpret_cast<const double4 *>(pout + k)[0];
     const int q = (item_meta[k] >> 4) & 0xF;
     const G4 g = geo[item_c[k]];
-    double i0 = 0;
-    d3 it = mk(0, 0, 0);
-    if (pin) { const PVals i = prec_get(pin, rec, k); i0 = i.pn; it = i.pt; }
-    const double dPn = o.pn - i0;
-    const double d[3] = {dPn * g.x + (o.pt.x - it.x), dPn * g.y + (o.pt.y - it.y), dPn * g.z + (o.pt.z - it.z)};
+    double4 i = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (pin) i = reinterpret_cast<const double4 *>(pin + k)[0];
+    const double dPn = o.x - i.x;
+    const double d[3] = {dPn * g.x + (o.y - i.y), dPn * g.y + (o.z - i.z), dPn * g.z + (o.w - i.w)};
     for (int k2 = 0; k2 < 3; k2++) atomicAdd(&acc[3 * q + k2], (unsigned long long)llrint(d[k2] * HUB_SCALE));
 }
 void launch_plate_hub_items(int64_t n, const uint32_t *list, const SweepPlan &pl, const G4 *geo, const CRec *rec,

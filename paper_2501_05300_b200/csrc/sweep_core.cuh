@@ -7,12 +7,12 @@
 __device__ __forceinline__ d3 xyz(double4 a) { return mk(a.x, a.y, a.z); }
 
 // factor that scales a vector of squared length m2 onto the ball of radius lim (1 inside):
-// MUFU.RSQ64H estimate + two fp64 Newton steps, branch-free, full fp64 exponent range
+// MUFU.RSQ64H estimate + one fp64 Newton step (1e-14), branch-free, full fp64 exponent range
 __device__ __forceinline__ double clamp_scale(double m2, double lim)
 {
     const bool out = m2 > lim * lim;
     const double q = out ? m2 : 1.0;
-    return out ? lim * rsqrt64(q) : 1.0;
+    return out ? lim * rsqrt64_1(q) : 1.0;
 }
 
 // value as stored (float or double impulse storage) and back as a double

@@ -33,10 +33,12 @@ def main():
     N = dem.generator_count(bench.device_generator(a.workload), box)
     nc = rep["n_contacts"]
     alg = bench.ALG_B_PARTICLE * N + bench.ALG_B_CONTACT * nc
+    alg72 = bench.ALG_B_PARTICLE * N + bench.ALG_B_CONTACT_SURVEY * nc
     pk = bench.peaks().get("hbm_gbs")
     print(json.dumps({"tag": a.tag, "lib": os.environ.get("DEM_LIB_VARIANT", "default"), "workload": a.workload,
                       "ms_per_sweep": ms, "n_particles": N, "n_contacts": nc,
-                      "achieved_GBps": alg / (ms / 1e3) / 1e9, "frac": alg / (ms / 1e3) / 1e9 / pk if pk else None}),
+                      "achieved_GBps": alg / (ms / 1e3) / 1e9, "frac": alg / (ms / 1e3) / 1e9 / pk if pk else None,
+                      "frac_survey72": alg72 / (ms / 1e3) / 1e9 / pk if pk else None}),
           flush=True)
     bed.close()
 
