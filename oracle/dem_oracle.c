@@ -447,7 +447,7 @@ static void sweep(const or_world *w, const or_params *p, row *R, int64_t nc,
     if (accP) memset(accP, 0, sizeof(double) * 3 * (size_t)w->n_plates);
     const int64_t N = w->n;
     /* every contact from the sweep-start velocities (order-free: OpenMP over contacts) */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (nc > 4096)
     for (int64_t c = 0; c < nc; c++) {
         row *r = &R[c];
         const int64_t a = r->g.a;
@@ -524,7 +524,7 @@ static void sweep(const or_world *w, const or_params *p, row *R, int64_t nc,
             if (R[c].g.kind == 2) for (int k = 0; k < 3; k++) accP[3 * R[c].g.idx + k] += R[c].inc[k];
     /* 5. body update with the real masses (= mass-splitting average): per body, its contacts'
      *    increments in contact order (inc_s/inc_l lists them by increasing contact index) */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) if (N > 4096)
     for (int64_t i = 0; i < N; i++) {
         double aL[3] = {0.0, 0.0, 0.0}, aA[3] = {0.0, 0.0, 0.0};
         for (int64_t t = inc_s[i]; t < inc_s[i + 1]; t++) {

@@ -3,8 +3,9 @@
 impulses: the warm start of the next step), and the solver / material / box settings, in one
 .npz.  Resuming re-creates the bed through the C-ABI and hands the history back
 (dem_set_state), so the continued trajectory is bit-identical to the uninterrupted one.
-Plates and moving walls are not part of the checkpoint (their drives are re-issued by the
-caller)."""
+Plates, moved walls and the boundary clock are not part of the checkpoint: save() refuses a bed
+with a plate or with a wall that has moved or is moving (it would resume with the walls snapped
+back to the creation box).  Before the first step the history is empty."""
 from __future__ import annotations
 
 import json
@@ -17,8 +18,24 @@ from . import dem as D
 def save(bed: "D.Bed", path: str, meta: dict | None = None) -> None:
     if getattr(bed, "_world", 1) > 1:
         raise ValueError("checkpoint a single context (gather the slabs first)")
+    if getattr(bed, "n_plates", 0):
+        raise ValueError("checkpoint: plates are not captured (save before adding them)")
+    lo, hi = bed.box["lo"], bed.box["hi"]
+    for wall in range(6):
+        if not (bed.box.get("wall_mask", 0x3F) >> wall) & 1:
+            continue
+        ws = bed.get_wall(wall)
+        ax = wall // 2
+        home = lo[ax] if wall % 2 == 0 else hi[ax]
+        if ws["velocity"] != 0.0 or ws["point"][ax] != home:
+            raise ValueError(f"checkpoint: wall {wall} has moved or is moving (walls are not captured)")
     st = bed.get_state()
-    c = bed.get_contacts()
+    try:
+        c = bed.get_contacts()
+    except D.DemError as e:
+        if e.status != D.DEM_ERR_STATE:
+            raise
+        c = np.zeros(0, dtype=D.CONTACT_DTYPE)          # no step yet: no history
     cfg = dict(solver={k: (list(v) if isinstance(v, (tuple, list)) else v) for k, v in bed.solver.items()},
                material=dict(bed.material), box={k: (list(v) if isinstance(v, (tuple, list)) else v)
                                                   for k, v in bed.box.items()},

@@ -334,16 +334,13 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
     TRY(A(ctx, &ctx->ke_part, N / 256 + 2));
     dfree(ctx, ctx->pl.noint);
     dfree(ctx, ctx->pl.rad);
-    dfree(ctx, ctx->pl.halo_n);
-    dfree(ctx, ctx->pl.halo_idx);
+    dfree(ctx, ctx->pl.wrange);
+    ctx->pl.wrange = nullptr;
     ctx->pl.noint = nullptr;
     ctx->pl.rad = nullptr;
-    ctx->pl.halo_n = nullptr;
-    ctx->pl.halo_idx = nullptr;
     TRY(A(ctx, &ctx->pl.noint, N / SWEEP_TILE + 2));
     TRY(A(ctx, &ctx->pl.rad, N));
-    TRY(A(ctx, &ctx->pl.halo_n, N / SWEEP_TILE + 2));
-    TRY(A(ctx, &ctx->pl.halo_idx, (N / SWEEP_TILE + 2) * HALO_CAP));
+    TRY(A(ctx, &ctx->pl.wrange, (N / SWEEP_TILE + 2) * (SWEEP_TILE / 32 + 1)));
     if (!ctx->lvbox) {
         TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));
         TRY(A(ctx, &ctx->db, 1));
@@ -827,6 +824,20 @@ static dem_status sync_check(dem_ctx *ctx, const char *where)
     return DEM_OK;
 }
 
+// Decomposed: a failure on one rank must stop every rank before the next collective (else the
+// others block in it).  The statuses are max-reduced over the ranks at each decision point;
+// ranks that did not fail themselves report the failure of another.
+static dem_status agree(dem_ctx *ctx, dem_status st)
+{
+    if (!ctx->tp) return st;
+    double f = (double)(int)st;
+    std::string e;
+    if (!ctx->tp->allreduce_f64(&f, 1, 1, ctx->s, e)) { ctx->err = e; return DEM_ERR_NCCL; }
+    const dem_status g = (dem_status)(int)f;
+    if (g != DEM_OK && st == DEM_OK) ctx->err = "another rank failed (status " + std::to_string((int)g) + ")";
+    return g;
+}
+
 static dem_status rebuild(dem_ctx *ctx)
 {
     cudaStream_t s = ctx->s;
@@ -834,7 +845,7 @@ static dem_status rebuild(dem_ctx *ctx)
     if (!ctx->hist_pending) TRY(export_history(ctx));
     ctx->hist_pending = false;
     if (ctx->tp) {
-        TRY(ensure_keys(ctx, std::max<int64_t>(ctx->N, 1)));
+        TRY(agree(ctx, ensure_keys(ctx, std::max<int64_t>(ctx->N, 1))));
         TRY(redistribute(ctx));
     } else {
         ctx->N_own = ctx->N;
@@ -1020,7 +1031,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     std::memset(rep, 0, sizeof(*rep));
     tstart(ctx, 0);
     if (ctx->need_rebuild) {
-        TRY(rebuild(ctx));
+        TRY(agree(ctx, rebuild(ctx)));      // local failures after the band exchange (OOM): all ranks stop
         rep->rebuilt = 1;
     }
     const int64_t N = ctx->N;          // after the rebuild: the decomposition changes the local count
@@ -1040,14 +1051,16 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     CK(cudaMemcpyAsync(ctx->hnc, ctx->cscan + ncand, 4, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     nc = *ctx->hnc;
-    if (nc > INC_CMASK) { ctx->err = "more than 2^31 contacts on one rank"; return DEM_ERR_OOM; }
+    dem_status cst = DEM_OK;
+    if (nc > INC_CMASK) { ctx->err = "more than 2^31 contacts on one rank"; cst = DEM_ERR_OOM; }
+    TRY(agree(ctx, cst));
     ctx->nc = nc;
     launch_compact(ncand, ctx->cand, ctx->cflag, ctx->cscan, ctx->pos, ctx->db, sp, ctx->Pca, ctx->Pcb, ctx->cij,
                    ctx->geo, ctx->row, ctx->cdel, ctx->Pwa, ctx->Pwb, ctx->ccand, ctx->gid, ctx->dsc, s);
     launch_count_kinds(nc, OWN(ctx), ctx->cij, ctx->gid, ctx->dsc, s);
     launch_inc(N, ctx->co_start, ctx->cand, ctx->cscan, ctx->ct_start, ctx->ct_list, ctx->cflag, ctx->gid, ctx->inc_cnt,
                ctx->inc_start, ctx->inc, ctx->scan_tmp, s, &ctx->launches);
-    if (ctx->sol.ordering == 0) TRY(build_plan(ctx, N));
+    if (ctx->sol.ordering == 0) TRY(agree(ctx, build_plan(ctx, N)));
     ctx->n_plist = 0;
     ctx->n_it_plist = 0;
     if (mono_active(ctx) && nc) {
@@ -1289,35 +1302,44 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
 }
 
 // ------------------------------------------------------------------ state loading
-static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, const double *rad, const double *vel,
-                                 const double *ang, const uint32_t *gid, int on_device, bool first, bool check_slab = true)
+// host copies of a particle set being loaded, validated before the context is touched
+struct HostSet { std::vector<double> r, x; std::vector<uint32_t> g, gs; };
+static dem_status validate_particles(dem_ctx *ctx, int64_t n, const double *pos, const double *rad, const uint32_t *gid,
+                                     int on_device, bool check_slab, HostSet &h)
 {
-    // validate on the host
-    std::vector<double> r(n), x(3 * n);
-    std::vector<uint32_t> g(n);
+    h.r.resize(n); h.x.resize(3 * n); h.g.resize(n);
     cudaMemcpyKind kind = on_device ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
     if (n) {
-        CK(cudaMemcpy(r.data(), rad, n * 8, kind));
-        CK(cudaMemcpy(x.data(), pos, 3 * n * 8, kind));
-        if (gid) CK(cudaMemcpy(g.data(), gid, n * 4, kind));
-        else for (int64_t i = 0; i < n; i++) g[i] = (uint32_t)i;
+        CK(cudaMemcpy(h.r.data(), rad, n * 8, kind));
+        CK(cudaMemcpy(h.x.data(), pos, 3 * n * 8, kind));
+        if (gid) CK(cudaMemcpy(h.g.data(), gid, n * 4, kind));
+        else for (int64_t i = 0; i < n; i++) h.g[i] = (uint32_t)i;
     }
     for (int64_t i = 0; i < n; i++) {
-        if (!(r[i] > 0) || !std::isfinite(r[i])) { ctx->err = "radius must be positive and finite"; return DEM_ERR_INVALID; }
-        for (int k = 0; k < 3; k++) if (!std::isfinite(x[3 * i + k])) { ctx->err = "non-finite position"; return DEM_ERR_INVALID; }
-        if (g[i] >= PLATE_KEY_BASE) { ctx->err = "gid must be < 2^32-4096"; return DEM_ERR_INVALID; }
-        if (check_slab && ctx->tp && !((ctx->rank == 0 || x[3 * i] >= ctx->slab_lo) && (ctx->rank == ctx->G - 1 || x[3 * i] < ctx->slab_hi))) {
+        if (!(h.r[i] > 0) || !std::isfinite(h.r[i])) { ctx->err = "radius must be positive and finite"; return DEM_ERR_INVALID; }
+        for (int k = 0; k < 3; k++) if (!std::isfinite(h.x[3 * i + k])) { ctx->err = "non-finite position"; return DEM_ERR_INVALID; }
+        if (h.g[i] >= PLATE_KEY_BASE) { ctx->err = "gid must be < 2^32-4096"; return DEM_ERR_INVALID; }
+        if (check_slab && ctx->tp && !((ctx->rank == 0 || h.x[3 * i] >= ctx->slab_lo) && (ctx->rank == ctx->G - 1 || h.x[3 * i] < ctx->slab_hi))) {
             ctx->err = "particle outside this rank's slab [slab_lo, slab_hi)";
             return DEM_ERR_INVALID;
         }
     }
-    std::vector<uint32_t> gs(g);
-    std::sort(gs.begin(), gs.end());
-    for (int64_t i = 1; i < n; i++) if (gs[i] == gs[i - 1]) { ctx->err = "duplicate gid"; return DEM_ERR_INVALID; }
+    h.gs = h.g;
+    std::sort(h.gs.begin(), h.gs.end());
+    for (int64_t i = 1; i < n; i++) if (h.gs[i] == h.gs[i - 1]) { ctx->err = "duplicate gid"; return DEM_ERR_INVALID; }
+    return DEM_OK;
+}
+
+// loads a validated set (first: new particle arrays; else: same count as the context's)
+static dem_status commit_particles(dem_ctx *ctx, int64_t n, const HostSet &h, const double *pos, const double *rad,
+                                   const double *vel, const double *ang, int on_device, bool first)
+{
+    const std::vector<double> &r = h.r;
+    const std::vector<uint32_t> &g = h.g, &gs = h.gs;
     if (first) {
+        TRY(alloc_particles(ctx, n));     // counts are set once the arrays exist (an OOM leaves them as they were)
         ctx->N = n;
         ctx->N_own = n;
-        TRY(alloc_particles(ctx, n));
     } else if (n != ctx->N) {
         ctx->err = "set_state: particle count differs from create";
         return DEM_ERR_INVALID;
@@ -1346,6 +1368,14 @@ static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, con
     ctx->need_rebuild = true;
     ctx->have_step = false;
     return DEM_OK;
+}
+
+static dem_status load_particles(dem_ctx *ctx, int64_t n, const double *pos, const double *rad, const double *vel,
+                                 const double *ang, const uint32_t *gid, int on_device, bool first, bool check_slab = true)
+{
+    HostSet h;
+    TRY(validate_particles(ctx, n, pos, rad, gid, on_device, check_slab, h));
+    return commit_particles(ctx, n, h, pos, rad, vel, ang, on_device, first);
 }
 
 // ------------------------------------------------------------------ C-ABI
@@ -1775,17 +1805,22 @@ int64_t dem_num_particles(const dem_ctx *ctx) { return ctx ? ctx->N_own : -1; }
 int64_t dem_num_local(const dem_ctx *ctx) { return ctx ? ctx->N : -1; }
 
 // the particle set changes (emitter, trimming): the current state is exported in
-// gid order on the device, edited, and loaded as a fresh set; the contact history is exported
-// first and handed to the next rebuild (dem_set_state's path), so the warm start survives
+// gid order on the device, edited, validated, and only then is the contact history snapshot
+// (handed to the next rebuild, dem_set_state's path: the warm start survives) and the new set
+// loaded; a rejected edit leaves the context as it was
+static dem_status snapshot_history(dem_ctx *ctx)
+{
+    if (ctx->have_step && !ctx->hist_pending) TRY(export_history(ctx));
+    ctx->hist_pending = true;
+    if (ctx->hauth && ctx->nh) CK(cudaMemsetAsync(ctx->hauth, 0, ctx->nh, ctx->s));
+    return DEM_OK;
+}
 static dem_status export_particles(dem_ctx *ctx, int64_t extra, double **x, double **r, double **v, double **w,
                                    uint32_t **g)
 {
     const int64_t N = ctx->N, M = N + extra;
     TRY(A(ctx, x, 3 * M + 3)); TRY(A(ctx, r, M + 1)); TRY(A(ctx, v, 3 * M + 3)); TRY(A(ctx, w, 3 * M + 3));
     TRY(A(ctx, g, M + 1));
-    if (ctx->have_step && !ctx->hist_pending) TRY(export_history(ctx));
-    ctx->hist_pending = true;
-    if (ctx->hauth && ctx->nh) CK(cudaMemsetAsync(ctx->hauth, 0, ctx->nh, ctx->s));
     TRY(sync_check(ctx, "export_particles entry"));
     launch_to_gid_order(N, N, nullptr, ctx->gid, ctx->gid_sorted, ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], *x,
                         *v, *w, *r, *g, ctx->s);
@@ -1812,7 +1847,10 @@ dem_status dem_add_particles(dem_ctx *ctx, int64_t n, const double *pos, const d
     if (vel) CK(cudaMemcpyAsync(v + 3 * N, vel, 3 * n * 8, k, s)); else CK(cudaMemsetAsync(v + 3 * N, 0, 3 * n * 8, s));
     if (angvel) CK(cudaMemcpyAsync(w + 3 * N, angvel, 3 * n * 8, k, s)); else CK(cudaMemsetAsync(w + 3 * N, 0, 3 * n * 8, s));
     CK(cudaStreamSynchronize(s));
-    const dem_status st = load_particles(ctx, N + n, x, r, v, w, g, 1, true);
+    HostSet h;
+    dem_status st = validate_particles(ctx, N + n, x, r, g, 1, true, h);
+    if (st == DEM_OK) st = snapshot_history(ctx);
+    if (st == DEM_OK) st = commit_particles(ctx, N + n, h, x, r, v, w, 1, true);
     for (void *q : {(void *)x, (void *)r, (void *)v, (void *)w, (void *)g}) dfree(ctx, q);
     if (st == DEM_OK) TRY(sync_check(ctx, "add_particles end"));
     return st;
@@ -1839,7 +1877,10 @@ dem_status dem_remove_particles(dem_ctx *ctx, int32_t axis, double lo, double hi
     TRY(A(ctx, &w2, 3 * (int64_t)keep + 3)); TRY(A(ctx, &g2, keep + 1));
     launch_keep_gather(N, flag, scan, x, r, v, w, g, x2, r2, v2, w2, g2, s);
     CK(cudaStreamSynchronize(s));
-    const dem_status st = load_particles(ctx, keep, x2, r2, v2, w2, g2, 1, true);
+    HostSet h;
+    dem_status st = validate_particles(ctx, keep, x2, r2, g2, 1, true, h);
+    if (st == DEM_OK) st = snapshot_history(ctx);
+    if (st == DEM_OK) st = commit_particles(ctx, keep, h, x2, r2, v2, w2, 1, true);
     for (void *q : {(void *)x, (void *)r, (void *)v, (void *)w, (void *)g, (void *)flag, (void *)scan, (void *)x2,
                     (void *)r2, (void *)v2, (void *)w2, (void *)g2})
         dfree(ctx, q);

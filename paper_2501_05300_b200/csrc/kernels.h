@@ -97,10 +97,16 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 #define SWEEP_TILE 256           // <= 256: the owner index is 8 bits
 #endif
 #ifndef SWEEP_SLOT_CAP
-#define SWEEP_SLOT_CAP 768
+#define SWEEP_SLOT_CAP (3 * SWEEP_TILE)
 #endif
 #ifndef SWEEP_MINB
 #define SWEEP_MINB 2
+#endif
+#ifndef SWEEP_PREFETCH
+#define SWEEP_PREFETCH 1         // the next chunk's item records loaded during the current one
+#endif
+#ifndef SWEEP_PERSIST
+#define SWEEP_PERSIST 0          // 1: persistent CTAs, next tile staged by cp.async during the sweep
 #endif
 #define IT_INTRA 0x80000000u     // partner in the tile, body b's share goes to slot (bits 9..20)
 #define IT_B 0x40000000u         // cross pair: the owner is the canonical body b
@@ -109,11 +115,6 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 #define IT_LOC 0x1FFu            // intra pair: partner's index in the tile
 #define IT_SLOT_SHIFT 9
 #define IT_SLOT_MASK 0xFFFu
-#define IT_HALO (IT_INTRA | IT_EXT)   // cross pair whose partner is staged in the tile's halo (bits 0..9)
-#define IT_HMASK 0x3FFu
-#ifndef HALO_CAP
-#define HALO_CAP 448                  // staged cross-tile partners per tile
-#endif
 struct __align__(32) CRec { double nx, ny, nz, delta; };  // per item, per stage (meta in n's low bits, sweep.cu)
 struct __align__(32) PRec { double pn, pt[3], pr[3], b; }; // per item, ping-pong: fp64 impulses + SPOOK bias
 static_assert(sizeof(CRec) == 32 && sizeof(PRec) == 64, "item records");
@@ -125,8 +126,7 @@ struct SweepPlan {
     uint32_t *item_c = nullptr;   // [items] contact index
     uint32_t *item_meta = nullptr;// [items] meta word
     uint8_t *item_own = nullptr;  // [items] owner's index in the tile
-    int *halo_n = nullptr;        // [tiles] staged partners of the tile
-    uint32_t *halo_idx = nullptr; // [tiles * HALO_CAP] their local indices (sorted)
+    uint32_t *wrange = nullptr;   // [tiles * (TT/32 + 1)] the sweep warps' item ranges
     double *rad = nullptr;        // [N] radius
 };
 void plan_counts(int64_t N, const uint32_t *inc_start, const uint2 *inc, const SweepPlan &pl, uint32_t *nitem,

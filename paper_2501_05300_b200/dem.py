@@ -425,16 +425,19 @@ class Bed:
         return self.last_report
 
     def set_solver(self, **kw):
-        """Replace solver settings (keys of dem_solver); unspecified keys keep their values."""
-        self.solver.update(kw)
+        """Replace solver settings (keys of dem_solver); unspecified keys keep their values.  The
+        mirror (self.solver) changes only once the library accepted the new settings."""
+        merged = dict(self.solver)
+        merged.update(kw)
         s = Solver()
-        for k, v in self.solver.items():
+        for k, v in merged.items():
             if k == "gravity":
                 for j in range(3):
                     s.gravity[j] = v[j]
             else:
                 setattr(s, k, v)
         self._check(lib().dem_set_solver(self._h, C.byref(s)))
+        self.solver = merged
 
     @property
     def n_owned(self):
@@ -516,6 +519,7 @@ class Bed:
 
     # -- boundaries
     def add_plate(self, boxes_lo, boxes_hi, pos, mass, mu_t=0.4, mu_r=0.1):
+        self.n_plates = getattr(self, "n_plates", 0) + 1
         lo = np.ascontiguousarray(boxes_lo, dtype=np.float64).reshape(-1, 3)
         hi = np.ascontiguousarray(boxes_hi, dtype=np.float64).reshape(-1, 3)
         d = PlateDesc(len(lo), 0, lo.ctypes.data, hi.ctypes.data, mass, mu_t, mu_r)

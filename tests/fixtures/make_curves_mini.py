@@ -62,7 +62,7 @@ def run(kind, seed):
         nc[s] = W.last_report.n_plate
         if s % 5000 == 0:
             print(kind, seed, s, len(c), f[s], x[s], f"{time.time() - t1:.0f}s", flush=True)
-    out = os.path.join(ROOT, "tests", "golden", f"curves_mini_{kind}_{seed}.npz")
+    out = os.path.join(os.environ.get("CURVES_OUT", os.path.join(ROOT, "tests", "golden")), f"curves_mini_{kind}_{seed}.npz")
     np.savez_compressed(out, force=f.astype(np.float32), pos=x, n_plate=nc, digest=dg, n_particles=b.n,
                         settle_s=t1 - t0, run_s=time.time() - t1)
     print("wrote", out, b.n, "particles", f"settle {t1 - t0:.0f}s run {time.time() - t1:.0f}s", flush=True)

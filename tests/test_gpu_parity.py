@@ -558,6 +558,35 @@ def test_checkpoint_resume_bit_identical(tmp_path):
         b.close()
 
 
+def test_checkpoint_guards(tmp_path):
+    """checkpoint.save before any step writes an empty history (the resumed bed steps like a
+    fresh one); a moved or moving wall, or a plate, is refused (not captured)."""
+    from paper_2501_05300_b200 import checkpoint as CP
+    D = dem()
+    bed = synth.random_cloud(300, (0.002, 0.002, 0.002), (0.038, 0.038, 0.03), 1.5e-3, 3e-3, 15, v_scale=0.1)
+    kw = dict(solver=dict(dt=2e-5, n_iter=20), box=dict(lo=(0, 0, 0), hi=(0.04, 0.04, 0.06)))
+    a = D.Bed(bed.x, bed.r, bed.v, bed.w, bed.gid, **kw)
+    p = str(tmp_path / "fresh.npz")
+    try:
+        CP.save(a, p)
+        b = CP.load(p)
+        try:
+            a.step(5)
+            b.step(5)
+            assert np.array_equal(a.get_state()["pos"], b.get_state()["pos"])
+        finally:
+            b.close()
+        a.drive_wall(1, -0.01)
+        with pytest.raises(ValueError):       # the wall is moving
+            CP.save(a, p)
+        a.step(1)
+        a.drive_wall(1, 0.0)
+        with pytest.raises(ValueError):       # the wall has moved
+            CP.save(a, p)
+    finally:
+        a.close()
+
+
 def test_add_and_remove_particles_match_recreate():
     """dem_add_particles / dem_remove_particles keep the state and the contact history: the run
     continues bit-identically to re-creating the bed from the edited state with the history

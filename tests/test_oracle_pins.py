@@ -798,6 +798,17 @@ def test_residual_report_closed_forms(oracle_mod):
     res = W.last_report.max_normal_residual
     assert res == pytest.approx((P1 + P2) / m, rel=1e-9)
     assert abs(res - max(P1, P2) / m) > 0.1 * res
+    # (c) the report's cone excess max(|P_t| - mu_t P_n, |P_r| - mu_r R* P_n, 0): a sphere sliding
+    # down a steep incline sits on the friction cone (|P_t| = mu_t P_n), so the
+    # excess is zero to rounding while |P_t| is at the limit
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4, mu_t=0.4, mu_r=0.1)
+    th = math.atan(1.4)
+    W = oracle_mod.OracleWorld([[0, 0, r]], np.zeros((1, 3)), np.zeros((1, 3)), [r], [0], walls=floor)
+    pp = oracle_mod.make_params(h=h, n_it=60, E=1e9, nu=0.15, rho=2200.0, g=(9.81 * math.sin(th), 0, -9.81 * math.cos(th)))
+    for _ in range(200):
+        c, _, _ = W.step(pp)
+    assert np.linalg.norm(c["P"][0, 1:4]) == pytest.approx(0.4 * c["P"][0, 0], rel=1e-9)
+    assert 0.0 <= W.last_report.max_cone_excess <= 1e-12 * c["P"][0, 0]
 
 
 def test_centre_inside_plate_box_dense_directions(oracle_mod):
