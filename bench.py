@@ -447,7 +447,7 @@ def main():
                    "parallelism": f"x-slab decomposition x{world} (NCCL ghost exchange per sweep)"
                    if (world > 1 or args.decompose) else "single GPU",
                    "l2": l2_note,
-                   "precision": "fp64 state and row math; fp64 normal/overlap/bias records, fp32 impulses",
+                   "precision": "fp64 state and row math; fp64 normal, overlap and impulse records in the sweep; fp32 contact-array impulses between steps",
                    "ordering": "coloured Gauss-Seidel" if args.ordering == "gs" else "Jacobi (mass splitting)",
                    "reduction": "exact int64 fixed point per particle (order-free: bit-identical for any decomposition)",
                    "plates": n_plates, "plate_contacts_per_step": {"min": min(r["n_plate"] for r in reps),

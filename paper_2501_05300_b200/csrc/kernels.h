@@ -94,7 +94,7 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 // contacts owned by a tile (intra-tile pairs once, cross-tile pairs once per side, boundary
 // contacts once); item meta word: flags + partner (see IT_*).
 #ifndef SWEEP_TILE
-#define SWEEP_TILE 256           // <= 256: the owner index is 8 bits
+#define SWEEP_TILE 256           // <= 512: the owner index is 9 bits
 #endif
 #ifndef SWEEP_SLOT_CAP
 #define SWEEP_SLOT_CAP (3 * SWEEP_TILE)
@@ -125,7 +125,7 @@ struct SweepPlan {
     uint32_t *slot_of = nullptr;  // [nc] slot of an intra contact at body b
     uint32_t *item_c = nullptr;   // [items] contact index
     uint32_t *item_meta = nullptr;// [items] meta word
-    uint8_t *item_own = nullptr;  // [items] owner's index in the tile
+    uint16_t *item_own = nullptr; // [items] owner's index in the tile
     uint32_t *wrange = nullptr;   // [tiles * (TT/32 + 1)] the sweep warps' item ranges
     double *rad = nullptr;        // [N] radius
 };

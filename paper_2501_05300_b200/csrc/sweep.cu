@@ -31,6 +31,8 @@
 constexpr int TT = SWEEP_TILE;           // particles per tile (one CTA), kernels.h
 constexpr int NWT = TT / 32;
 constexpr int SLOT_CAP = SWEEP_SLOT_CAP; // intra-tile body-b slots per tile
+static_assert(TT % 32 == 0 && TT <= 512, "tile: whole warps, owner index in 9 bits");
+static_assert(SLOT_CAP <= (int)IT_SLOT_MASK + 1 && SLOT_CAP < 65536, "slot index: 12 bits in the meta word");
 constexpr int FX_EL = 42, FX_EA = 36;    // fixed-point exponents (linear, angular)
 
 __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { return make_double4(a.x, a.y, b.x, b.y); }
@@ -78,7 +80,7 @@ __device__ __forceinline__ d3 share_b(double lb, const d3 x, const d3 r)
 // ------------------------------------------------------------------ item records
 // CRec (32 B, written per stage): n (a -> b) and delta in fp64; the item's 32-bit meta word
 // rides in the low 16 bits of n.x and n.y (n keeps 36 mantissa bits there: ~1e-11), the owner's
-// index in the tile in the low 8 bits of delta (44 bits left: ~1e-13).
+// index in the tile in the low 9 bits of delta (43 bits left: ~1e-13).
 // PRec (64 B, ping-pong): P_n, P_t (3), P_r (3) and the stage's SPOOK bias b, all fp64.  fp64
 // impulses are what the 1e-5 force/torque bar needs: with fp32 storage the rounding of the
 // impulses at every sweep, amplified by the rigid friction and rolling rows, reaches 6.8e-5 in
@@ -93,10 +95,11 @@ __device__ __forceinline__ uint32_t crec_meta(const double4 c)
     return (uint32_t)((unsigned long long)__double_as_longlong(c.x) & N_LOWMASK) |
            ((uint32_t)((unsigned long long)__double_as_longlong(c.y) & N_LOWMASK) << 16);
 }
-__device__ __forceinline__ int crec_owner(const double4 c) { return (int)((unsigned long long)__double_as_longlong(c.w) & 0xFFull); }
+constexpr unsigned long long OWN_MASK = 0x1FFull;    // owner index bits in delta (tiles <= 512)
+__device__ __forceinline__ int crec_owner(const double4 c) { return (int)((unsigned long long)__double_as_longlong(c.w) & OWN_MASK); }
 __device__ __forceinline__ double crec_delta(const double4 c)
 {
-    return __longlong_as_double((long long)((unsigned long long)__double_as_longlong(c.w) & ~0xFFull));
+    return __longlong_as_double((long long)((unsigned long long)__double_as_longlong(c.w) & ~OWN_MASK));
 }
 __device__ __forceinline__ double4 crec_encode(const d3 n, double delta, uint32_t meta, uint32_t owner)
 {
@@ -104,7 +107,7 @@ __device__ __forceinline__ double4 crec_encode(const d3 n, double delta, uint32_
                                                        (meta & 0xFFFFu)));
     const double ny = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(n.y) & ~N_LOWMASK) |
                                                        (meta >> 16)));
-    const double dl = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(delta) & ~0xFFull) | owner));
+    const double dl = __longlong_as_double((long long)(((unsigned long long)__double_as_longlong(delta) & ~OWN_MASK) | owner));
     return make_double4(nx, ny, n.z, dl);
 }
 __device__ __forceinline__ double4 ldg4d(const void *p)
@@ -446,7 +449,7 @@ __global__ void k_plan_slot(int64_t N, const uint32_t *__restrict__ inc_start, c
 __global__ void k_plan_fill(int64_t N, const uint32_t *__restrict__ inc_start, const uint2 *__restrict__ inc,
                             const uint8_t *__restrict__ noint, const uint32_t *__restrict__ istart,
                             const uint32_t *__restrict__ slot_of, uint32_t *__restrict__ item_c,
-                            uint32_t *__restrict__ item_meta, uint8_t *__restrict__ item_own)
+                            uint32_t *__restrict__ item_meta, uint16_t *__restrict__ item_own)
 {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
@@ -464,7 +467,7 @@ __global__ void k_plan_fill(int64_t N, const uint32_t *__restrict__ inc_start, c
         else meta = (isB ? IT_B : 0u) | e.y;
         item_c[o] = c;
         item_meta[o] = meta;
-        item_own[o] = (uint8_t)(i - tb);
+        item_own[o] = (uint16_t)(i - tb);
         o++;
     }
 }
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(TT) k_plan_warps(int64_t N, const uint32_t *__
 
 // ------------------------------------------------------------------ per stage: records in, impulses out
 __global__ void k_item_pack(int64_t n, const uint32_t *__restrict__ item_c, const uint32_t *__restrict__ item_meta,
-                            const uint8_t *__restrict__ item_own,
+                            const uint16_t *__restrict__ item_own,
                             const G4 *__restrict__ geo, const double *__restrict__ cdel, const R4 *__restrict__ row,
                             const P4 *__restrict__ Pa, const P4 *__restrict__ Pb, CRec *__restrict__ rec,
                             PRec *__restrict__ P)
