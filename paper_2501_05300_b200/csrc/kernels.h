@@ -105,6 +105,9 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 #ifndef SWEEP_PREFETCH
 #define SWEEP_PREFETCH 1         // the next chunk's item records loaded during the current one
 #endif
+#ifndef SWEEP_RR
+#define SWEEP_RR 0               // 1: warps take the tile's 32-item chunks round robin (0: plan ranges)
+#endif
 #ifndef SWEEP_PERSIST
 #define SWEEP_PERSIST 0          // 1: persistent CTAs, next tile staged by cp.async during the sweep
 #endif

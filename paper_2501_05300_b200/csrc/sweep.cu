@@ -199,7 +199,16 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
         const int64_t p0 = tile * TT;
         const int np = (int)min((int64_t)TT, N - p0);
         // the warp's items [k0, k1) and its first chunk's records, requested before the wait
+#if SWEEP_RR
+        // round-robin chunks: warp w sweeps the tile's 32-item chunks w, w + NWT, ... (one partial
+        // chunk per tile); a particle whose items cross a chunk edge is summed with smem atomics
+        const uint32_t I1 = __ldg(&istart[p0 + np]);
+        const uint32_t k0 = __ldg(&istart[p0]) + 32u * (uint32_t)w, k1 = I1;
+        constexpr uint32_t KSTEP = 32u * NWT;
+#else
         const uint32_t k0 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w]), k1 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w + 1]);
+        constexpr uint32_t KSTEP = 32u;
+#endif
         double4 cn;
         PRaw qn;
         if (SWEEP_PREFETCH && k0 + lane < k1) { cn = ldg4d(rec + k0 + lane); qn = ld_praw(Pin, k0 + lane); }
@@ -219,13 +228,13 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
         for (int f = 0; f < 6; f++) sAcc[f][t] = 0;
         sBad[t] = 0;
         __syncthreads();
-        for (uint32_t kb = k0; kb < k1; kb += 32) {
+        for (uint32_t kb = k0; kb < k1; kb += KSTEP) {
             const uint32_t k = kb + lane;
             const bool valid = k < k1;
             if (!SWEEP_PREFETCH && valid) { cn = ldg4d(rec + k); qn = ld_praw(Pin, k); }
             const double4 cr = cn;
             const PRaw q = qn;
-            if (SWEEP_PREFETCH && kb + 32 + lane < k1) { cn = ldg4d(rec + kb + 32 + lane); qn = ld_praw(Pin, kb + 32 + lane); }   // next chunk in flight
+            if (SWEEP_PREFETCH && kb + KSTEP + lane < k1) { cn = ldg4d(rec + kb + KSTEP + lane); qn = ld_praw(Pin, kb + KSTEP + lane); }   // next chunk in flight
             // segments of the chunk: runs of equal owner (items are grouped by owner)
             const int o = valid ? crec_owner(cr) : -1;
             const int op = __shfl_up_sync(0xffffffffu, o, 1);
@@ -315,9 +324,15 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
             const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1);
             if (seg_end) {
                 unsigned long long *A0 = reinterpret_cast<unsigned long long *>(&sAcc[0][0]);
-                A0[0 * TT + o] += (unsigned long long)v0; A0[1 * TT + o] += (unsigned long long)v1;
-                A0[2 * TT + o] += (unsigned long long)v2; A0[3 * TT + o] += (unsigned long long)v3;
-                A0[4 * TT + o] += (unsigned long long)v4; A0[5 * TT + o] += (unsigned long long)v5;
+                if (SWEEP_RR && (sstart == 0 || lane == 31)) {   // may continue in another warp's chunk
+                    atomicAdd(&A0[0 * TT + o], (unsigned long long)v0); atomicAdd(&A0[1 * TT + o], (unsigned long long)v1);
+                    atomicAdd(&A0[2 * TT + o], (unsigned long long)v2); atomicAdd(&A0[3 * TT + o], (unsigned long long)v3);
+                    atomicAdd(&A0[4 * TT + o], (unsigned long long)v4); atomicAdd(&A0[5 * TT + o], (unsigned long long)v5);
+                } else {      // the particle's items all lie in this chunk: one plain add
+                    A0[0 * TT + o] += (unsigned long long)v0; A0[1 * TT + o] += (unsigned long long)v1;
+                    A0[2 * TT + o] += (unsigned long long)v2; A0[3 * TT + o] += (unsigned long long)v3;
+                    A0[4 * TT + o] += (unsigned long long)v4; A0[5 * TT + o] += (unsigned long long)v5;
+                }
             }
         }
         __syncthreads();

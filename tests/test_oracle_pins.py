@@ -866,3 +866,29 @@ def test_openmp_sweeps_bit_identical(oracle_mod):
         oracle_mod.set_threads(n0)
     for u, v in zip(*out):
         assert np.array_equal(u, v)
+
+
+@pytest.mark.parametrize("n_it", [1, 2, 7])
+def test_mass_splitting_duplicated_support_is_exact(oracle_mod, n_it):
+    """The finite-N_it Jacobi iterate with mass splitting (reading C22: contact j of
+    body i sees the inverse mass c_i/m_i, the body update sums the increments with 1/m_i).  A
+    sphere resting on TWO coincident frictionless floors (c = 2) has duplicated normal rows; the
+    exact LCP gives each half of Lambda = -(u + b)/(1/m + Sigma/2), and the mass-split Jacobi
+    reaches it after ONE sweep and stays there (each copy solves -(u + b)/(2/m + Sigma)).  SPOOK's
+    bias b does not depend on the stiffness and Sigma ~ 1/k, so the result equals a
+    single floor of doubled stiffness solved exactly (one row: one sweep).  A split count of 1
+    (or an update scaled by c/m) overshoots by ~2x; an average instead of a sum undershoots."""
+    r, h, k, d0, rho = 5e-3, 1e-4, 2e4, 2e-5, 2600.0
+    floor = oracle_mod.box_walls((-1, -1, 0), (1, 1, 1), mask=1 << 4)
+    out = {}
+    for tag, walls, kl in (("dup", list(floor) * 2, k), ("one2k", list(floor), 2 * k), ("onek", list(floor), k)):
+        W = oracle_mod.OracleWorld([[0, 0, r - d0]], [[0.0, 0.0, -0.01]], np.zeros((1, 3)), [r], [0], walls=walls)
+        c, _, _ = W.step(oracle_mod.make_params(h=h, n_it=n_it, e_H=1.0, k_lin=kl, rho=rho))
+        assert len(c) == len(walls) and W.last_report.impact_fired == 0
+        out[tag] = (W.v[0].copy(), W.x[0].copy(), c["P"][:, 0].sum())
+    vd, xd, Pd = out["dup"]
+    v2, x2, P2 = out["one2k"]
+    assert vd[2] == pytest.approx(v2[2], rel=1e-12, abs=1e-15)
+    assert xd[2] == pytest.approx(x2[2], rel=1e-14)
+    assert Pd == pytest.approx(P2, rel=1e-12)
+    assert abs(out["onek"][2] - P2) > 1e-3 * abs(P2)           # the stiffness matters at this size
