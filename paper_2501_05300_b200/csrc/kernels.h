@@ -102,15 +102,6 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 #ifndef SWEEP_MINB
 #define SWEEP_MINB 2
 #endif
-#ifndef SWEEP_PREFETCH
-#define SWEEP_PREFETCH 1         // the next chunk's item records loaded during the current one
-#endif
-#ifndef SWEEP_RR
-#define SWEEP_RR 0               // 1: warps take the tile's 32-item chunks round robin (0: plan ranges)
-#endif
-#ifndef SWEEP_PERSIST
-#define SWEEP_PERSIST 0          // 1: persistent CTAs, next tile staged by cp.async during the sweep
-#endif
 #define IT_INTRA 0x80000000u     // partner in the tile, body b's share goes to slot (bits 9..20)
 #define IT_B 0x40000000u         // cross pair: the owner is the canonical body b
 #define IT_EXT 0x20000000u       // wall / plate box: bits 0..28 = boundary code (PARTNER_* codes)

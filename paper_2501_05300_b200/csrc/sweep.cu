@@ -130,14 +130,16 @@ __device__ __forceinline__ PRaw ld_praw(const PRec *P, uint32_t k)
 }
 
 // ------------------------------------------------------------------ the sweep kernel
-// Persistent CTAs (2 per SM) walk the tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the next
-// tile's particles are staged into the second half of a double buffer with cp.async while the
-// current tile's items are swept (the staging latency leaves the critical path).  Each warp
-// takes a contiguous range of the tile's particles holding ~1/NWT of its items (plan
-// k_plan_warps: the tile's final barrier does not wait on a warp of coarse particles) and walks
-// their items 32 at a time, the next chunk's records in flight while the current one computes.
-// Operands are loaded by index straight into their canonical (a, b) slots (no selects): the
-// tile's particles from shared memory, cross-tile partners from global memory.
+// One CTA per tile of TT consecutive particles (2 CTAs per SM).  The tile's particle states are
+// staged into shared memory with cp.async.  Each warp takes a contiguous range of the tile's
+// particles holding ~1/NWT of its items (plan k_plan_warps: the tile's final barrier does not
+// wait on a warp of coarse particles) and walks their items 32 at a time, the next chunk's item
+// records in flight (registers) while the current chunk computes.  Operands are loaded by index
+// straight into their canonical (a, b) slots (no selects): the tile's particles from shared
+// memory, cross-tile pairs from global memory (both bodies: the own particle hits L1/L2).
+// Measured and dropped (profiles/r02_sweep_variants.jsonl): the next chunk's cross-tile partners
+// gathered by cp.async into a shared-memory ring (3.55 ms vs 3.03) or prefetched into L1 (3.24),
+// warps taking the tile's chunks round robin with smem atomics at chunk edges (3.17).
 __device__ __forceinline__ void cp_async16(void *s, const void *g)
 {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g) : "memory");
@@ -153,7 +155,8 @@ __device__ __forceinline__ void cp_async4(void *s, const void *g)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// one staging buffer: the tile's particle states as double2 halves, radii, item starts, slots
+// the tile's particle states (v and w as double2 halves: conflict-free 16-byte reads), radii,
+// item starts and incoming-slot words
 struct StageBuf {
     double2 va[TT], vb[TT], wa[TT], wb[TT];
     double r[TT];
@@ -164,209 +167,187 @@ __device__ __forceinline__ void stage_tile(StageBuf &B, int64_t p0, int np, int 
                                            const double4 *win, const double *rad, const uint32_t *istart,
                                            const uint32_t *pin)
 {
+    // 16-byte chunk c of the tile's v (w) array: particle c/2, half c%2; consecutive threads take
+    // consecutive chunks, so a warp reads 512 contiguous bytes and writes two 256-byte runs
+    const double2 *v = reinterpret_cast<const double2 *>(vin + p0), *o = reinterpret_cast<const double2 *>(win + p0);
+    for (int c = t; c < 2 * np; c += TT) {
+        double2 *dv = (c & 1) ? B.vb : B.va, *dw = (c & 1) ? B.wb : B.wa;
+        cp_async16(&dv[c >> 1], v + c);
+        cp_async16(&dw[c >> 1], o + c);
+    }
     if (t < np) {
-        const double *v = reinterpret_cast<const double *>(vin + p0 + t), *o = reinterpret_cast<const double *>(win + p0 + t);
-        cp_async16(&B.va[t], v); cp_async16(&B.vb[t], v + 2);
-        cp_async16(&B.wa[t], o); cp_async16(&B.wb[t], o + 2);
         cp_async8(&B.r[t], rad + p0 + t);
         cp_async4(&B.in[t], pin + p0 + t);
     }
     for (int q = t; q <= np; q += TT) cp_async4(&B.is[q], istart + p0 + q);
     cp_async_commit();
 }
-
 template <bool IMPACT>
 __global__ void __launch_bounds__(TT, SWEEP_MINB)
-    k_sweep(int64_t N, int64_t ntiles, const double4 *__restrict__ vin, const double4 *__restrict__ win,
+    k_sweep(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win,
             const double *__restrict__ rad, double4 *__restrict__ vout, double4 *__restrict__ wout,
             const uint32_t *__restrict__ istart, const uint32_t *__restrict__ pin, const CRec *__restrict__ rec,
             const PRec *__restrict__ Pin, PRec *__restrict__ Pout, const DevBoundary *__restrict__ bnd,
             const uint32_t *__restrict__ wrange, SolveParams sp)
 {
-    // dynamic shared memory (> 48 KB in total): two staging buffers and the body-b slots
+    // dynamic shared memory (> 48 KB in total): the tile's states and the body-b slots
     extern __shared__ double2 sDyn[];
-    StageBuf *sBuf = reinterpret_cast<StageBuf *>(sDyn);
-    longlong2 *sSlot = reinterpret_cast<longlong2 *>(sBuf + (SWEEP_PERSIST ? 2 : 1));   // [SLOT_CAP][3]
+    StageBuf &B = *reinterpret_cast<StageBuf *>(sDyn);
+    longlong2 *sSlot = reinterpret_cast<longlong2 *>(&B + 1);   // [SLOT_CAP][3]
     __shared__ double2 sSig[TT];          // fixed-point scales (linear, angular) of the particle
     __shared__ long long sAcc[6][TT];
     __shared__ int sBad[TT];
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-    int64_t tile = blockIdx.x;
-    if (tile >= ntiles) return;
-    stage_tile(sBuf[0], tile * TT, (int)min((int64_t)TT, N - tile * TT), t, vin, win, rad, istart, pin);
-    for (int it = 0; tile < ntiles; tile += gridDim.x, it++) {
-        StageBuf &B = sBuf[SWEEP_PERSIST ? (it & 1) : 0];
-        const int64_t p0 = tile * TT;
-        const int np = (int)min((int64_t)TT, N - p0);
-        // the warp's items [k0, k1) and its first chunk's records, requested before the wait
-#if SWEEP_RR
-        // round-robin chunks: warp w sweeps the tile's 32-item chunks w, w + NWT, ... (one partial
-        // chunk per tile); a particle whose items cross a chunk edge is summed with smem atomics
-        const uint32_t I1 = __ldg(&istart[p0 + np]);
-        const uint32_t k0 = __ldg(&istart[p0]) + 32u * (uint32_t)w, k1 = I1;
-        constexpr uint32_t KSTEP = 32u * NWT;
-#else
-        const uint32_t k0 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w]), k1 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w + 1]);
-        constexpr uint32_t KSTEP = 32u;
-#endif
-        double4 cn;
-        PRaw qn;
-        if (SWEEP_PREFETCH && k0 + lane < k1) { cn = ldg4d(rec + k0 + lane); qn = ld_praw(Pin, k0 + lane); }
-        cp_async_wait_all();
-        __syncthreads();                  // this tile's buffer is complete; the other one is free
-        const int64_t nt = tile + gridDim.x;
-        if (SWEEP_PERSIST && nt < ntiles)
-            stage_tile(sBuf[(it & 1) ^ 1], nt * TT, (int)min((int64_t)TT, N - nt * TT), t, vin, win, rad, istart, pin);
-        double2 *sVa = B.va, *sVb = B.vb, *sWa = B.wa, *sWb = B.wb;
-        const double *sR = B.r;
-        if (t < np) {
-            const uint32_t c = (B.is[t + 1] - B.is[t]) + (B.in[t] >> 16);
-            sSig[t] = c ? make_double2(pow2(FX_EL + fx_exp(sVb[t].y, c)), pow2(FX_EA + fx_exp(sWb[t].y, c)))
-                        : make_double2(0.0, 0.0);
-        }
+    const int64_t tile = blockIdx.x;
+    const int64_t p0 = tile * TT;
+    const int np = (int)min((int64_t)TT, N - p0);
+    stage_tile(B, p0, np, t, vin, win, rad, istart, pin);
+    // the warp's items [k0, k1) and its first chunk's records, requested before the wait
+    const uint32_t k0 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w]), k1 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w + 1]);
+    double4 cn;
+    PRaw qn;
+    if (k0 + lane < k1) { cn = ldg4d(rec + k0 + lane); qn = ld_praw(Pin, k0 + lane); }
+    cp_async_wait_all();
+    __syncthreads();                      // the tile's states are in shared memory
+    const double2 *sVa = B.va, *sVb = B.vb, *sWa = B.wa, *sWb = B.wb;
+    const double *sR = B.r;
+    if (t < np) {
+        const uint32_t c = (B.is[t + 1] - B.is[t]) + (B.in[t] >> 16);
+        sSig[t] = c ? make_double2(pow2(FX_EL + fx_exp(sVb[t].y, c)), pow2(FX_EA + fx_exp(sWb[t].y, c)))
+                    : make_double2(0.0, 0.0);
+    }
 #pragma unroll
-        for (int f = 0; f < 6; f++) sAcc[f][t] = 0;
-        sBad[t] = 0;
-        __syncthreads();
-        for (uint32_t kb = k0; kb < k1; kb += KSTEP) {
-            const uint32_t k = kb + lane;
-            const bool valid = k < k1;
-            if (!SWEEP_PREFETCH && valid) { cn = ldg4d(rec + k); qn = ld_praw(Pin, k); }
-            const double4 cr = cn;
-            const PRaw q = qn;
-            if (SWEEP_PREFETCH && kb + KSTEP + lane < k1) { cn = ldg4d(rec + kb + KSTEP + lane); qn = ld_praw(Pin, kb + KSTEP + lane); }   // next chunk in flight
-            // segments of the chunk: runs of equal owner (items are grouped by owner)
-            const int o = valid ? crec_owner(cr) : -1;
-            const int op = __shfl_up_sync(0xffffffffu, o, 1);
-            const unsigned smask = __ballot_sync(0xffffffffu, valid && (lane == 0 || op != o));
-            const unsigned le = smask & (0xffffffffu >> (31 - lane));
-            const int sstart = le ? 31 - __clz(le) : 0;
-            long long v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
-            if (valid) {
-                const uint32_t meta = crec_meta(cr);
-                const uint32_t kind = meta & (IT_INTRA | IT_EXT);
-                const bool intra = kind == IT_INTRA, ext = kind == IT_EXT, isB = (meta & IT_B) != 0;
-                double4 VA, WA, VB, WB;
-                double ra, rb, mt, mr;
-                int pl = -1;
-                if (ext) {           // the particle is body a, the wall / plate body b
-                    d3 bv;
-                    boundary_body((meta & IT_IDX) | PARTNER_EXT, bnd, bv, mt, mr);
-                    VA = cat2(sVa[o], sVb[o]); WA = cat2(sWa[o], sWb[o]); ra = sR[o];
-                    VB = make_double4(bv.x, bv.y, bv.z, 0.0);
-                    WB = make_double4(0.0, 0.0, 0.0, 0.0);
-                    rb = 0.0;
-                } else {
-                    mt = sp.mu_t;
-                    mr = sp.mu_r;
-                    int ia = -1, ib = -1;      // shared-memory slots of bodies a and b
-                    int64_t g = -1;
-                    if (intra) { pl = (int)(meta & IT_LOC); ia = o; ib = pl; }       // owned by body a
-                    else {
-                        g = (int64_t)(meta & IT_IDX);
-                        const int64_t l = g - p0;
-                        if (l >= 0 && l < np) { ia = isB ? (int)l : o; ib = isB ? o : (int)l; g = -1; }
-                    }
-                    if (g < 0) {
-                        VA = cat2(sVa[ia], sVb[ia]); WA = cat2(sWa[ia], sWb[ia]); ra = sR[ia];
-                        VB = cat2(sVa[ib], sVb[ib]); WB = cat2(sWa[ib], sWb[ib]); rb = sR[ib];
-                    } else {         // cross-tile partner: from global memory (the own particle too: L1)
-                        const int64_t me = p0 + o, ga = isB ? g : me, gb = isB ? me : g;
-                        VA = ld4g(&vin[ga]); WA = ld4g(&win[ga]); ra = __ldg(&rad[ga]);
-                        VB = ld4g(&vin[gb]); WB = ld4g(&win[gb]); rb = __ldg(&rad[gb]);
-                    }
+    for (int f = 0; f < 6; f++) sAcc[f][t] = 0;
+    sBad[t] = 0;
+    __syncthreads();
+    for (uint32_t kb = k0; kb < k1; kb += 32) {
+        const uint32_t k = kb + lane;
+        const bool valid = k < k1;
+        const double4 cr = cn;
+        const PRaw q = qn;
+        if (kb + 32 + lane < k1) { cn = ldg4d(rec + kb + 32 + lane); qn = ld_praw(Pin, kb + 32 + lane); }   // next chunk in flight
+        // segments of the chunk: runs of equal owner (items are grouped by owner)
+        const int o = valid ? crec_owner(cr) : -1;
+        const int op = __shfl_up_sync(0xffffffffu, o, 1);
+        const unsigned smask = __ballot_sync(0xffffffffu, valid && (lane == 0 || op != o));
+        const unsigned le = smask & (0xffffffffu >> (31 - lane));
+        const int sstart = le ? 31 - __clz(le) : 0;
+        long long v0 = 0, v1 = 0, v2 = 0, v3 = 0, v4 = 0, v5 = 0;
+        if (valid) {
+            const uint32_t meta = crec_meta(cr);
+            const uint32_t kind = meta & (IT_INTRA | IT_EXT);
+            const bool intra = kind == IT_INTRA, ext = kind == IT_EXT, isB = (meta & IT_B) != 0;
+            double4 VA, WA, VB, WB;
+            double ra, rb, mt, mr;
+            int pl = -1;
+            if (ext) {           // the particle is body a, the wall / plate body b
+                d3 bv;
+                boundary_body((meta & IT_IDX) | PARTNER_EXT, bnd, bv, mt, mr);
+                VA = cat2(sVa[o], sVb[o]); WA = cat2(sWa[o], sWb[o]); ra = sR[o];
+                VB = make_double4(bv.x, bv.y, bv.z, 0.0);
+                WB = make_double4(0.0, 0.0, 0.0, 0.0);
+                rb = 0.0;
+            } else {
+                mt = sp.mu_t;
+                mr = sp.mu_r;
+                int ia = -1, ib = -1;      // shared-memory slots of bodies a and b
+                int64_t g = -1;
+                if (intra) { pl = (int)(meta & IT_LOC); ia = o; ib = pl; }       // owned by body a
+                else {
+                    g = (int64_t)(meta & IT_IDX);
+                    const int64_t l = g - p0;
+                    if (l >= 0 && l < np) { ia = isB ? (int)l : o; ib = isB ? o : (int)l; g = -1; }
                 }
-                const d3 n = mk(clr_low(cr.x), clr_low(cr.y), cr.z);
-                const double delta = crec_delta(cr), bias = q.b.w;
-                const double Rs = ext ? ra : rstar(ra, rb);
-                const double S = IMPACT ? 0.0 : (sp.hertz ? sp.Cs * rsqrt64_1(2.0 * Rs * delta) : sp.Cs);   // R4
-                const double la = ra - 0.5 * delta, lb = ext ? 0.0 : rb - 0.5 * delta;
-                const ContactOutT<double, double> c = contact_core_t<double, double>(
-                    VA, WA, VB, WB, mt, n, mr * Rs, S, bias, la, lb, q.a.x, mk(q.a.y, q.a.z, q.a.w), mk(q.b.x, q.b.y, q.b.z),
-                    sp.rolling_dims);
-                double *po = reinterpret_cast<double *>(Pout + k);
-                stg4d(po, c.pn, c.pt[0], c.pt[1], c.pt[2]);
-                stg4d(po + 4, c.pr[0], c.pr[1], c.pr[2], bias);
-                // shares: body a gets -(L), -(la n x dPt + dPr); body b gets +L, -lb n x dPt + dPr
-                bool bad = false;
-                if (intra) {   // body b of an intra-tile contact: its slot (stored first: fewer live registers)
-                    const double2 sg = sSig[pl];
-                    const Fx6 ot = fx6(c.L, share_b(lb, c.nxdPt, c.dPr), sg.x, sg.y, bad);
-                    const int sl = (int)((meta >> IT_SLOT_SHIFT) & IT_SLOT_MASK);
-                    sSlot[3 * sl] = make_longlong2(ot.v[0], ot.v[1]);
-                    sSlot[3 * sl + 1] = make_longlong2(ot.v[2], ot.v[3]);
-                    sSlot[3 * sl + 2] = make_longlong2(ot.v[4], ot.v[5]);
-                    if (bad) atomicOr(&sBad[pl], 1);
-                }
-                const double2 ss = sSig[o];
-                const d3 Ls = isB ? c.L : mk(-c.L.x, -c.L.y, -c.L.z);
-                const d3 As = isB ? share_b(lb, c.nxdPt, c.dPr) : share_a(la, c.nxdPt, c.dPr);
-                const Fx6 me6 = fx6(Ls, As, ss.x, ss.y, bad);
-                v0 = me6.v[0]; v1 = me6.v[1]; v2 = me6.v[2]; v3 = me6.v[3]; v4 = me6.v[4]; v5 = me6.v[5];
-                if (bad) atomicOr(&sBad[o], 1);
-            }
-            // segmented sum of the self shares (items are grouped by owner): exact int64
-            const int dist = valid ? lane - sstart : 0;
-            const int maxd = __reduce_max_sync(0xffffffffu, dist);
-            for (int d = 1; d <= maxd; d <<= 1) {
-                const long long u0 = __shfl_up_sync(0xffffffffu, v0, d), u1 = __shfl_up_sync(0xffffffffu, v1, d);
-                const long long u2 = __shfl_up_sync(0xffffffffu, v2, d), u3 = __shfl_up_sync(0xffffffffu, v3, d);
-                const long long u4 = __shfl_up_sync(0xffffffffu, v4, d), u5 = __shfl_up_sync(0xffffffffu, v5, d);
-                if (lane - d >= sstart) {     // mod 2^64 (raw patterns)
-                    v0 = (long long)((unsigned long long)v0 + (unsigned long long)u0);
-                    v1 = (long long)((unsigned long long)v1 + (unsigned long long)u1);
-                    v2 = (long long)((unsigned long long)v2 + (unsigned long long)u2);
-                    v3 = (long long)((unsigned long long)v3 + (unsigned long long)u3);
-                    v4 = (long long)((unsigned long long)v4 + (unsigned long long)u4);
-                    v5 = (long long)((unsigned long long)v5 + (unsigned long long)u5);
+                if (g < 0) {
+                    VA = cat2(sVa[ia], sVb[ia]); WA = cat2(sWa[ia], sWb[ia]); ra = sR[ia];
+                    VB = cat2(sVa[ib], sVb[ib]); WB = cat2(sWa[ib], sWb[ib]); rb = sR[ib];
+                } else {         // cross-tile partner: from global memory (the own particle too: L1)
+                    const int64_t me = p0 + o, ga = isB ? g : me, gb = isB ? me : g;
+                    VA = ld4g(&vin[ga]); WA = ld4g(&win[ga]); ra = __ldg(&rad[ga]);
+                    VB = ld4g(&vin[gb]); WB = ld4g(&win[gb]); rb = __ldg(&rad[gb]);
                 }
             }
-            const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1);
-            if (seg_end) {
-                unsigned long long *A0 = reinterpret_cast<unsigned long long *>(&sAcc[0][0]);
-                if (SWEEP_RR && (sstart == 0 || lane == 31)) {   // may continue in another warp's chunk
-                    atomicAdd(&A0[0 * TT + o], (unsigned long long)v0); atomicAdd(&A0[1 * TT + o], (unsigned long long)v1);
-                    atomicAdd(&A0[2 * TT + o], (unsigned long long)v2); atomicAdd(&A0[3 * TT + o], (unsigned long long)v3);
-                    atomicAdd(&A0[4 * TT + o], (unsigned long long)v4); atomicAdd(&A0[5 * TT + o], (unsigned long long)v5);
-                } else {      // the particle's items all lie in this chunk: one plain add
-                    A0[0 * TT + o] += (unsigned long long)v0; A0[1 * TT + o] += (unsigned long long)v1;
-                    A0[2 * TT + o] += (unsigned long long)v2; A0[3 * TT + o] += (unsigned long long)v3;
-                    A0[4 * TT + o] += (unsigned long long)v4; A0[5 * TT + o] += (unsigned long long)v5;
-                }
+            const d3 n = mk(clr_low(cr.x), clr_low(cr.y), cr.z);
+            const double delta = crec_delta(cr), bias = q.b.w;
+            const double Rs = ext ? ra : rstar(ra, rb);
+            const double S = IMPACT ? 0.0 : (sp.hertz ? sp.Cs * rsqrt64_1(2.0 * Rs * delta) : sp.Cs);   // R4
+            const double la = ra - 0.5 * delta, lb = ext ? 0.0 : rb - 0.5 * delta;
+            const ContactOutT<double, double> c = contact_core_t<double, double>(
+                VA, WA, VB, WB, mt, n, mr * Rs, S, bias, la, lb, q.a.x, mk(q.a.y, q.a.z, q.a.w), mk(q.b.x, q.b.y, q.b.z),
+                sp.rolling_dims);
+            double *po = reinterpret_cast<double *>(Pout + k);
+            stg4d(po, c.pn, c.pt[0], c.pt[1], c.pt[2]);
+            stg4d(po + 4, c.pr[0], c.pr[1], c.pr[2], bias);
+            // shares: body a gets -(L), -(la n x dPt + dPr); body b gets +L, -lb n x dPt + dPr
+            bool bad = false;
+            if (intra) {   // body b of an intra-tile contact: its slot (stored first: fewer live registers)
+                const double2 sg = sSig[pl];
+                const Fx6 ot = fx6(c.L, share_b(lb, c.nxdPt, c.dPr), sg.x, sg.y, bad);
+                const int sl = (int)((meta >> IT_SLOT_SHIFT) & IT_SLOT_MASK);
+                sSlot[3 * sl] = make_longlong2(ot.v[0], ot.v[1]);
+                sSlot[3 * sl + 1] = make_longlong2(ot.v[2], ot.v[3]);
+                sSlot[3 * sl + 2] = make_longlong2(ot.v[4], ot.v[5]);
+                if (bad) atomicOr(&sBad[pl], 1);
+            }
+            const double2 ss = sSig[o];
+            const d3 Ls = isB ? c.L : mk(-c.L.x, -c.L.y, -c.L.z);
+            const d3 As = isB ? share_b(lb, c.nxdPt, c.dPr) : share_a(la, c.nxdPt, c.dPr);
+            const Fx6 me6 = fx6(Ls, As, ss.x, ss.y, bad);
+            v0 = me6.v[0]; v1 = me6.v[1]; v2 = me6.v[2]; v3 = me6.v[3]; v4 = me6.v[4]; v5 = me6.v[5];
+            if (bad) atomicOr(&sBad[o], 1);
+        }
+        // segmented sum of the self shares (items are grouped by owner): exact int64
+        const int dist = valid ? lane - sstart : 0;
+        const int maxd = __reduce_max_sync(0xffffffffu, dist);
+        for (int d = 1; d <= maxd; d <<= 1) {
+            const long long u0 = __shfl_up_sync(0xffffffffu, v0, d), u1 = __shfl_up_sync(0xffffffffu, v1, d);
+            const long long u2 = __shfl_up_sync(0xffffffffu, v2, d), u3 = __shfl_up_sync(0xffffffffu, v3, d);
+            const long long u4 = __shfl_up_sync(0xffffffffu, v4, d), u5 = __shfl_up_sync(0xffffffffu, v5, d);
+            if (lane - d >= sstart) {     // mod 2^64 (raw patterns)
+                v0 = (long long)((unsigned long long)v0 + (unsigned long long)u0);
+                v1 = (long long)((unsigned long long)v1 + (unsigned long long)u1);
+                v2 = (long long)((unsigned long long)v2 + (unsigned long long)u2);
+                v3 = (long long)((unsigned long long)v3 + (unsigned long long)u3);
+                v4 = (long long)((unsigned long long)v4 + (unsigned long long)u4);
+                v5 = (long long)((unsigned long long)v5 + (unsigned long long)u5);
             }
         }
-        __syncthreads();
-        if (t < np) {
-            double4 V = cat2(sVa[t], sVb[t]), W = cat2(sWa[t], sWb[t]);
-            const uint32_t in = B.in[t], is = in & 0xFFFFu, ic = in >> 16;
-            const uint32_t cnt = (B.is[t + 1] - B.is[t]) + ic;      // contacts of the particle (mass splitting)
-            if (cnt) {
-                long long a[6];
-#pragma unroll
-                for (int f = 0; f < 6; f++) a[f] = sAcc[f][t];
-                for (uint32_t s = is; s < is + ic; s++) {
-                    const longlong2 x0 = sSlot[3 * s], x1 = sSlot[3 * s + 1], x2 = sSlot[3 * s + 2];
-                    const long long x[6] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y};
-#pragma unroll
-                    for (int f = 0; f < 6; f++) a[f] = (long long)((unsigned long long)a[f] + (unsigned long long)x[f]);
-                }
-                const unsigned long long mc = (unsigned long long)cnt * (unsigned long long)FX_MAGIC_BITS;
-#pragma unroll
-                for (int f = 0; f < 6; f++) a[f] = (long long)((unsigned long long)a[f] - mc);
-                // body update with the real masses (1/m = (c/m)/c): the mass-splitting average
-                const double2 sg = sSig[t];
-                const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
-                const double qL = (1.0 / sg.x) * im, qA = (1.0 / sg.y) * iI;   // 1/s exact (powers of two)
-                V.x += (double)a[0] * qL; V.y += (double)a[1] * qL; V.z += (double)a[2] * qL;
-                W.x += (double)a[3] * qA; W.y += (double)a[4] * qA; W.z += (double)a[5] * qA;
-                if (sBad[t]) { V.x = __longlong_as_double(0x7FF8000000000000LL); }
-            }
-            st4g(&vout[p0 + t], V);
-            st4g(&wout[p0 + t], W);
+        const bool seg_end = valid && (lane == 31 || ((smask >> (lane + 1)) & 1u) || k + 1 >= k1);
+        if (seg_end) {
+            unsigned long long *A0 = reinterpret_cast<unsigned long long *>(&sAcc[0][0]);
+            A0[0 * TT + o] += (unsigned long long)v0; A0[1 * TT + o] += (unsigned long long)v1;
+            A0[2 * TT + o] += (unsigned long long)v2; A0[3 * TT + o] += (unsigned long long)v3;
+            A0[4 * TT + o] += (unsigned long long)v4; A0[5 * TT + o] += (unsigned long long)v5;
         }
-        __syncthreads();                  // sSlot, sAcc, sSig reused by the next tile
-        if (!SWEEP_PERSIST && nt < ntiles)
-            stage_tile(sBuf[0], nt * TT, (int)min((int64_t)TT, N - nt * TT), t, vin, win, rad, istart, pin);
+    }
+    __syncthreads();
+    if (t < np) {
+        double4 V = cat2(sVa[t], sVb[t]), W = cat2(sWa[t], sWb[t]);
+        const uint32_t in = B.in[t], is = in & 0xFFFFu, ic = in >> 16;
+        const uint32_t cnt = (B.is[t + 1] - B.is[t]) + ic;      // contacts of the particle (mass splitting)
+        if (cnt) {
+            long long a[6];
+#pragma unroll
+            for (int f = 0; f < 6; f++) a[f] = sAcc[f][t];
+            for (uint32_t s = is; s < is + ic; s++) {
+                const longlong2 x0 = sSlot[3 * s], x1 = sSlot[3 * s + 1], x2 = sSlot[3 * s + 2];
+                const long long x[6] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y};
+#pragma unroll
+                for (int f = 0; f < 6; f++) a[f] = (long long)((unsigned long long)a[f] + (unsigned long long)x[f]);
+            }
+            const unsigned long long mc = (unsigned long long)cnt * (unsigned long long)FX_MAGIC_BITS;
+#pragma unroll
+            for (int f = 0; f < 6; f++) a[f] = (long long)((unsigned long long)a[f] - mc);
+            // body update with the real masses (1/m = (c/m)/c): the mass-splitting average
+            const double2 sg = sSig[t];
+            const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
+            const double qL = (1.0 / sg.x) * im, qA = (1.0 / sg.y) * iI;   // 1/s exact (powers of two)
+            V.x += (double)a[0] * qL; V.y += (double)a[1] * qL; V.z += (double)a[2] * qL;
+            W.x += (double)a[3] * qA; W.y += (double)a[4] * qA; W.z += (double)a[5] * qA;
+            if (sBad[t]) { V.x = __longlong_as_double(0x7FF8000000000000LL); }
+        }
+        st4g(&vout[p0 + t], V);
+        st4g(&wout[p0 + t], W);
     }
 }
 
@@ -375,24 +356,25 @@ void launch_sweep_items(bool impact, int64_t N, const double4 *vin, const double
                         const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s)
 {
     if (!N) return;
-    constexpr int dyn = (SWEEP_PERSIST ? 2 : 1) * (int)sizeof(StageBuf) + 3 * SLOT_CAP * (int)sizeof(longlong2);
-    static int grid_cap = [] {
+    constexpr int dyn = (int)sizeof(StageBuf) + 3 * SLOT_CAP * (int)sizeof(longlong2);
+    static const bool attr = [] {
         cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
-        int dev = 0, sms = 148, per = SWEEP_MINB;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, TT, dyn);
-        return sms * (per > 0 ? per : 1);
+        if (getenv("DEM_DEBUG")) {
+            int per = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, TT, dyn);
+            fprintf(stderr, "k_sweep: %d B dynamic smem, %d CTAs per SM\n", dyn, per);
+        }
+        return true;
     }();
-    const int64_t ntiles = (N + TT - 1) / TT;
-    const unsigned gb = (unsigned)(SWEEP_PERSIST ? std::min<int64_t>(ntiles, grid_cap) : ntiles);
+    (void)attr;
+    const unsigned ntiles = (unsigned)((N + TT - 1) / TT);
     if (impact)
-        k_sweep<true><<<gb, TT, dyn, s>>>(N, ntiles, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd,
-                                          pl.wrange, sp);
+        k_sweep<true><<<ntiles, TT, dyn, s>>>(N, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd,
+                                              pl.wrange, sp);
     else
-        k_sweep<false><<<gb, TT, dyn, s>>>(N, ntiles, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd,
-                                           pl.wrange, sp);
+        k_sweep<false><<<ntiles, TT, dyn, s>>>(N, vin, win, rad, vout, wout, pl.istart, pl.pin, rec, Pin, Pout, bnd,
+                                               pl.wrange, sp);
 }
 
 // ================================================================== the tile plan (per step)
