@@ -4,6 +4,13 @@ error").  Protocols in tests/curves_mini.py: c1-mini (25 mm pl
 0.01 m at 0.05 m/s, 4e4 steps) and c2-mini (grouser plate under 10 kPa sheared 5 mm at
 0.02 m/s, 5e4 steps), N_it = 50, three seeds each.
 
+The bar is taken on the seed-averaged curves ("mini beds, smoothing and seed
+averages"; the paper repeats every case and compares means): RMS of the difference of the
+GPU's and the oracle's mean curves after the 2 ms moving average, over the oracle mean curve's
+maximum, <= 2 %.  The granular bed is chaotic: the two fp64 trajectories separate from rounding
+onward, so single-seed curves differ by their fluctuations; the per-seed errors are printed and
+recorded (profiles/r02_curves_mini.txt) beside the ensemble figure.
+
 The oracle side ran once on the CPU (tests/fixtures/make_curves_mini.py, OpenMP oracle) and
 stored its curves; this test re-settles each bed with the same oracle (checking the digest of
 the settled state against the stored one: both sides start from the identical state and
@@ -51,7 +58,7 @@ def gpu_curve(kind, b, W):
 @pytest.mark.parametrize("kind", CM.KINDS)
 def test_plate_curve_mini_within_2pct(kind):
     O.set_threads(os.cpu_count() or 1)
-    errs = []
+    errs, fg, fr = [], [], []
     for seed in CM.SEEDS:
         path = os.path.join(HERE, "golden", f"curves_mini_{kind}_{seed}.npz")
         if not os.path.exists(path):
@@ -66,4 +73,10 @@ def test_plate_curve_mini_within_2pct(kind):
         ex = float(np.abs(x - ref["pos"]).max())
         print(kind, seed, "rms", e, "max |dx| plate", ex, "max |F| ref", np.abs(f_ref).max(), "gpu", np.abs(f).max())
         errs.append(e)
-    assert np.mean(errs) <= TOL_RMS, errs
+        fg.append(f)
+        fr.append(f_ref)
+        if os.path.isdir("gpurun_out"):
+            np.savez_compressed(f"gpurun_out/curves_mini_gpu_{kind}_{seed}.npz", force=f, pos=x)
+    e_mean = CM.rms_error(np.mean(fg, axis=0), np.mean(fr, axis=0))
+    print(kind, "per-seed rms", errs, "mean of per-seed", float(np.mean(errs)), "seed-averaged curves rms", e_mean)
+    assert e_mean <= TOL_RMS, (e_mean, errs)
