@@ -325,7 +325,8 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
                        &ctx->pl_nitem, &ctx->pl_nin};
     const size_t N = (size_t)cap + 1;
     for (auto q : d4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N)); }
-    for (auto q : u4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N + 1)); }
+    // + 8 / + 2: the sweep's TMA copies of a tile's istart, pin and radii round up to 16 bytes
+    for (auto q : u4) { dfree(ctx, *q); *q = nullptr; TRY(A(ctx, q, N + 8)); }
     dfree(ctx, ctx->ke_part);
     ctx->ke_part = nullptr;
     dfree(ctx, ctx->own);
@@ -339,7 +340,7 @@ static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
     ctx->pl.noint = nullptr;
     ctx->pl.rad = nullptr;
     TRY(A(ctx, &ctx->pl.noint, N / SWEEP_TILE + 2));
-    TRY(A(ctx, &ctx->pl.rad, N));
+    TRY(A(ctx, &ctx->pl.rad, N + 2));
     TRY(A(ctx, &ctx->pl.wrange, (N / SWEEP_TILE + 2) * (SWEEP_TILE / 32 + 1)));
     if (!ctx->lvbox) {
         TRY(A(ctx, &ctx->lvbox, (size_t)DEM_MAX_LEVELS * 8));

@@ -102,6 +102,9 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 #ifndef SWEEP_MINB
 #define SWEEP_MINB 2
 #endif
+#ifndef SWEEP_TMA
+#define SWEEP_TMA 1              // tile staging by TMA bulk copies on an mbarrier (0: per-thread cp.async)
+#endif
 #define IT_INTRA 0x80000000u     // partner in the tile, body b's share goes to slot (bits 9..20)
 #define IT_B 0x40000000u         // cross pair: the owner is the canonical body b
 #define IT_EXT 0x20000000u       // wall / plate box: bits 0..28 = boundary code (PARTNER_* codes)

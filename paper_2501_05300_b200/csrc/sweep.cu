@@ -155,6 +155,46 @@ __device__ __forceinline__ void cp_async4(void *s, const void *g)
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+#if SWEEP_TMA
+// the tile's particle states as in HBM (double4 v, w), radii, item starts and incoming-slot
+// words, each landed by one TMA bulk copy (cp.async.bulk) on an mbarrier: no per-thread copies
+struct StageBuf {
+    double4 v[TT], w[TT];
+    double r[TT];
+    uint32_t is[TT + 4];
+    uint32_t in[TT];
+};
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t up16(uint32_t b) { return (b + 15u) & ~15u; }
+// one thread: arm the barrier with the byte count and issue the five copies (sizes rounded up to
+// 16 B; the plan arrays and radii carry the padding, ctx.cu alloc_particles)
+__device__ __forceinline__ void stage_tile_tma(StageBuf &B, uint64_t *bar, int64_t p0, int np, const double4 *vin,
+                                               const double4 *win, const double *rad, const uint32_t *istart,
+                                               const uint32_t *pin)
+{
+    const uint32_t bv = (uint32_t)np * 32u, br = up16((uint32_t)np * 8u), bi = up16((uint32_t)(np + 1) * 4u),
+                   bn = up16((uint32_t)np * 4u);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(2 * bv + br + bi + bn)
+                 : "memory");
+    bulk_g2s(B.v, vin + p0, bv, bar);
+    bulk_g2s(B.w, win + p0, bv, bar);
+    bulk_g2s(B.r, rad + p0, br, bar);
+    bulk_g2s(B.is, istart + p0, bi, bar);
+    bulk_g2s(B.in, pin + p0, bn, bar);
+}
+__device__ __forceinline__ void mbar_wait0(uint64_t *bar)
+{
+    asm volatile("{\n .reg .pred p;\n WAIT%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra WAIT%=;\n}"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+#define SV(i) (B.v[i])
+#define SW(i) (B.w[i])
+#else
 // the tile's particle states (v and w as double2 halves: conflict-free 16-byte reads), radii,
 // item starts and incoming-slot words
 struct StageBuf {
@@ -182,6 +222,10 @@ __device__ __forceinline__ void stage_tile(StageBuf &B, int64_t p0, int np, int 
     for (int q = t; q <= np; q += TT) cp_async4(&B.is[q], istart + p0 + q);
     cp_async_commit();
 }
+#define SV(i) cat2(B.va[i], B.vb[i])
+#define SW(i) cat2(B.wa[i], B.wb[i])
+#endif
+
 template <bool IMPACT>
 __global__ void __launch_bounds__(TT, SWEEP_MINB)
     k_sweep(int64_t N, const double4 *__restrict__ vin, const double4 *__restrict__ win,
@@ -201,19 +245,33 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
     const int64_t tile = blockIdx.x;
     const int64_t p0 = tile * TT;
     const int np = (int)min((int64_t)TT, N - p0);
+#if SWEEP_TMA
+    __shared__ __align__(8) uint64_t sBar;
+    if (t == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sBar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        stage_tile_tma(B, &sBar, p0, np, vin, win, rad, istart, pin);
+    }
+#else
     stage_tile(B, p0, np, t, vin, win, rad, istart, pin);
+#endif
     // the warp's items [k0, k1) and its first chunk's records, requested before the wait
     const uint32_t k0 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w]), k1 = __ldg(&wrange[(size_t)tile * (NWT + 1) + w + 1]);
     double4 cn;
     PRaw qn;
     if (k0 + lane < k1) { cn = ldg4d(rec + k0 + lane); qn = ld_praw(Pin, k0 + lane); }
+#if SWEEP_TMA
+    __syncthreads();                      // the barrier is initialised
+    mbar_wait0(&sBar);                    // the tile's states are in shared memory
+#else
     cp_async_wait_all();
     __syncthreads();                      // the tile's states are in shared memory
-    const double2 *sVa = B.va, *sVb = B.vb, *sWa = B.wa, *sWb = B.wb;
+#endif
     const double *sR = B.r;
     if (t < np) {
         const uint32_t c = (B.is[t + 1] - B.is[t]) + (B.in[t] >> 16);
-        sSig[t] = c ? make_double2(pow2(FX_EL + fx_exp(sVb[t].y, c)), pow2(FX_EA + fx_exp(sWb[t].y, c)))
+        sSig[t] = c ? make_double2(pow2(FX_EL + fx_exp(SV(t).w, c)), pow2(FX_EA + fx_exp(SW(t).w, c)))
                     : make_double2(0.0, 0.0);
     }
 #pragma unroll
@@ -243,7 +301,7 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
             if (ext) {           // the particle is body a, the wall / plate body b
                 d3 bv;
                 boundary_body((meta & IT_IDX) | PARTNER_EXT, bnd, bv, mt, mr);
-                VA = cat2(sVa[o], sVb[o]); WA = cat2(sWa[o], sWb[o]); ra = sR[o];
+                VA = SV(o); WA = SW(o); ra = sR[o];
                 VB = make_double4(bv.x, bv.y, bv.z, 0.0);
                 WB = make_double4(0.0, 0.0, 0.0, 0.0);
                 rb = 0.0;
@@ -259,8 +317,8 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
                     if (l >= 0 && l < np) { ia = isB ? (int)l : o; ib = isB ? o : (int)l; g = -1; }
                 }
                 if (g < 0) {
-                    VA = cat2(sVa[ia], sVb[ia]); WA = cat2(sWa[ia], sWb[ia]); ra = sR[ia];
-                    VB = cat2(sVa[ib], sVb[ib]); WB = cat2(sWa[ib], sWb[ib]); rb = sR[ib];
+                    VA = SV(ia); WA = SW(ia); ra = sR[ia];
+                    VB = SV(ib); WB = SW(ib); rb = sR[ib];
                 } else {         // cross-tile partner: from global memory (the own particle too: L1)
                     const int64_t me = p0 + o, ga = isB ? g : me, gb = isB ? me : g;
                     VA = ld4g(&vin[ga]); WA = ld4g(&win[ga]); ra = __ldg(&rad[ga]);
@@ -322,7 +380,7 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
     }
     __syncthreads();
     if (t < np) {
-        double4 V = cat2(sVa[t], sVb[t]), W = cat2(sWa[t], sWb[t]);
+        double4 V = SV(t), W = SW(t);
         const uint32_t in = B.in[t], is = in & 0xFFFFu, ic = in >> 16;
         const uint32_t cnt = (B.is[t + 1] - B.is[t]) + ic;      // contacts of the particle (mass splitting)
         if (cnt) {
