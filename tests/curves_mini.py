@@ -75,6 +75,14 @@ def plate(kind: str, x: np.ndarray, r: np.ndarray, box_hi):
     return lo, hi, pos, 7850.0 * vol, drives
 
 
+def plate_coupling(kind: str) -> int:
+    """c2's plate rides on a 10 kPa force axis: staggered coupling (R18) lets the 0.5 kg plate
+    take each step's full rigid-body reaction and bounce (measured: its contact count falls from
+    ~430 to ~5 within 0.1 s), so c2 couples it monolithically (R18b, tools in the same
+    MCP).  c1's plate is kinematic: the coupling does not apply."""
+    return 1 if kind == "c2" else 0
+
+
 def curve_axis(kind: str) -> int:
     return 2 if kind == "c1" else 0
 

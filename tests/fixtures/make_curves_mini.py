@@ -48,7 +48,7 @@ def run(kind, seed):
     W.plates = (O.Plate * 1)(P)
     W.n_plates = 1
     W.time = 0.0
-    p = O.make_params(h=CM.DT, n_it=CM.N_IT)
+    p = O.make_params(h=CM.DT, n_it=CM.N_IT, plate_coupling=CM.plate_coupling(kind))
     ax = CM.curve_axis(kind)
     n = CM.N_STEPS[kind]
     f = np.empty(n)

@@ -34,7 +34,8 @@ TOL_RMS = 0.02
 def gpu_curve(kind, b, W):
     from paper_2501_05300_b200 import dem
     box = dict(lo=b.box_lo, hi=b.box_hi, wall_mask=CM.WALL_MASK)
-    g = dem.Bed(W.x, W.r, W.v, W.w, W.gid, solver=dict(dt=CM.DT, n_iter=CM.N_IT), box=box)
+    g = dem.Bed(W.x, W.r, W.v, W.w, W.gid, solver=dict(dt=CM.DT, n_iter=CM.N_IT, plate_coupling=CM.plate_coupling(kind)),
+                box=box)
     try:
         g.set_state(W.x, W.r, W.v, W.w, W.gid, hist=W.hist)
         lo, hi, pos, mass, drives = CM.plate(kind, W.x, W.r, b.box_hi)
