@@ -6,8 +6,13 @@ P:166-202).
 * a mini box triaxial test (0.05 m cube, 2.5 mm spheres, servo (K = 5e-5) consolidation to
   sigma_3 then shear at 0.02 m/s to 8 % strain) at sigma_3 = 5, 15, 25 kPa: the servo holds the confinement,
   sigma_1 rises above it, and the Mohr-Coulomb angle of the frictional material exceeds the
-  frictionless one (frictionless particles -> small angle).
+  frictionless one (frictionless particles -> small angle); the peak
+  deviators and the friction angle agree with the same protocol run on the fp64 oracle
+  (tests/golden/triaxial_mini_oracle.json).
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -90,6 +95,15 @@ def test_mini_triaxial_mohr_coulomb():
     phi0, c0 = TX.mohr_coulomb_fit(peaks0)
     print("frictional phi", phi, "c", c, "peaks", peaks)
     print("frictionless phi", phi0, "c", c0, "peaks", peaks0)
+    # the same servo protocol driving the fp64 oracle (tests/fixtures/make_triaxial_oracle.py,
+    # tests/oracle_triaxial.py).  The lattice sample does not amplify rounding: measured peak
+    # deviators agree to 6e-6 and phi to 2e-5 degrees; bars 1e-4 relative and 1e-3 degrees
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "triaxial_mini_oracle.json")))
+    for (s3, s1), pk_ref in zip(peaks, ref["peak"]):
+        print("sigma3", s3, "peak deviator gpu", s1 - s3, "oracle", pk_ref)
+        assert abs((s1 - s3) - pk_ref) <= 1e-4 * pk_ref
+    print("phi gpu", phi, "oracle", ref["phi_deg"])
+    assert abs(phi - ref["phi_deg"]) <= 1e-3
     # measured: 20.0 deg (c = 269 Pa) frictional, 3.3 deg frictionless; the paper's 34 deg (Table 1)
     # needs its settled random beds of ~10^4 particles and 5 mm/s (not this 600-sphere lattice)
     assert 15.0 < phi < 50.0
