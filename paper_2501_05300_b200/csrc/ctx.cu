@@ -60,7 +60,7 @@ struct dem_ctx {
     uint64_t ncells = 0, cap_cells = 0;
     uint32_t *cstart = nullptr, *cend = nullptr;
     // candidates
-    int64_t ncand = 0, cap_cand = 0;
+    int64_t ncand = 0, cap_cand = 0, cap_c = 0;   // candidate / contact capacities
     uint2 *cand = nullptr;
     uint32_t *co_start = nullptr, *ct_cnt = nullptr, *ct_start = nullptr, *ct_cursor = nullptr, *ct_list = nullptr;
     P4 *Pca = nullptr, *Pcb = nullptr;
@@ -72,7 +72,7 @@ struct dem_ctx {
     R4 *row = nullptr, *row_imp = nullptr;
     double *cdel = nullptr;
     P4 *Pwa = nullptr, *Pwb = nullptr;            // warm start
-    P4 *Pa[2] = {nullptr, nullptr}, *Pb[2] = {nullptr, nullptr};
+    P4 *Pa[2] = {nullptr, nullptr}, *Pb[2] = {nullptr, nullptr};   // [0] only (the final impulses)
     P4 *Pfa = nullptr, *Pfb = nullptr;            // final impulses of the last step
     uint32_t *ccand = nullptr;
     // incidence
@@ -379,23 +379,36 @@ static dem_status ensure_cand(dem_ctx *ctx, int64_t n)
     TRY(regrow(ctx, &ctx->cand, cap)); TRY(regrow(ctx, &ctx->ct_list, cap));
     TRY(regrow(ctx, &ctx->Pca, cap)); TRY(regrow(ctx, &ctx->Pcb, cap));
     TRY(regrow(ctx, &ctx->cflag, cap + 1)); TRY(regrow(ctx, &ctx->cscan, cap + 1));
-    TRY(regrow(ctx, &ctx->cij, cap)); TRY(regrow(ctx, &ctx->geo, cap)); TRY(regrow(ctx, &ctx->row, cap)); TRY(regrow(ctx, &ctx->cdel, cap));
-    TRY(regrow(ctx, &ctx->row_imp, cap)); TRY(regrow(ctx, &ctx->Pwa, cap)); TRY(regrow(ctx, &ctx->Pwb, cap));
-    for (int k = 0; k < 2; k++) { TRY(regrow(ctx, &ctx->Pa[k], cap)); TRY(regrow(ctx, &ctx->Pb[k], cap)); }
-    TRY(regrow(ctx, &ctx->ccand, cap));
-    TRY(regrow(ctx, &ctx->pl.slot_of, cap));
-    TRY(regrow(ctx, &ctx->plist, cap + 1));
-    TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
-    if (ctx->sol.ordering == 1 || ctx->gs_cij) {
-        TRY(regrow(ctx, &ctx->gs_cij, cap)); TRY(regrow(ctx, &ctx->gs_geo, cap)); TRY(regrow(ctx, &ctx->gs_row, cap));
-        TRY(regrow(ctx, &ctx->gs_Pa, cap)); TRY(regrow(ctx, &ctx->gs_Pb, cap));
-    }
     if (!ctx->gs_scr) TRY(A(ctx, &ctx->gs_scr, 260));
-    TRY(regrow(ctx, &ctx->inc, 2 * cap));
     ctx->cap_cand = cap;
     ctx->nc = 0;
     ctx->have_step = false;
     return ensure_keys(ctx, std::max<int64_t>(cap, ctx->N));
+}
+
+// the contact-indexed arrays, sized by the contact count of the step (about half the candidates
+// with the Verlet skin) rather than by the candidates; contents are dead at the point of call
+// (before the compaction), so a regrow keeps nothing
+static dem_status ensure_contacts(dem_ctx *ctx, int64_t n)
+{
+    if (n <= ctx->cap_c) return DEM_OK;
+    int64_t cap = std::max<int64_t>(n + n / 4, 1024);
+    TRY(regrow(ctx, &ctx->cij, cap)); TRY(regrow(ctx, &ctx->geo, cap)); TRY(regrow(ctx, &ctx->row, cap)); TRY(regrow(ctx, &ctx->cdel, cap));
+    TRY(regrow(ctx, &ctx->row_imp, cap)); TRY(regrow(ctx, &ctx->Pwa, cap)); TRY(regrow(ctx, &ctx->Pwb, cap));
+    TRY(regrow(ctx, &ctx->Pa[0], cap)); TRY(regrow(ctx, &ctx->Pb[0], cap));   // final impulses, contact order
+    ctx->Pfa = ctx->Pa[0];
+    ctx->Pfb = ctx->Pb[0];
+    TRY(regrow(ctx, &ctx->ccand, cap));
+    TRY(regrow(ctx, &ctx->pl.slot_of, cap));
+    TRY(regrow(ctx, &ctx->plist, cap + 1));
+    if (ctx->sol.ordering == 1 || ctx->gs_cij) {   // Gauss-Seidel buffers only when that ordering is used
+        TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
+        TRY(regrow(ctx, &ctx->gs_cij, cap)); TRY(regrow(ctx, &ctx->gs_geo, cap)); TRY(regrow(ctx, &ctx->gs_row, cap));
+        TRY(regrow(ctx, &ctx->gs_Pa, cap)); TRY(regrow(ctx, &ctx->gs_Pb, cap));
+    }
+    TRY(regrow(ctx, &ctx->inc, 2 * cap));
+    ctx->cap_c = cap;
+    return DEM_OK;
 }
 
 // ------------------------------------------------------------------ level bounding boxes
@@ -1054,6 +1067,7 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     nc = *ctx->hnc;
     dem_status cst = DEM_OK;
     if (nc > INC_CMASK) { ctx->err = "more than 2^31 contacts on one rank"; cst = DEM_ERR_OOM; }
+    else cst = ensure_contacts(ctx, std::max<int64_t>(nc, 1));
     TRY(agree(ctx, cst));
     ctx->nc = nc;
     launch_compact(ncand, ctx->cand, ctx->cflag, ctx->cscan, ctx->pos, ctx->db, sp, ctx->Pca, ctx->Pcb, ctx->cij,
@@ -1101,16 +1115,17 @@ static dem_status step_once(dem_ctx *ctx, dem_step_report *rep)
     const int n_imp = ctx->sol.n_iter_impact > 0 ? ctx->sol.n_iter_impact : ctx->sol.n_iter;
     const bool gs = ctx->sol.ordering == 1;
     if (gs) {
+        if (!ctx->gs_cij) {   // ordering switched on after the buffers were sized
+            const int64_t cap = ctx->cap_c;
+            TRY(regrow(ctx, &ctx->gs_key, cap)); TRY(regrow(ctx, &ctx->gs_col, cap)); TRY(regrow(ctx, &ctx->gs_ord, cap));
+            TRY(regrow(ctx, &ctx->gs_cij, cap)); TRY(regrow(ctx, &ctx->gs_geo, cap)); TRY(regrow(ctx, &ctx->gs_row, cap));
+            TRY(regrow(ctx, &ctx->gs_Pa, cap)); TRY(regrow(ctx, &ctx->gs_Pb, cap));
+        }
         // colour the contact graph (priority SplitMix64(key): the oracle's greedy colouring)
         const int ncol = gs_color(nc, ctx->cij, ctx->gid, ctx->inc_start, ctx->inc, ctx->gs_key, ctx->gs_col, ctx->keys,
                                   ctx->vals, ctx->sort_tmp, ctx->gs_scr, ctx->gs_cstart, s, &ctx->launches);
         if (ncol < 0) { ctx->err = "Gauss-Seidel colouring needs more than 256 colours"; return DEM_ERR_INVALID; }
         if (nc) CK(cudaMemcpyAsync(ctx->gs_ord, ctx->vals[0], nc * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        if (!ctx->gs_cij) {   // ordering switched on after the buffers were sized
-            const int64_t cap = ctx->cap_cand;
-            TRY(regrow(ctx, &ctx->gs_cij, cap)); TRY(regrow(ctx, &ctx->gs_geo, cap)); TRY(regrow(ctx, &ctx->gs_row, cap));
-            TRY(regrow(ctx, &ctx->gs_Pa, cap)); TRY(regrow(ctx, &ctx->gs_Pb, cap));
-        }
         gs_gather(nc, ctx->gs_ord, ctx->cij, ctx->geo, nullptr, nullptr, nullptr, ctx->gs_cij, ctx->gs_geo, nullptr,
                   nullptr, nullptr, s);
         ctx->launches += 1;
