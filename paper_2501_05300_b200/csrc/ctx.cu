@@ -43,9 +43,10 @@ struct dem_ctx {
     bool lv_present[DEM_MAX_LEVELS] = {false};
 
     // particles (sorted order)
-    double4 *pos = nullptr, *pos2 = nullptr, *vel[2] = {nullptr, nullptr}, *ang[2] = {nullptr, nullptr};
-    double4 *vel2 = nullptr, *ang2 = nullptr, *xref = nullptr, *pos_prev = nullptr, *vel_prev = nullptr,
-            *ang_prev = nullptr;
+    double4 *pos = nullptr, *vel[2] = {nullptr, nullptr}, *ang[2] = {nullptr, nullptr};
+    // *_prev: the state at the step start (rollback); outside that window they are scratch (the
+    // rebuild's permutation target, the force evaluation, the sweep benchmark)
+    double4 *xref = nullptr, *pos_prev = nullptr, *vel_prev = nullptr, *ang_prev = nullptr;
     uint32_t *gid = nullptr, *gid2 = nullptr, *gid_sorted = nullptr;
     int cur = 0;
     // sort / scan scratch
@@ -318,8 +319,8 @@ static dem_status upload_boundary(dem_ctx *ctx)
 // (re)allocate the particle-sized arrays for capacity cap (contents are not preserved)
 static dem_status alloc_particles(dem_ctx *ctx, int64_t cap)
 {
-    double4 **d4[] = {&ctx->pos, &ctx->pos2, &ctx->vel[0], &ctx->vel[1], &ctx->ang[0], &ctx->ang[1], &ctx->vel2,
-                      &ctx->ang2, &ctx->xref, &ctx->pos_prev, &ctx->vel_prev, &ctx->ang_prev};
+    double4 **d4[] = {&ctx->pos, &ctx->vel[0], &ctx->vel[1], &ctx->ang[0], &ctx->ang[1], &ctx->xref, &ctx->pos_prev,
+                      &ctx->vel_prev, &ctx->ang_prev};
     uint32_t **u4[] = {&ctx->gid, &ctx->gid2, &ctx->gid_sorted, &ctx->co_start, &ctx->ct_cnt, &ctx->ct_start,
                        &ctx->ct_cursor, &ctx->inc_cnt, &ctx->inc_start, &ctx->pl.istart, &ctx->pl.pin,
                        &ctx->pl_nitem, &ctx->pl_nin};
@@ -872,11 +873,12 @@ static dem_status rebuild(dem_ctx *ctx)
         launch_keys(N, ctx->pos, ctx->grid, ctx->keys[0], ctx->vals[0], s);
         const int nbits = 3 * ctx->grid.bits + 3;
         radix_sort_u64(ctx->keys, ctx->vals, N, nbits, ctx->sort_tmp, s, &ctx->launches);
-        launch_permute(N, ctx->vals[0], ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->gid, ctx->pos2, ctx->vel2,
-                       ctx->ang2, ctx->gid2, s);
-        std::swap(ctx->pos, ctx->pos2);
-        std::swap(ctx->vel[ctx->cur], ctx->vel2);
-        std::swap(ctx->ang[ctx->cur], ctx->ang2);
+        // into the *_prev buffers (free until the step copies its start state there)
+        launch_permute(N, ctx->vals[0], ctx->pos, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->gid, ctx->pos_prev,
+                       ctx->vel_prev, ctx->ang_prev, ctx->gid2, s);
+        std::swap(ctx->pos, ctx->pos_prev);
+        std::swap(ctx->vel[ctx->cur], ctx->vel_prev);
+        std::swap(ctx->ang[ctx->cur], ctx->ang_prev);
         std::swap(ctx->gid, ctx->gid2);
         ctx->launches += 2;
         // (b) per-level dense cell tables
@@ -1648,11 +1650,11 @@ dem_status dem_get_forces(dem_ctx *ctx, double *F, double *T, int32_t on_device)
     const int64_t N = ctx->N, Nown = ctx->N_own;
     if (!N) return DEM_OK;
     cudaStream_t s = ctx->s;
-    launch_apply(SWEEP_MODE_FORCES, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel2, ctx->ang2, ctx->inc_start,
+    launch_apply(SWEEP_MODE_FORCES, N, ctx->vel[ctx->cur], ctx->ang[ctx->cur], ctx->vel_prev, ctx->ang_prev, ctx->inc_start,
                  ctx->inc, ctx->geo, ctx->row, ctx->Pfa, ctx->Pfb, ctx->sp, s);
     double *d = nullptr;
     TRY(A(ctx, &d, 6 * N));
-    launch_to_gid_order(N, Nown, OWN(ctx), ctx->gid, ctx->gid_sorted, ctx->vel2, ctx->ang2, nullptr, d, d + 3 * Nown, nullptr, nullptr,
+    launch_to_gid_order(N, Nown, OWN(ctx), ctx->gid, ctx->gid_sorted, ctx->vel_prev, ctx->ang_prev, nullptr, d, d + 3 * Nown, nullptr, nullptr,
                         nullptr, s);
     ctx->launches += 2;
     cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -1793,7 +1795,7 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     const int64_t N = ctx->N;
     cudaStream_t s = ctx->s;
     item_pack(ctx->n_items, ctx->pl, ctx->geo, ctx->cdel, ctx->row, ctx->Pfa, ctx->Pfb, ctx->it_rec, ctx->it_P[0], s);
-    double4 *vb[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel2}, *wb[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang2};
+    double4 *vb[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel_prev}, *wb[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang_prev};
     const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];
     cudaEventRecord(ctx->ev[6], s);
     for (int it = 0; it < n; it++) {
