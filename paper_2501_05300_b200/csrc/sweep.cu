@@ -278,12 +278,12 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
     for (int f = 0; f < 6; f++) sAcc[f][t] = 0;
     sBad[t] = 0;
     __syncthreads();
-    for (uint32_t kb = k0; kb < k1; kb += 32) {
+    // one chunk of 32 items from records (cr, q).  (Unrolling the loop twice, so that the next
+    // chunk's records land in a second register set without copies, measured slower: 3.00 ms vs
+    // 2.80, profiles/r02_sweep_variants.jsonl.)
+    auto chunk = [&](const uint32_t kb, const double4 &cr, const PRaw &q) {
         const uint32_t k = kb + lane;
         const bool valid = k < k1;
-        const double4 cr = cn;
-        const PRaw q = qn;
-        if (kb + 32 + lane < k1) { cn = ldg4d(rec + kb + 32 + lane); qn = ld_praw(Pin, kb + 32 + lane); }   // next chunk in flight
         // segments of the chunk: runs of equal owner (items are grouped by owner)
         const int o = valid ? crec_owner(cr) : -1;
         const int op = __shfl_up_sync(0xffffffffu, o, 1);
@@ -377,6 +377,12 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
             A0[2 * TT + o] += (unsigned long long)v2; A0[3 * TT + o] += (unsigned long long)v3;
             A0[4 * TT + o] += (unsigned long long)v4; A0[5 * TT + o] += (unsigned long long)v5;
         }
+    };
+    for (uint32_t kb = k0; kb < k1; kb += 32) {
+        const double4 cr = cn;
+        const PRaw q = qn;
+        if (kb + 32 + lane < k1) { cn = ldg4d(rec + kb + 32 + lane); qn = ld_praw(Pin, kb + 32 + lane); }   // next chunk in flight
+        chunk(kb, cr, q);
     }
     __syncthreads();
     if (t < np) {
