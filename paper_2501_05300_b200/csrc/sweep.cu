@@ -136,7 +136,7 @@ __device__ __forceinline__ PRaw ld_praw(const PRec *P, uint32_t k)
 // wait on a warp of coarse particles) and walks their items 32 at a time, the next chunk's item
 // records in flight (registers) while the current chunk computes.  Operands are loaded by index
 // straight into their canonical (a, b) slots (no selects): the tile's particles from shared
-// memory, cross-tile pairs from global memory (both bodies: the own particle hits L1/L2).
+// memory, the partner of a cross-tile pair from global memory.
 // Measured and dropped (profiles/r02_sweep_variants.jsonl): the next chunk's cross-tile partners
 // gathered by cp.async into a shared-memory ring (3.55 ms vs 3.03) or prefetched into L1 (3.24),
 // warps taking the tile's chunks round robin with smem atomics at chunk edges (3.17).
@@ -319,10 +319,15 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
                 if (g < 0) {
                     VA = SV(ia); WA = SW(ia); ra = sR[ia];
                     VB = SV(ib); WB = SW(ib); rb = sR[ib];
-                } else {         // cross-tile partner: from global memory (the own particle too: L1)
-                    const int64_t me = p0 + o, ga = isB ? g : me, gb = isB ? me : g;
-                    VA = ld4g(&vin[ga]); WA = ld4g(&win[ga]); ra = __ldg(&rad[ga]);
-                    VB = ld4g(&vin[gb]); WB = ld4g(&win[gb]); rb = __ldg(&rad[gb]);
+                } else {         // cross-tile partner: from global memory
+                    // the own particle from the staged tile, placed by select (the TMA staging
+                    // does not allocate in L1, so a global re-read would go to L2)
+                    const double4 VP = ld4g(&vin[g]), WP = ld4g(&win[g]);
+                    const double rp = __ldg(&rad[g]);
+                    const double4 VO = SV(o), WO = SW(o);
+                    const double ro = sR[o];
+                    VA = isB ? VP : VO; WA = isB ? WP : WO; ra = isB ? rp : ro;
+                    VB = isB ? VO : VP; WB = isB ? WO : WP; rb = isB ? ro : rp;
                 }
             }
             const d3 n = mk(clr_low(cr.x), clr_low(cr.y), cr.z);
