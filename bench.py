@@ -455,8 +455,9 @@ def main():
                    "plate_motion": "kinematic -z 0.05 m/s and +x 0.05 m/s (SURVEY C21: pressed and sheared)"
                    if n_plates else None},
         "value_main_stage_only": value_main,
-        "main_stage_only_note": "particle-steps/s with the impact-stage sweeps' time removed (a settled bed fires it "
-                                "rarely); the timed steps themselves all include it when it fires",
+        "main_stage_only_note": "particle-steps/s with the impact-stage sweeps' time removed, for comparison with "
+                                "plate-free settled beds; with the C21 plates moving at 0.05 m/s new plate contacts "
+                                "fire the impact stage in nearly every step, and the timed steps include it",
         "contacts_per_s": contacts_per_s,
         "contact_sweeps_per_s": tm["contact_sweeps"] / (ms / 1e3) * world,   # rank-local contacts (incl. ghost copies)
         "roofline": {"bound": "hbm", "kernel": "k_gs_color (all colours of a sweep)" if args.ordering == "gs" else "k_sweep", "achieved": achieved, "peak": hbm, "unit": "GB/s",
