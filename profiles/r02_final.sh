@@ -1,4 +1,4 @@
-# round 2, final evidence: bench lines (config4-geom with plates; config4-count), the launch list of
+# round 2, final evidence (re-run after the own-particle select): bench lines (config4-geom with plates; config4-count), the launch list of
 # the bench's timed window and one ncu --set full capture of k_sweep inside it (TMA-staged kernel)
 set -x
 mkdir -p gpurun_out
