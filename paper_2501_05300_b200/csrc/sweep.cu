@@ -8,8 +8,9 @@
 //   * cross-tile particle pairs: one item in each of the two tiles (each evaluates the contact
 //     from the same canonical operands, bit-identically; each keeps only its own body's share);
 //   * wall / plate contacts: one item, owned by the particle.
-// A tile's items are stored contiguously, grouped by owner (warp w's 32 particles' items form
-// one range), so records move with coalesced 256-bit accesses:
+// A tile's items are stored contiguously, grouped by owner (each warp takes a range of whole
+// particles, plan k_plan_warps), so records move with coalesced 256-bit accesses; the tile's
+// particle states land in shared memory by TMA bulk copies on an mbarrier:
 //   CRec 32 B per item: n (a -> b) and delta, fp64 (the item's meta word in n's low bits)
 //   PRec 64 B per item: P_n, P_t (3), P_r (3) and the stage's SPOOK bias b, fp64
 // Everything else the contact row needs is derived from the radii: R* = r_a r_b/(r_a + r_b),
