@@ -36,6 +36,20 @@ static_assert(TT % 32 == 0 && TT <= 512, "tile: whole warps, owner index in 9 bi
 static_assert(SLOT_CAP <= (int)IT_SLOT_MASK + 1 && SLOT_CAP < 65536, "slot index: 12 bits in the meta word");
 constexpr int FX_EL = 42, FX_EA = 36;    // fixed-point exponents (linear, angular)
 
+// DEM_CHECK builds (tests only, never shipped): index invariants of the tile plan trap
+#ifdef DEM_CHECK
+#define SW_CHECK(c, what)                                                                          \
+    do {                                                                                           \
+        if (!(c)) {                                                                                \
+            printf("k_sweep check failed: %s (tile %lld thread %d)\n", what, (long long)blockIdx.x, \
+                   (int)threadIdx.x);                                                              \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define SW_CHECK(c, what) ((void)0)
+#endif
+
 __device__ __forceinline__ double4 cat2(const double2 a, const double2 b) { return make_double4(a.x, a.y, b.x, b.y); }
 
 // ------------------------------------------------------------------ fixed point
@@ -287,6 +301,7 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
         const bool valid = k < k1;
         // segments of the chunk: runs of equal owner (items are grouped by owner)
         const int o = valid ? crec_owner(cr) : -1;
+        SW_CHECK(!valid || o < np, "owner inside the tile");
         const int op = __shfl_up_sync(0xffffffffu, o, 1);
         const unsigned smask = __ballot_sync(0xffffffffu, valid && (lane == 0 || op != o));
         const unsigned le = smask & (0xffffffffu >> (31 - lane));
@@ -311,9 +326,10 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
                 mr = sp.mu_r;
                 int ia = -1, ib = -1;      // shared-memory slots of bodies a and b
                 int64_t g = -1;
-                if (intra) { pl = (int)(meta & IT_LOC); ia = o; ib = pl; }       // owned by body a
+                if (intra) { pl = (int)(meta & IT_LOC); ia = o; ib = pl; SW_CHECK(pl < np && pl != o, "intra partner"); }
                 else {
                     g = (int64_t)(meta & IT_IDX);
+                    SW_CHECK(g < N && g != p0 + o, "cross partner index");
                     const int64_t l = g - p0;
                     if (l >= 0 && l < np) { ia = isB ? (int)l : o; ib = isB ? o : (int)l; g = -1; }
                 }
@@ -348,6 +364,7 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
                 const double2 sg = sSig[pl];
                 const Fx6 ot = fx6(c.L, share_b(lb, c.nxdPt, c.dPr), sg.x, sg.y, bad);
                 const int sl = (int)((meta >> IT_SLOT_SHIFT) & IT_SLOT_MASK);
+                SW_CHECK(sl < SLOT_CAP, "slot capacity");
                 sSlot[3 * sl] = make_longlong2(ot.v[0], ot.v[1]);
                 sSlot[3 * sl + 1] = make_longlong2(ot.v[2], ot.v[3]);
                 sSlot[3 * sl + 2] = make_longlong2(ot.v[4], ot.v[5]);
@@ -399,6 +416,7 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
             long long a[6];
 #pragma unroll
             for (int f = 0; f < 6; f++) a[f] = sAcc[f][t];
+            SW_CHECK(is + ic <= (uint32_t)SLOT_CAP, "incoming slots");
             for (uint32_t s = is; s < is + ic; s++) {
                 const longlong2 x0 = sSlot[3 * s], x1 = sSlot[3 * s + 1], x2 = sSlot[3 * s + 2];
                 const long long x[6] = {x0.x, x0.y, x1.x, x1.y, x2.x, x2.y};

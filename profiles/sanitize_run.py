@@ -9,7 +9,8 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 from paper_2501_05300_b200 import dem  # noqa: E402
 
-bed = synth.random_cloud(1500, (0.002, 0.002, 0.002), (0.058, 0.058, 0.03), 1.0e-3, 3.0e-3, 5, v_scale=0.05, w_scale=3.0,
+N = int(sys.argv[1]) if len(sys.argv) > 1 else 1500    # 1501: a ragged last tile of odd size
+bed = synth.random_cloud(N, (0.002, 0.002, 0.002), (0.058, 0.058, 0.03), 1.0e-3, 3.0e-3, 5, v_scale=0.05, w_scale=3.0,
                          loguniform=True)
 b = dem.Bed(bed.x, bed.r, bed.v, bed.w, bed.gid, solver=dict(dt=2e-5, n_iter=20),
             box=dict(lo=(0, 0, 0), hi=(0.06, 0.06, 0.06)))
