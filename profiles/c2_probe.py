@@ -1,6 +1,6 @@
 """c2-mini plate behaviour on the GPU under staggered (0) and monolithic (1) plate coupling:
 plate contact count, vertical position and the shear-force curve by windows of 2500 steps.
-Settles the bed with the oracle (as tests/test_gpu_curves_mini.py does)."""
+Settles the bed with the oracle (as tests/test_gpu_z_curves_mini.py does)."""
 import os
 import sys
 

@@ -2,7 +2,7 @@
 shear stress-displacement curves agree within 2 % RMS normalised error").  Test infrastructure:
 the protocol definitions shared by the ORACLE side (tests/fixtures/make_curves_mini.py, run once
 on the CPU; it writes the settled beds and the oracle curves under tests/golden/) and the GPU
-side (tests/test_gpu_curves_mini.py).  Nothing here holds arithmetic of the method: it places
+side (tests/test_gpu_z_curves_mini.py).  Nothing here holds arithmetic of the method: it places
 spheres (synth), places a plate, and filters curves.
 
 c1-mini (config 1 shape, P:205-217 pressure-sinkage): 0.1 x 0.1 x 0.075 m box, 2 mm spheres over

@@ -5,6 +5,8 @@ position, per step) to tests/golden/curves_mini_<kind>_<seed>.npz with a digest 
 state (the GPU test re-settles with the same oracle and checks the digest).  Produced only by
 oracle/ code; run once on the CPU (OpenMP sweeps):
     python tests/fixtures/make_curves_mini.py [kind] [seed]
+and the settled beds the GPU test starts from (tests/golden/curves_mini_<kind>_<seed>_settled.npz):
+    python tests/fixtures/make_curves_mini.py [kind] [seed] --settled-only
 """
 import hashlib
 import os
@@ -19,13 +21,35 @@ import oracle as O  # noqa: E402
 from tests import curves_mini as CM  # noqa: E402
 
 
-def settled(kind, seed):
-    """the bed settled under gravity by the oracle (cell-list mode), with its contact history"""
+def settled_path(kind, seed):
+    return os.path.join(ROOT, "tests", "golden", f"curves_mini_{kind}_{seed}_settled.npz")
+
+
+def settled(kind, seed, use_cache=True):
+    """the bed settled under gravity by the oracle (cell-list mode), with its contact history.
+    The settled state is cached under tests/golden (written by this script from the oracle, see
+    save_settled) so that the GPU test does not re-run the oracle's settling on the GPU box; the
+    test checks its digest against the one stored with the oracle curve."""
     b = CM.make_bed(kind, seed)
+    path = settled_path(kind, seed)
+    if use_cache and os.path.exists(path):
+        z = np.load(path)
+        W = O.OracleWorld(z["x"], z["v"], z["w"], z["r"], z["gid"],
+                          walls=O.box_walls(b.box_lo, b.box_hi, mask=CM.WALL_MASK), time=float(z["time"]))
+        W.hist = z["hist"].astype(O.CONTACT_DTYPE)
+        return b, W
     O.set_binning(True)
     W = O.OracleWorld(b.x, b.v, b.w, b.r, b.gid, walls=O.box_walls(b.box_lo, b.box_hi, mask=CM.WALL_MASK))
     W.step(O.make_params(h=CM.SETTLE["h"], n_it=CM.SETTLE["n_it"]), CM.SETTLE["steps"])
     return b, W
+
+
+def save_settled(kind, seed):
+    """settle with the oracle (never from the cache) and store the state with its digest"""
+    b, W = settled(kind, seed, use_cache=False)
+    np.savez_compressed(settled_path(kind, seed), x=W.x, v=W.v, w=W.w, r=W.r, gid=W.gid, hist=W.hist,
+                        time=W.time, digest=digest(W))
+    print("wrote", settled_path(kind, seed), digest(W), flush=True)
 
 
 def digest(W):
@@ -69,9 +93,13 @@ def run(kind, seed):
 
 
 if __name__ == "__main__":
-    kinds = [sys.argv[1]] if len(sys.argv) > 1 else list(CM.KINDS)
-    seeds = [int(sys.argv[2])] if len(sys.argv) > 2 else list(CM.SEEDS)
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    kinds = [args[0]] if len(args) > 0 else list(CM.KINDS)
+    seeds = [int(args[1])] if len(args) > 1 else list(CM.SEEDS)
     O.set_threads(int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1)))
     for k in kinds:
         for sd in seeds:
-            run(k, sd)
+            if "--settled-only" in sys.argv:
+                save_settled(k, sd)
+            else:
+                run(k, sd)

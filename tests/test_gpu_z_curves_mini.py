@@ -12,10 +12,12 @@ onward, so single-seed curves differ by their fluctuations; the per-seed errors 
 recorded (profiles/r02_curves_mini.txt) beside the ensemble figure.
 
 The oracle side ran once on the CPU (tests/fixtures/make_curves_mini.py, OpenMP oracle) and
-stored its curves; this test re-settles each bed with the same oracle (checking the digest of
-the settled state against the stored one: both sides start from the identical state and
-contact history), runs the GPU through the C-ABI, and compares the 2 ms moving averages: RMS of
-the difference over the oracle curve's maximum, mean over the seeds <= 2 %.
+stored its curves and the oracle-settled beds; this test loads each settled bed (or re-settles it
+with the oracle when the cache is absent), checks the digest of the settled state against the one
+stored with the oracle curve (both sides start from the identical state and contact history),
+runs the GPU through the C-ABI, and compares the 2 ms moving averages: RMS of the difference of the
+seed-averaged curves over the oracle mean curve's maximum <= 2 %.  (The file name sorts last: the
+long acceptance runs come after the parity suites under `pytest -x`.)
 """
 import os
 
