@@ -990,7 +990,12 @@ static dem_status item_sweeps(dem_ctx *ctx, int stage, int n, const SolveParams 
                            ctx->it_rec, ctx->it_P[it & 1], ctx->it_P[(it & 1) ^ 1], ctx->db, sp, s);
     };
     ctx->launches += n;
-    if (ctx->tp || n < 2 || getenv("DEM_NO_GRAPHS")) {
+    // decomposed contexts: the loop (sweep, halo pack, grouped NCCL send/recv, unpack) is captured
+    // only over a graph-safe transport without a monolithic plate (whose per-sweep allreduce
+    // synchronises the host), and only on request (DEM_GRAPH_NCCL=1): NCCL inside graphs has not
+    // been validated on a multi-GPU box here
+    const bool capturable = !ctx->tp || (ctx->tp->graph_safe() && !hub && getenv("DEM_GRAPH_NCCL"));
+    if (!capturable || n < 2 || getenv("DEM_NO_GRAPHS")) {
         for (int it = 0; it < n; it++) {
             one(it, ctx->cur);
             if (hub) TRY(plate_hub(ctx, true, ctx->it_P[it & 1], ctx->it_P[(it & 1) ^ 1], 0));
@@ -1002,8 +1007,10 @@ static dem_status item_sweeps(dem_ctx *ctx, int stage, int n, const SolveParams 
     // key: everything the captured launches bake in
     const void *ptrs[] = {ctx->vel[0], ctx->vel[1], ctx->ang[0], ctx->ang[1], ctx->pl.rad, ctx->pl.istart, ctx->pl.pin,
                           ctx->it_rec, ctx->it_P[0], ctx->it_P[1], ctx->db, ctx->it_plist, ctx->pl.item_c, ctx->geo,
-                          ctx->hub_acc};
-    const int64_t ints[] = {N, n, c0, hub ? ctx->n_it_plist : -1};
+                          ctx->hub_acc, ctx->hs[0], ctx->hs[1], ctx->hr[0], ctx->hr[1], ctx->send_idx[0],
+                          ctx->send_idx[1], ctx->recv_idx[0], ctx->recv_idx[1]};
+    const int64_t ints[] = {N, n, c0, hub ? ctx->n_it_plist : -1, ctx->n_send[0], ctx->n_send[1], ctx->n_recv[0],
+                            ctx->n_recv[1]};
     std::vector<unsigned char> key(sizeof(ptrs) + sizeof(ints) + sizeof(SolveParams));
     std::memcpy(key.data(), ptrs, sizeof(ptrs));
     std::memcpy(key.data() + sizeof(ptrs), ints, sizeof(ints));
@@ -1022,15 +1029,23 @@ static dem_status item_sweeps(dem_ctx *ctx, int stage, int n, const SolveParams 
         if (g.exec) { cudaGraphExecDestroy(g.exec); g.exec = nullptr; }
         cudaGraph_t graph = nullptr;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        for (int it = 0; it < n; it++) {
+        dem_status st = DEM_OK;
+        for (int it = 0; it < n && st == DEM_OK; it++) {
             one(it, c0 ^ (it & 1));
             if (hub) {
                 launch_plate_hub_items(ctx->n_it_plist, ctx->it_plist, ctx->pl, ctx->geo, ctx->it_rec, ctx->it_P[it & 1],
                                        ctx->it_P[(it & 1) ^ 1], ctx->hub_acc, s);
                 launch_plate_kick(ctx->db, ctx->hub_acc, sp.h, 0, s);
             }
+            const int a = c0 ^ (it & 1) ^ 1;   // the velocities this sweep wrote
+            st = halo(ctx, ctx->vel[a], ctx->ang[a]);
         }
-        CK(cudaStreamEndCapture(s, &graph));
+        const cudaError_t ce = cudaStreamEndCapture(s, &graph);
+        if (st != DEM_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return st;
+        }
+        CK(ce);
         CK(cudaGraphInstantiate(&g.exec, graph, 0));
         cudaGraphDestroy(graph);
         g.key = key;

@@ -95,6 +95,7 @@ struct NcclTransport : Transport {
     {
         return allreduce<double>(v, n, op, s, err, dbuf, ncclFloat64);
     }
+    bool graph_safe() const override { return true; }   // grouped ncclSend/ncclRecv: stream-ordered
     bool allreduce_i64(long long *v, int n, int op, cudaStream_t s, std::string &err) override
     {
         return allreduce<long long>(v, n, op, s, err, ibuf, ncclInt64);

@@ -30,6 +30,9 @@ struct Transport {
     // host-side reductions (op 0 sum, 1 max) over all ranks; the caller has synchronised s
     virtual bool allreduce_f64(double *v, int n, int op, cudaStream_t s, std::string &err) = 0;
     virtual bool allreduce_i64(long long *v, int n, int op, cudaStream_t s, std::string &err) = 0;
+    // exchange() only enqueues stream-ordered work (no host synchronisation): it can be captured
+    // in a CUDA graph
+    virtual bool graph_safe() const { return false; }
 };
 
 Transport *make_nccl_transport(int rank, int G, const void *unique_id, std::string &err);

@@ -93,12 +93,17 @@ def test_loopback_plate_reaction_summed_over_ranks():
         assert np.array_equal(out["state"][k], ref["state"][k]), k
 
 
-@pytest.mark.parametrize("transport", ["nccl", "loopback"])
-def test_single_rank_transport_selftest_bit_identical(transport):
+@pytest.mark.parametrize("transport", ["nccl", "nccl_graph", "loopback"])
+def test_single_rank_transport_selftest_bit_identical(transport, monkeypatch):
     """world_size 1 over a real transport (NCCL communicator of one rank, or a loopback group of
     one) runs the decomposed code path -- ownership pass, band exchange with no neighbours,
-    allreduces -- and must reproduce the undecomposed context bit for bit."""
+    allreduces -- and must reproduce the undecomposed context bit for bit.  nccl_graph: the
+    decomposed sweep loop (sweeps, halo pack, grouped NCCL send/recv, unpack) captured in a CUDA
+    graph (DEM_GRAPH_NCCL=1)."""
     D = dem()
+    if transport == "nccl_graph":
+        monkeypatch.setenv("DEM_GRAPH_NCCL", "1")
+        transport = "nccl"
     bed, box = drifting_bed(drift=1.0, seed=7)
     solver = dict(dt=2e-5, n_iter=20)
     ref = single(bed, 6, solver, box)
