@@ -1,5 +1,5 @@
 // gs.cu -- coloured projected Gauss-Seidel ordering of the contact solve (the paper
-// solves the MCP with PGS), the alternative to the Jacobi sweep of k_sweep_t2.
+// solves the MCP with PGS), the alternative to the Jacobi sweep k_sweep (sweep.cu).
 //
 // Colouring: two contacts conflict if they share a particle.  Priority pi(c) = SplitMix64 of the
 // contact's public key (ties: smaller key first).  Jones-Plassmann rounds: an uncoloured contact
