@@ -1809,6 +1809,7 @@ dem_status dem_bench_sweeps(dem_ctx *ctx, int32_t variant, int32_t n, double *ms
     if (ctx->sol.ordering != 0) { ctx->err = "dem_bench_sweeps times the Jacobi sweep (ordering 0)"; return DEM_ERR_INVALID; }
     const int64_t N = ctx->N;
     cudaStream_t s = ctx->s;
+    if (getenv("DEM_DEBUG")) fprintf(stderr, "dem_bench_sweeps: %lld particles, %lld items\n", (long long)N, (long long)ctx->n_items);
     item_pack(ctx->n_items, ctx->pl, ctx->geo, ctx->cdel, ctx->row, ctx->Pfa, ctx->Pfb, ctx->it_rec, ctx->it_P[0], s);
     double4 *vb[2] = {ctx->vel[ctx->cur ^ 1], ctx->vel_prev}, *wb[2] = {ctx->ang[ctx->cur ^ 1], ctx->ang_prev};
     const double4 *vi = ctx->vel[ctx->cur], *wi = ctx->ang[ctx->cur];

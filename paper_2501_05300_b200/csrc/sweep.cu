@@ -448,6 +448,11 @@ void launch_sweep_items(bool impact, int64_t N, const double4 *vin, const double
     static const bool attr = [] {
         cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
         cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn);
+        // shared-memory carveout (percent of the unified L1/shared capacity; unset: the driver's choice)
+        if (const char *cv = getenv("DEM_SWEEP_CARVEOUT")) {
+            cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+            cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(cv));
+        }
         if (getenv("DEM_DEBUG")) {
             int per = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sweep<false>, TT, dyn);
