@@ -102,6 +102,9 @@ void launch_load_state(int64_t N, const double *x, const double *r, const double
 #ifndef SWEEP_MINB
 #define SWEEP_MINB 2
 #endif
+#ifndef SWEEP_SIG16
+#define SWEEP_SIG16 0            // 1: scale exponents as int16 pairs and bad flags as a bitmask (-4 KB of shared memory per CTA)
+#endif
 #ifndef SWEEP_TMA
 #define SWEEP_TMA 1              // tile staging by TMA bulk copies on an mbarrier (0: per-thread cp.async)
 #endif

@@ -60,6 +60,8 @@ __device__ __forceinline__ int fx_exp(double w, uint32_t c)
     return (int)((__double_as_longlong(w) >> 52) & 0x7FF) - 1023 - (31 - __clz((int)c));
 }
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
+// the (linear, angular) scales from their exponents packed as two int16 (SWEEP_SIG16)
+__device__ __forceinline__ double2 sig2(int x) { return make_double2(pow2((int)(short)(x & 0xFFFF)), pow2(x >> 16)); }
 // Fixed-point value of x s (s a power of two, so x s is exact), kept as raw bits: t = x s + 1.5 2^52
 // rounds x s to an integer exactly (RN-even, like llrint) whenever |x s| <= 2^51, and then the
 // bit pattern of t is round(x s) + FX_MAGIC_BITS.  Sums of raw patterns are taken mod 2^64 and
@@ -253,9 +255,21 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
     extern __shared__ double2 sDyn[];
     StageBuf &B = *reinterpret_cast<StageBuf *>(sDyn);
     longlong2 *sSlot = reinterpret_cast<longlong2 *>(&B + 1);   // [SLOT_CAP][3]
+#if SWEEP_SIG16
+    __shared__ int sSig[TT];              // fixed-point scale exponents (linear: low int16, angular: high)
+    __shared__ long long sAcc[6][TT];
+    __shared__ unsigned sBad[NWT];        // one bit per particle: a share out of range (poisons it)
+#define SIG(i) sig2(sSig[i])
+#define BAD_SET(i) atomicOr(&sBad[(i) >> 5], 1u << ((i) & 31))
+#define BAD_GET(i) ((sBad[(i) >> 5] >> ((i) & 31)) & 1u)
+#else
     __shared__ double2 sSig[TT];          // fixed-point scales (linear, angular) of the particle
     __shared__ long long sAcc[6][TT];
     __shared__ int sBad[TT];
+#define SIG(i) sSig[i]
+#define BAD_SET(i) atomicOr(&sBad[i], 1)
+#define BAD_GET(i) sBad[i]
+#endif
     const int t = threadIdx.x, lane = t & 31, w = t >> 5;
     const int64_t tile = blockIdx.x;
     const int64_t p0 = tile * TT;
@@ -286,12 +300,20 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
     const double *sR = B.r;
     if (t < np) {
         const uint32_t c = (B.is[t + 1] - B.is[t]) + (B.in[t] >> 16);
+#if SWEEP_SIG16
+        sSig[t] = c ? (((FX_EL + fx_exp(SV(t).w, c)) & 0xFFFF) | ((FX_EA + fx_exp(SW(t).w, c)) << 16)) : 0;
+#else
         sSig[t] = c ? make_double2(pow2(FX_EL + fx_exp(SV(t).w, c)), pow2(FX_EA + fx_exp(SW(t).w, c)))
                     : make_double2(0.0, 0.0);
+#endif
     }
 #pragma unroll
     for (int f = 0; f < 6; f++) sAcc[f][t] = 0;
+#if SWEEP_SIG16
+    if (t < NWT) sBad[t] = 0u;
+#else
     sBad[t] = 0;
+#endif
     __syncthreads();
     // one chunk of 32 items from records (cr, q).  (Unrolling the loop twice, so that the next
     // chunk's records land in a second register set without copies, measured slower: 3.00 ms vs
@@ -361,21 +383,21 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
             // shares: body a gets -(L), -(la n x dPt + dPr); body b gets +L, -lb n x dPt + dPr
             bool bad = false;
             if (intra) {   // body b of an intra-tile contact: its slot (stored first: fewer live registers)
-                const double2 sg = sSig[pl];
+                const double2 sg = SIG(pl);
                 const Fx6 ot = fx6(c.L, share_b(lb, c.nxdPt, c.dPr), sg.x, sg.y, bad);
                 const int sl = (int)((meta >> IT_SLOT_SHIFT) & IT_SLOT_MASK);
                 SW_CHECK(sl < SLOT_CAP, "slot capacity");
                 sSlot[3 * sl] = make_longlong2(ot.v[0], ot.v[1]);
                 sSlot[3 * sl + 1] = make_longlong2(ot.v[2], ot.v[3]);
                 sSlot[3 * sl + 2] = make_longlong2(ot.v[4], ot.v[5]);
-                if (bad) atomicOr(&sBad[pl], 1);
+                if (bad) BAD_SET(pl);
             }
-            const double2 ss = sSig[o];
+            const double2 ss = SIG(o);
             const d3 Ls = isB ? c.L : mk(-c.L.x, -c.L.y, -c.L.z);
             const d3 As = isB ? share_b(lb, c.nxdPt, c.dPr) : share_a(la, c.nxdPt, c.dPr);
             const Fx6 me6 = fx6(Ls, As, ss.x, ss.y, bad);
             v0 = me6.v[0]; v1 = me6.v[1]; v2 = me6.v[2]; v3 = me6.v[3]; v4 = me6.v[4]; v5 = me6.v[5];
-            if (bad) atomicOr(&sBad[o], 1);
+            if (bad) BAD_SET(o);
         }
         // segmented sum of the self shares (items are grouped by owner): exact int64
         const int dist = valid ? lane - sstart : 0;
@@ -427,18 +449,21 @@ __global__ void __launch_bounds__(TT, SWEEP_MINB)
 #pragma unroll
             for (int f = 0; f < 6; f++) a[f] = (long long)((unsigned long long)a[f] - mc);
             // body update with the real masses (1/m = (c/m)/c): the mass-splitting average
-            const double2 sg = sSig[t];
+            const double2 sg = SIG(t);
             const double im = V.w / (double)cnt, iI = W.w / (double)cnt;
             const double qL = (1.0 / sg.x) * im, qA = (1.0 / sg.y) * iI;   // 1/s exact (powers of two)
             V.x += (double)a[0] * qL; V.y += (double)a[1] * qL; V.z += (double)a[2] * qL;
             W.x += (double)a[3] * qA; W.y += (double)a[4] * qA; W.z += (double)a[5] * qA;
-            if (sBad[t]) { V.x = __longlong_as_double(0x7FF8000000000000LL); }
+            if (BAD_GET(t)) { V.x = __longlong_as_double(0x7FF8000000000000LL); }
         }
         st4g(&vout[p0 + t], V);
         st4g(&wout[p0 + t], W);
     }
 }
 
+#undef SIG
+#undef BAD_SET
+#undef BAD_GET
 void launch_sweep_items(bool impact, int64_t N, const double4 *vin, const double4 *win, const double *rad, double4 *vout,
                         double4 *wout, const SweepPlan &pl, const CRec *rec, const PRec *Pin, PRec *Pout,
                         const DevBoundary *bnd, const SolveParams &sp, cudaStream_t s)
